@@ -1,0 +1,170 @@
+"""Seeded synthetic inputs for BASELINE.json configs C1-C5 (test infrastructure).
+
+None of the five families comes from the reference's generators
+(generators.py:70-257 builds different families); the recipes follow
+BASELINE.json ``configs`` and SURVEY.md section 8(d).  Every family exposes a
+per-tile generator so the largest configs (C3: 8.6 GB dense, C5: 34 GB) never
+materialise the dense matrix on the host; the same float64 tiles feed both
+the oracle and the GPU path.
+
+The product package has its own copy of these recipes on the device
+(``paper_2208_06194_b200.configs``) for the benchmark; bitwise equality of
+tiles between the two is not required there (the bench only times the
+factorization), while parity tests always feed the oracle's tiles to both.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .blr import weak_map
+
+
+@dataclass(frozen=True)
+class Config:
+    name: str
+    family: str
+    n: int
+    b: int
+    eps: float
+    methods: tuple
+    seed: int = 0
+
+
+CONFIGS = {
+    "C1": Config("C1", "random16", 2048, 256, 1e-8, ("mgs", "blocked-hh", "tiled-hh")),
+    "C2": Config("C2", "laplace", 16384, 256, 1e-8, ("blocked-hh",)),
+    "C3": Config("C3", "expcov", 32768, 512, 1e-8, ("tiled-hh",)),
+    "C4": Config("C4", "invpoisson", 16384, 256, 1e-10, ("mgs", "blocked-hh", "tiled-hh")),
+    "C5": Config("C5", "laplace", 65536, 1024, 1e-8, ("tiled-hh",)),
+}
+
+
+# --- C1: random BLR with rank-16 geometric spectrum --------------------------
+
+
+def random16_dense(n: int, b: int, seed: int = 0, rank: int = 16) -> np.ndarray:
+    """Diagonal tiles N(0,1); off-diagonal U diag(s) V^T, U,V = Q of N(0,1),
+    s_i = 10^(-i/2), i = 0..rank-1; tiles drawn in row-major order."""
+    rng = np.random.default_rng(seed)
+    p = n // b
+    s = 10.0 ** (-np.arange(rank) / 2.0)
+    out = np.empty((n, n))
+    for i in range(p):
+        for j in range(p):
+            if i == j:
+                t = rng.standard_normal((b, b))
+            else:
+                u = np.linalg.qr(rng.standard_normal((b, rank)))[0]
+                v = np.linalg.qr(rng.standard_normal((b, rank)))[0]
+                t = (u * s) @ v.T
+            out[i * b:(i + 1) * b, j * b:(j + 1) * b] = t
+    return out
+
+
+# --- C2 / C5: Laplace single-layer kernel on the unit circle ----------------
+
+
+class Laplace:
+    """A_ij = -log|x_i - x_j| / (2 pi), x_i equispaced on the unit circle;
+    A_ii = 1 + (1/n) sum_{j != i} |A_ij|.  Circulant: A_ij = g[(i - j) mod n],
+    |x_i - x_j| = 2 |sin(pi (i - j) / n)|."""
+
+    def __init__(self, n: int):
+        self.n = n
+        d = np.arange(n)
+        g = np.zeros(n)
+        g[1:] = -np.log(2.0 * np.abs(np.sin(np.pi * d[1:] / n))) / (2.0 * np.pi)
+        g[0] = 1.0 + np.sum(np.abs(g[1:])) / n
+        self.g = g
+
+    def tile(self, i0: int, j0: int, rows: int, cols: int) -> np.ndarray:
+        r = np.arange(i0, i0 + rows)[:, None]
+        c = np.arange(j0, j0 + cols)[None, :]
+        return self.g[(r - c) % self.n]
+
+
+# --- C3: exponential covariance on Morton-sorted random points ---------------
+
+
+def morton_sort(x: np.ndarray, bits: int = 21) -> np.ndarray:
+    """Stable argsort by 2-D Morton key (x bits at even, y bits at odd positions)."""
+    q = np.clip((x * (1 << bits)).astype(np.int64), 0, (1 << bits) - 1)
+    key = np.zeros(len(x), dtype=np.int64)
+    for t in range(bits):
+        key |= ((q[:, 0] >> t) & 1) << (2 * t)
+        key |= ((q[:, 1] >> t) & 1) << (2 * t + 1)
+    return np.argsort(key, kind="stable")
+
+
+class ExpCov:
+    """A_ij = exp(-|x_i - x_j| / ell) + 1e-4 delta_ij, x uniform in [0,1]^2."""
+
+    def __init__(self, n: int, seed: int = 0, ell: float = 0.1, nugget: float = 1e-4):
+        x = np.random.default_rng(seed).uniform(0.0, 1.0, (n, 2))
+        self.x = np.ascontiguousarray(x[morton_sort(x)])
+        self.ell, self.nugget = ell, nugget
+
+    def tile(self, i0: int, j0: int, rows: int, cols: int) -> np.ndarray:
+        a = self.x[i0:i0 + rows]
+        c = self.x[j0:j0 + cols]
+        dx = a[:, 0:1] - c[None, :, 0]
+        dy = a[:, 1:2] - c[None, :, 1]
+        t = np.exp(-np.sqrt(dx * dx + dy * dy) / self.ell)
+        for d in range(max(i0, j0), min(i0 + rows, j0 + cols)):
+            t[d - i0, d - j0] += self.nugget
+        return t
+
+
+# --- C4: inverse 2-D Dirichlet Laplacian in Morton order ---------------------
+
+
+def invpoisson_dense(g: int) -> np.ndarray:
+    """L = (T (x) I + I (x) T) / h^2, T = tridiag(-1, 2, -1), h = 1/(g+1);
+    returns L^{-1} with rows/cols permuted to the Morton order of the grid,
+    through the sine eigenbasis: L^{-1} = W diag(h^2 / (l_a + l_b)) W^T."""
+    h = 1.0 / (g + 1)
+    k = np.arange(1, g + 1)
+    s = np.sqrt(2.0 / (g + 1)) * np.sin(np.outer(k, k) * np.pi / (g + 1))
+    lam = 2.0 - 2.0 * np.cos(k * np.pi / (g + 1))
+    ix, iy = np.meshgrid(np.arange(g), np.arange(g), indexing="ij")
+    ix, iy = ix.ravel(), iy.ravel()
+    pts = np.stack([ix, iy], axis=1).astype(float) / g
+    order = morton_sort(pts, bits=max(1, int(np.ceil(np.log2(g)))))
+    ix, iy = ix[order], iy[order]
+    w = s[ix][:, :, None] * s[iy][:, None, :]  # n x g x g: W[p, (a,b)]
+    w = w.reshape(len(ix), g * g)
+    d = (h * h) / (lam[:, None] + lam[None, :]).ravel()
+    out = (w * d) @ w.T
+    return 0.5 * (out + out.T)
+
+
+# --- common ------------------------------------------------------------------
+
+
+def tile_source(cfg: Config, n: int | None = None):
+    """(tile(i0, j0, rows, cols) callable, n) for a config (optionally rescaled n)."""
+    n = n or cfg.n
+    if cfg.family == "laplace":
+        return Laplace(n).tile, n
+    if cfg.family == "expcov":
+        return ExpCov(n, cfg.seed).tile, n
+    if cfg.family == "random16":
+        d = random16_dense(n, cfg.b, cfg.seed)
+        return (lambda i0, j0, r, c: d[i0:i0 + r, j0:j0 + c].copy()), n
+    if cfg.family == "invpoisson":
+        g = int(round(np.sqrt(n)))
+        d = invpoisson_dense(g)
+        return (lambda i0, j0, r, c: d[i0:i0 + r, j0:j0 + c].copy()), n
+    raise ValueError(cfg.family)
+
+
+def dense(cfg: Config, n: int | None = None) -> np.ndarray:
+    tile, n = tile_source(cfg, n)
+    return tile(0, 0, n, n)
+
+
+def weak(n: int, b: int) -> np.ndarray:
+    return weak_map(n // b, n // b)
