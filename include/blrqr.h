@@ -1,0 +1,176 @@
+/*
+ * blrqr.h — C ABI of libblrqr.so, the sm_100a BLR-QR engine.
+ *
+ * The reference (`blrqr`, pure Python + numpy/LAPACK) has no FFI; its
+ * "operator API" is the set of Python functions in blrqr.lowrank,
+ * blrqr.kernels, blrqr.factorize and blrqr.scheduler.  Each entry
+ * below replaces the numeric core of one of those functions; the Python
+ * package paper_2208_06194_b200 binds them with ctypes and keeps the
+ * reference names, argument meaning and error behaviour.
+ *
+ * Conventions
+ *  - Every pointer is a DEVICE pointer (owned by the caller, e.g. a torch
+ *    tensor); the library never allocates persistent memory and never frees.
+ *  - FP64, column-major, leading dimension = row count unless stated.
+ *  - `ws` is caller-provided scratch of blrqr_workspace_doubles(...) doubles
+ *    per CTA times `nctas`.
+ *  - `status` is one device int, OR-ed with BLRQR_ST_* bits by the kernels;
+ *    `flops` is BLRQR_FLOP_KINDS device uint64 counters (reference flop
+ *    model, flops.py:28-55, per kind).
+ *  - Every entry is stream-ordered on `stream` (a cudaStream_t, NULL =
+ *    legacy default) and returns 0, or a negative code for a bad argument
+ *    (the shim raises ValueError), or a CUDA error code + 1000.
+ */
+#ifndef BLRQR_H
+#define BLRQR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BLRQR_ST_RANK_OVERFLOW 1  /* a result rank exceeded the slab capacity */
+#define BLRQR_ST_ARENA_OVERFLOW 2 /* per-CTA workspace too small */
+#define BLRQR_ST_NONFINITE 4
+#define BLRQR_ST_MGS_COLLAPSE 8   /* RankDeficiencyWarning (kernels.py:214-221) */
+#define BLRQR_ST_BAD_KIND 16      /* e.g. low-rank diagonal block */
+#define BLRQR_ST_BAD_ARG 32
+
+/* flop-model kinds (flops.add sites): compress, rounded_add, expand, lr_mul,
+ * gemm, panel_qr, apply_wy, update_qr, apply_tp */
+#define BLRQR_FLOP_KINDS 9
+
+/* Device-resident BLR grid (replaces blrqr.core.BlrMatrix, core.py:135-189).
+ * Cell (i, j) is row-major index c = i*q + j.  Dense cells: b x b data at
+ * pool + off_u[c].  Low-rank cells: U (b x cap) at pool + off_u[c] and
+ * V (b x cap) at pool + off_v[c], rank in rank[c]. */
+typedef struct {
+  int p, q, b, cap;
+  const unsigned char* lowrank; /* p*q kind map (1 = low-rank cell) */
+  int* rank;                    /* p*q ranks (dense cells: ignored) */
+  double* pool;
+  const int64_t* off_u;
+  const int64_t* off_v;
+} blrqr_grid;
+
+/* Householder reflector store.
+ *  tiled (TileReflectorStore, factorize.py:159-170):
+ *    diag[k]: Y = pool + y_off[k*q+k] (b x b, unit lower, explicit), T at t_off[k*q+k]
+ *    updates[(i,k)]: T at t_off[i*q+k]; Ytilde low-rank = (U_ik slab, V_ik slab
+ *      holding Y^T) with rank yrank[i*q+k], or dense Y at y_off[i*q+k].
+ *  blocked (ReflectorColumn, factorize.py:146-156):
+ *    T_k at t_off[k*q+k]; entry (k,k) dense Y at y_off[k*q+k]; entries (i,k),
+ *    i > k, as for tiled updates.
+ *  Offsets are -1 where unused. */
+typedef struct {
+  double* pool;
+  const int64_t* y_off;
+  const int64_t* t_off;
+  int* yrank;
+} blrqr_refl;
+
+/* one tiled task: kind 0 DiagQR(k), 1 ApplyBlockReflector(k,j),
+ * 2 UpdateQR(k,i), 3 ApplyTrapReflector(k,i,j) (scheduler.py:61-70) */
+typedef struct {
+  int kind, k, i, j;
+} blrqr_task;
+
+/* ---- sizing / info ---------------------------------------------------- */
+int blrqr_version(void);
+/* doubles of per-CTA scratch the kernels need for block size b, capacity cap */
+int64_t blrqr_workspace_doubles(int b, int cap, int max_panel_rows);
+/* recommended number of resident CTAs (2 per SM) on the current device */
+int blrqr_default_ctas(void);
+
+/* ---- low-rank arithmetic (lowrank.py) ---------------------------------- */
+/* Batched rounded addition (lowrank.rounded_add, lowrank.py:173-221).
+ * Problem t: A = (ua[t] m x ra[t], va[t] n x ra[t]), B likewise; output
+ * factors into uo[t] (m x cap), vo[t] (n x cap), rank into ro[t].  ra/rb/ro are
+ * device int arrays; ua.. are device arrays of device pointers. */
+int blrqr_rounded_add_batched(int nbatch, int m, int n, const double* const* ua, const double* const* va,
+                              const int* ra, const double* const* ub, const double* const* vb, const int* rb,
+                              double* const* uo, double* const* vo, int* ro, int cap, double eps, double* ws,
+                              int64_t ws_per_cta, int nctas, int* status, unsigned long long* flops, void* stream);
+
+/* Batched truncated RRQR compression (compress_rrqr lowrank.py:138-150 with
+ * max_rank = floor(fraction*min(m,n)); compress_to_lowrank :153-158 with
+ * max_rank = min(m,n)).  a[t] (m x n) is NOT modified.  ro[t] = rank, or -1
+ * when the dense fallback applies. */
+int blrqr_compress_batched(int nbatch, int m, int n, const double* const* a, double* const* uo,
+                           double* const* vo, int* ro, int cap, double eps, int max_rank, double* ws,
+                           int64_t ws_per_cta, int nctas, int* status, unsigned long long* flops, void* stream);
+
+/* Products: op 0 lr_add_into_dense d + u v^T (lowrank.py:224-231) into out;
+ * op 1 lr_times_dense side=right: v_out = d^T v (lowrank.py:246-247);
+ * op 2 lr_times_dense side=left: (Q, R) = qr(d u), v_out = v R^T (:248-255);
+ * op 3 lr_times_lr (lowrank.py:264-287).  Single problem, device pointers. */
+int blrqr_lr_product(int op, int m, int k, int n, const double* u, const double* v, int r, const double* d,
+                     const double* u2, const double* v2, int r2, double* out_u, double* out_v, int* out_r,
+                     double* ws, int64_t ws_doubles, int* status, unsigned long long* flops, void* stream);
+
+/* ---- dense panel kernels (kernels.py) ----------------------------------- */
+/* qr_compact_wy (kernels.py:87-103): a (m x n, m >= n) -> y (m x n, unit
+ * lower trapezoidal, explicit diagonal), t (n x n upper), r (n x n upper). */
+int blrqr_geqrt(int m, int n, const double* a, double* y, double* t, double* r, double* ws, int64_t ws_doubles,
+                int* status, unsigned long long* flops, void* stream);
+/* c <- c - y op(t) (y^T c) (kernels.py:111-128); c is m x nc */
+int blrqr_apply_wy(int m, int n, int nc, const double* y, const double* t, double* c, int transpose, double* ws,
+                   int64_t ws_doubles, int* status, unsigned long long* flops, void* stream);
+/* tp_qr (kernels.py:131-155): r_top (n x n upper) and a_bot (k x n) ->
+ * r_new, y (k x n), t (n x n).  Inputs are not modified. */
+int blrqr_tpqrt(int n, int k, const double* r_top, const double* a_bot, double* r_new, double* y, double* t,
+                double* ws, int64_t ws_doubles, int* status, unsigned long long* flops, void* stream);
+/* apply_tp(_transpose) (kernels.py:158-186): in place on c_top (n x nc), c_bot (k x nc) */
+int blrqr_apply_tp(int n, int k, int nc, const double* y, const double* t, double* c_top, double* c_bot,
+                   int transpose, double* ws, int64_t ws_doubles, int* status, unsigned long long* flops,
+                   void* stream);
+/* mgs_panel_qr (kernels.py:192-225): a (m x n) -> q (m x n), r (n x n) */
+int blrqr_mgs_panel(int m, int n, const double* a, double* q, double* r, double* ws, int64_t ws_doubles,
+                    int* status, unsigned long long* flops, void* stream);
+
+/* ---- BLR construction (core.dense_to_blr, core.py:227-259) ------------- */
+/* Compress the admissible cells of a dense m x n matrix (column-major, lda)
+ * into the grid (whose off_u/off_v slabs must exist for every cell).
+ * lowrank_io: in = admissibility (1 = compress), out = 0 where the dense
+ * fallback applied (the dense tile is then copied into the cell's u slab,
+ * which must hold b*b doubles). */
+int blrqr_dense_to_blr(const double* a, int64_t lda, blrqr_grid* g, unsigned char* lowrank_io, double eps,
+                       double fallback, double* ws, int64_t ws_per_cta, int nctas, int* status,
+                       unsigned long long* flops, void* stream);
+
+/* Copy every cell between the grid and a contiguous staging buffer (device):
+ * stage_off[c] (device int64, -1 = skip) is cell c's offset; dense cells
+ * occupy b*b doubles, low-rank cells b*rank (U) followed by b*rank (V), with
+ * rank taken from g->rank.  to_grid = 1 uploads, 0 downloads. */
+int blrqr_grid_pack(const blrqr_grid* g, double* stage, const int64_t* stage_off, int to_grid, void* stream);
+
+/* ---- factorizations (factorize.py / scheduler.py) ---------------------- */
+/* Tiled Householder: static level schedule of the tiled DAG
+ * (scheduler.py:109-201).  Fills tasks (ntasks = blrqr_tiled_task_count) in
+ * execution order and level_start (nlevels + 1 entries); returns nlevels. */
+int64_t blrqr_tiled_task_count(int p, int q);
+int blrqr_tiled_schedule(int p, int q, blrqr_task* tasks_host, int64_t* level_start_host, int64_t max_levels);
+/* Run levels [l0, l1) of a schedule already uploaded to tasks_dev. */
+int blrqr_tiled_run(const blrqr_grid* g, const blrqr_refl* rf, const blrqr_task* tasks_dev,
+                    const int64_t* level_start_host, int l0, int l1, double eps, double* ws, int64_t ws_per_cta,
+                    int nctas, int* status, unsigned long long* flops, void* stream);
+
+/* Blocked Householder (factorize.py:187-292): one panel + its column updates.
+ * zbuf: per-column scratch for z_j = T^T s_j: (q * 2 * b * cap) doubles + q ints
+ * (zrank). panel_ws: (b + sum_i rows_i) x b panel scratch sized by caller. */
+int blrqr_blocked_step(const blrqr_grid* g, const blrqr_refl* rf, int k, double eps, double* zbuf, int* zrank,
+                       double* ws, int64_t ws_per_cta, int nctas, int* status, unsigned long long* flops,
+                       void* stream);
+
+/* Blocked MGS (factorize.py:576-671): step j = panel(j), project(j, k>j),
+ * update(j, i, k>j).  qg: explicit Q grid (same kind map as a); rg: R grid (q x q). */
+int blrqr_mgs_step(const blrqr_grid* a, const blrqr_grid* qg, const blrqr_grid* rg, int j, double eps,
+                   double* ws, int64_t ws_per_cta, int nctas, int* status, unsigned long long* flops,
+                   void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BLRQR_H */

@@ -1,0 +1,170 @@
+"""ctypes binding of libblrqr.so (include/blrqr.h) plus device plumbing.
+
+The CUDA library is the only compute path: importing this module on a
+machine without the built library raises, and every entry point raises if no
+CUDA device is present.  There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libblrqr.so")
+
+FLOP_KINDS = ("compress", "rounded_add", "expand", "lr_mul", "gemm", "panel_qr",
+              "apply_wy", "update_qr", "apply_tp")
+ST_RANK_OVERFLOW, ST_ARENA_OVERFLOW, ST_NONFINITE, ST_MGS_COLLAPSE, ST_BAD_KIND, ST_BAD_ARG = (
+    1, 2, 4, 8, 16, 32)
+
+_lib = None
+_lock = threading.Lock()
+
+
+class Grid(C.Structure):
+    _fields_ = [("p", C.c_int), ("q", C.c_int), ("b", C.c_int), ("cap", C.c_int),
+                ("lowrank", C.c_void_p), ("rank", C.c_void_p), ("pool", C.c_void_p),
+                ("off_u", C.c_void_p), ("off_v", C.c_void_p)]
+
+
+class Refl(C.Structure):
+    _fields_ = [("pool", C.c_void_p), ("y_off", C.c_void_p), ("t_off", C.c_void_p),
+                ("yrank", C.c_void_p)]
+
+
+class Task(C.Structure):
+    _fields_ = [("kind", C.c_int), ("k", C.c_int), ("i", C.c_int), ("j", C.c_int)]
+
+
+_P = C.c_void_p
+_I = C.c_int
+_L = C.c_int64
+_D = C.c_double
+
+_SIGS = {
+    "blrqr_version": ([], _I),
+    "blrqr_workspace_doubles": ([_I, _I, _I], _L),
+    "blrqr_default_ctas": ([], _I),
+    "blrqr_rounded_add_batched": ([_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _D, _P, _L, _I, _P, _P, _P], _I),
+    "blrqr_compress_batched": ([_I, _I, _I, _P, _P, _P, _P, _I, _D, _I, _P, _L, _I, _P, _P, _P], _I),
+    "blrqr_lr_product": ([_I, _I, _I, _I, _P, _P, _I, _P, _P, _P, _I, _P, _P, _P, _P, _L, _P, _P, _P], _I),
+    "blrqr_geqrt": ([_I, _I, _P, _P, _P, _P, _P, _L, _P, _P, _P], _I),
+    "blrqr_apply_wy": ([_I, _I, _I, _P, _P, _P, _I, _P, _L, _P, _P, _P], _I),
+    "blrqr_tpqrt": ([_I, _I, _P, _P, _P, _P, _P, _P, _L, _P, _P, _P], _I),
+    "blrqr_apply_tp": ([_I, _I, _I, _P, _P, _P, _P, _I, _P, _L, _P, _P, _P], _I),
+    "blrqr_mgs_panel": ([_I, _I, _P, _P, _P, _P, _L, _P, _P, _P], _I),
+    "blrqr_dense_to_blr": ([_P, _L, C.POINTER(Grid), _P, _D, _D, _P, _L, _I, _P, _P, _P], _I),
+    "blrqr_grid_pack": ([C.POINTER(Grid), _P, _P, _I, _P], _I),
+    "blrqr_tiled_task_count": ([_I, _I], _L),
+    "blrqr_tiled_schedule": ([_I, _I, _P, _P, _L], _I),
+    "blrqr_tiled_run": ([C.POINTER(Grid), C.POINTER(Refl), _P, _P, _I, _I, _D, _P, _L, _I, _P, _P, _P], _I),
+    "blrqr_blocked_step": ([C.POINTER(Grid), C.POINTER(Refl), _I, _D, _P, _P, _P, _L, _I, _P, _P, _P], _I),
+    "blrqr_mgs_step": ([C.POINTER(Grid), C.POINTER(Grid), C.POINTER(Grid), _I, _D, _P, _L, _I, _P, _P, _P], _I),
+}
+
+EXPORTED = tuple(_SIGS)
+
+
+def load(path: str = LIB_PATH):
+    """Load (once) and type the C ABI.  Raises if the library is missing."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(path):
+                raise RuntimeError(
+                    f"libblrqr.so not built at {path}; run `python -c 'import __graft_entry__ as g; g.build()'` "
+                    "(there is no CPU fallback)")
+            lib = C.CDLL(path)
+            for name, (args, res) in _SIGS.items():
+                fn = getattr(lib, name)
+                fn.argtypes = args
+                fn.restype = res
+            _lib = lib
+    return _lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc == 0:
+        return
+    if rc < 0:
+        raise ValueError(f"{what}: invalid argument (code {rc})")
+    raise RuntimeError(f"{what}: CUDA error {rc - 1000 if rc >= 1000 else rc}")
+
+
+def require_cuda() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2208_06194_b200 needs a CUDA device (sm_100a); no CPU fallback exists")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+class Runtime:
+    """Per-process device state: workspace arena, status word, flop counters."""
+
+    def __init__(self):
+        self.dev = require_cuda()
+        self.lib = load()
+        self.status = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.flops = torch.zeros(len(FLOP_KINDS), dtype=torch.int64, device=self.dev)
+        self.nctas = int(self.lib.blrqr_default_ctas())
+        self._ws = None
+        self._ws_per_cta = 0
+
+    def workspace(self, b: int, cap: int, panel_rows: int = 0, nctas: int | None = None):
+        """(ptr, doubles_per_cta, nctas) — grows the shared arena on demand."""
+        nctas = nctas or self.nctas
+        per = int(self.lib.blrqr_workspace_doubles(b, cap, panel_rows))
+        need = per * nctas
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = None
+            torch.cuda.synchronize()
+            self._ws = torch.empty(need, dtype=torch.float64, device=self.dev)
+        return self._ws.data_ptr(), per, nctas
+
+    def reset_counters(self):
+        self.status.zero_()
+        self.flops.zero_()
+
+    def harvest(self, warn_mgs: bool = True) -> tuple[int, dict]:
+        """Synchronise, read and clear status + flop counters; raise on errors."""
+        st = int(self.status.item())
+        fl = self.flops.cpu().numpy().astype(np.int64)
+        self.status.zero_()
+        self.flops.zero_()
+        counts = {k: int(v) for k, v in zip(FLOP_KINDS, fl) if v}
+        from . import flops as _fl
+        for k, v in counts.items():
+            _fl.add(k, v)
+        if st & ST_ARENA_OVERFLOW:
+            raise RuntimeError("per-CTA workspace overflow (blrqr_workspace_doubles too small)")
+        if st & ST_RANK_OVERFLOW:
+            raise RuntimeError("a low-rank result exceeded the slab capacity (raise cap)")
+        if st & ST_BAD_KIND:
+            raise ValueError("diagonal blocks must be dense")
+        if st & ST_MGS_COLLAPSE and warn_mgs:
+            import warnings
+            from .kernels import RankDeficiencyWarning
+            warnings.warn("MGS panel column collapsed below 1e-300", RankDeficiencyWarning, stacklevel=3)
+        return st, counts
+
+
+_rt = None
+
+
+def runtime() -> Runtime:
+    global _rt
+    if _rt is None:
+        _rt = Runtime()
+    return _rt

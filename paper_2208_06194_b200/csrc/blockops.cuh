@@ -1,0 +1,332 @@
+// Kind-dispatched block arithmetic on device (factorize.py:68-138,
+// lowrank.py:161-231): low-rank blocks are factor pairs s * U V^T, dense
+// blocks s * D.  Products never truncate; every LR + LR sum is a rounded
+// addition (Alg. 6); writes are coerced to the structural kind of the target
+// cell.  All routines are CTA-cooperative.
+#pragma once
+#include "svd_rrqr.cuh"
+
+namespace blr {
+
+constexpr double NOISE_FLOOR = 64.0 * 2.220446049250313e-16;  // lowrank.py:170
+
+struct Blk {
+  int lr;        // 1: s * u v^T (rank columns), 0: s * u as dense rows x cols
+  int rank;
+  int rows, cols;
+  double* u;
+  int ldu;
+  double* v;
+  int ldv;
+  double s;
+};
+
+__device__ __forceinline__ Blk make_lr(int rows, int cols, int rank, double* u, int ldu, double* v, int ldv,
+                                       double s = 1.0) {
+  Blk b; b.lr = 1; b.rank = rank; b.rows = rows; b.cols = cols; b.u = u; b.ldu = ldu; b.v = v; b.ldv = ldv; b.s = s;
+  return b;
+}
+__device__ __forceinline__ Blk make_dense(int rows, int cols, double* d, int ld, double s = 1.0) {
+  Blk b; b.lr = 0; b.rank = -1; b.rows = rows; b.cols = cols; b.u = d; b.ldu = ld; b.v = nullptr; b.ldv = 0; b.s = s;
+  return b;
+}
+
+// ||s u v^T||_F from the factors (lowrank.py:161-166)
+__device__ __noinline__ double lr_norm(Ctx& cx, const Blk& a) {
+  if (a.rank == 0) return 0.0;
+  const long long mark = cx.top;
+  const int r = a.rank;
+  double* g = alloc(cx, (long long)r * r);
+  double* m = alloc(cx, (long long)a.cols * r);
+  if (!g || !m) { cx.top = mark; return 0.0; }
+  gemm(true, false, r, r, a.rows, 1.0, a.u, a.ldu, a.u, a.ldu, 0.0, g, r);
+  gemm(false, false, a.cols, r, r, 1.0, a.v, a.ldv, g, r, 0.0, m, a.cols);
+  double s = 0.0;
+  for (long long e = threadIdx.x; e < (long long)a.cols * r; e += NT) {
+    const int i = (int)(e % a.cols), c = (int)(e / a.cols);
+    s = fma(m[e], a.v[i + (long long)c * a.ldv], s);
+  }
+  s = cta_sum(s);
+  cx.top = mark;
+  return fabs(a.s) * sqrt(fmax(s, 0.0));
+}
+
+// Rounded addition C = A + B (lowrank.py:173-221).  Output factors are written
+// to (du, ldu_, dv, ldv_) with capacity `cap` columns (may alias A or B: the
+// inputs are consumed first).  Returns the output rank.
+__device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, double eps, double* du, int lddu, double* dv,
+                           int lddv, int cap) {
+  const int m = A.rows, n = A.cols;
+  if (A.rank == 0 && B.rank == 0) return 0;
+  const int c = A.rank + B.rank;
+  const long long mark = cx.top;
+  const double nA = lr_norm(cx, A), nB = lr_norm(cx, B);
+  double* Uc = alloc(cx, (long long)m * c);
+  double* Vc = alloc(cx, (long long)n * c);
+  double* tauU = alloc(cx, c);
+  double* tauV = alloc(cx, c);
+  double* TpU = alloc(cx, (long long)QR_NB * c);
+  double* TpV = alloc(cx, (long long)QR_NB * c);
+  if (!Uc || !Vc || !tauU || !tauV || !TpU || !TpV) { cx.top = mark; return 0; }
+  copy_mat(m, A.rank, A.u, A.ldu, Uc, m);
+  copy_mat(m, B.rank, B.u, B.ldu, Uc + (long long)A.rank * m, m);
+  copy_mat(n, A.rank, A.v, A.ldv, Vc, n, A.s);
+  copy_mat(n, B.rank, B.v, B.ldv, Vc + (long long)A.rank * n, n, B.s);
+  qr_blocked(cx, m, c, Uc, m, tauU, TpU);
+  qr_blocked(cx, n, c, Vc, n, tauV, TpV);
+  const int kU = min(m, c), kV = min(n, c);
+  const int k = kU;  // square blocks: kU == kV
+  double* RU = alloc(cx, (long long)kU * c);
+  double* RV = alloc(cx, (long long)kV * c);
+  double* G = alloc(cx, (long long)k * k);
+  double* J = alloc(cx, (long long)k * k);
+  double* sig = alloc(cx, k);
+  int* perm = reinterpret_cast<int*>(alloc(cx, k));
+  double* tail = alloc(cx, k + 1);
+  if (!RU || !RV || !G || !J || !sig || !perm || !tail) { cx.top = mark; return 0; }
+  for (long long e = threadIdx.x; e < (long long)kU * c; e += NT) {
+    const int i = (int)(e % kU), j = (int)(e / kU);
+    RU[e] = i <= j ? Uc[i + (long long)j * m] : 0.0;
+  }
+  for (long long e = threadIdx.x; e < (long long)kV * c; e += NT) {
+    const int i = (int)(e % kV), j = (int)(e / kV);
+    RV[e] = i <= j ? Vc[i + (long long)j * n] : 0.0;
+  }
+  __syncthreads();
+  gemm(false, true, kU, kV, c, 1.0, RU, kU, RV, kV, 0.0, G, k);
+  jacobi_svd(k, G, J, sig, perm);
+  add_flops(cx, FK_ROUNDED_ADD, qr_cost(m, c) + qr_cost(n, c) + mm_cost(kU, c, kV) + svd_cost(kU));
+  // truncation (lowrank.py:204-213), decided by one thread
+  __shared__ int s_rank;
+  if (threadIdx.x == 0) {
+    const double floor_ = NOISE_FLOOR * hypot(nA, nB);
+    int significant = 0;
+    double total2 = 0.0;
+    for (int i = 0; i < k; ++i) {
+      const double si = sig[perm[i]];
+      significant += si > floor_;
+      total2 += si * si;
+    }
+    int rank = 0;
+    if (total2 != 0.0 && significant != 0) {
+      tail[k] = 0.0;
+      double acc = 0.0;
+      for (int i = k - 1; i >= 0; --i) {
+        const double si = sig[perm[i]];
+        acc += si * si;
+        tail[i] = acc;
+      }
+      const double thresh2 = (eps * eps) * total2;
+      int first = k;
+      for (int i = 0; i <= k; ++i)
+        if (tail[i] <= thresh2) { first = i; break; }
+      rank = min(first, significant);
+    }
+    s_rank = rank;
+  }
+  __syncthreads();
+  int rank = s_rank;
+  if (rank > cap) {
+    set_status(cx, ST_RANK_OVERFLOW);
+    rank = cap;
+  }
+  if (rank > 0) {
+    double* ZU = alloc(cx, (long long)m * rank);
+    double* ZV = alloc(cx, (long long)n * rank);
+    if (!ZU || !ZV) { cx.top = mark; return 0; }
+    for (long long e = threadIdx.x; e < (long long)m * rank; e += NT) {
+      const int i = (int)(e % m), j = (int)(e / m);
+      const int pj = perm[j];
+      ZU[e] = i < k ? G[i + (long long)pj * k] / sig[pj] : 0.0;
+    }
+    for (long long e = threadIdx.x; e < (long long)n * rank; e += NT) {
+      const int i = (int)(e % n), j = (int)(e / n);
+      const int pj = perm[j];
+      ZV[e] = i < k ? J[i + (long long)pj * k] * sig[pj] : 0.0;
+    }
+    __syncthreads();
+    qr_apply(cx, m, kU, Uc, m, TpU, ZU, m, rank, false);
+    qr_apply(cx, n, kV, Vc, n, TpV, ZV, n, rank, false);
+    copy_mat(m, rank, ZU, m, du, lddu);
+    copy_mat(n, rank, ZV, n, dv, lddv);
+    add_flops(cx, FK_ROUNDED_ADD, mm_cost(m, kU, rank) + mm_cost(n, kV, rank));
+  }
+  cx.top = mark;
+  return rank;
+}
+
+// ---------------------------------------------------------------------------
+// products (factorize.py:68-108); results live in the arena or alias inputs
+// ---------------------------------------------------------------------------
+
+// x @ y
+__device__ Blk blk_mul(Ctx& cx, const Blk& x, const Blk& y) {
+  const double s = x.s * y.s;
+  if (x.lr) {
+    if (y.lr) {
+      double* core = alloc(cx, (long long)max(y.rank, 1) * max(x.rank, 1));
+      double* v = alloc(cx, (long long)y.cols * max(x.rank, 1));
+      gemm(true, false, y.rank, x.rank, x.cols, 1.0, y.u, y.ldu, x.v, x.ldv, 0.0, core, max(y.rank, 1));
+      gemm(false, false, y.cols, x.rank, y.rank, 1.0, y.v, y.ldv, core, max(y.rank, 1), 0.0, v, y.cols);
+      add_flops(cx, FK_LR_MUL, mm_cost(y.rank, x.cols, x.rank) + mm_cost(y.cols, y.rank, x.rank));
+      return make_lr(x.rows, y.cols, x.rank, x.u, x.ldu, v, y.cols, s);
+    }
+    double* v = alloc(cx, (long long)y.cols * max(x.rank, 1));
+    gemm(true, false, y.cols, x.rank, y.rows, 1.0, y.u, y.ldu, x.v, x.ldv, 0.0, v, y.cols);
+    add_flops(cx, FK_LR_MUL, mm_cost(y.cols, x.cols, x.rank));
+    return make_lr(x.rows, y.cols, x.rank, x.u, x.ldu, v, y.cols, s);
+  }
+  if (y.lr) {
+    double* u = alloc(cx, (long long)x.rows * max(y.rank, 1));
+    gemm(false, false, x.rows, y.rank, x.cols, 1.0, x.u, x.ldu, y.u, y.ldu, 0.0, u, x.rows);
+    add_flops(cx, FK_LR_MUL, mm_cost(x.rows, x.cols, y.rank));
+    return make_lr(x.rows, y.cols, y.rank, u, x.rows, y.v, y.ldv, s);
+  }
+  double* d = alloc(cx, (long long)x.rows * y.cols);
+  gemm(false, false, x.rows, y.cols, x.cols, 1.0, x.u, x.ldu, y.u, y.ldu, 0.0, d, x.rows);
+  add_flops(cx, FK_GEMM, mm_cost(x.rows, x.cols, y.cols));
+  return make_dense(x.rows, y.cols, d, x.rows, s);
+}
+
+// x^T @ y
+__device__ Blk blk_mul_t(Ctx& cx, const Blk& x, const Blk& y) {
+  const double s = x.s * y.s;
+  if (x.lr) {
+    if (y.lr) {
+      double* core = alloc(cx, (long long)max(y.rank, 1) * max(x.rank, 1));
+      double* v = alloc(cx, (long long)y.cols * max(x.rank, 1));
+      gemm(true, false, y.rank, x.rank, x.rows, 1.0, y.u, y.ldu, x.u, x.ldu, 0.0, core, max(y.rank, 1));
+      gemm(false, false, y.cols, x.rank, y.rank, 1.0, y.v, y.ldv, core, max(y.rank, 1), 0.0, v, y.cols);
+      add_flops(cx, FK_LR_MUL, mm_cost(y.rank, x.rows, x.rank) + mm_cost(y.cols, y.rank, x.rank));
+      return make_lr(x.cols, y.cols, x.rank, x.v, x.ldv, v, y.cols, s);
+    }
+    double* v = alloc(cx, (long long)y.cols * max(x.rank, 1));
+    gemm(true, false, y.cols, x.rank, y.rows, 1.0, y.u, y.ldu, x.u, x.ldu, 0.0, v, y.cols);
+    add_flops(cx, FK_LR_MUL, mm_cost(y.cols, x.rows, x.rank));
+    return make_lr(x.cols, y.cols, x.rank, x.v, x.ldv, v, y.cols, s);
+  }
+  if (y.lr) {
+    double* u = alloc(cx, (long long)x.cols * max(y.rank, 1));
+    gemm(true, false, x.cols, y.rank, x.rows, 1.0, x.u, x.ldu, y.u, y.ldu, 0.0, u, x.cols);
+    add_flops(cx, FK_LR_MUL, mm_cost(x.cols, x.rows, y.rank));
+    return make_lr(x.cols, y.cols, y.rank, u, x.cols, y.v, y.ldv, s);
+  }
+  double* d = alloc(cx, (long long)x.cols * y.cols);
+  gemm(true, false, x.cols, y.cols, x.rows, 1.0, x.u, x.ldu, y.u, y.ldu, 0.0, d, x.cols);
+  add_flops(cx, FK_GEMM, mm_cost(x.cols, x.rows, y.cols));
+  return make_dense(x.cols, y.cols, d, x.cols, s);
+}
+
+// op(t) @ s, keeping s's kind (factorize.py:102-108); t is n x n (ldt)
+__device__ Blk blk_dense_times(Ctx& cx, const double* t, int ldt, bool trans, const Blk& x) {
+  if (x.lr) {
+    double* u = alloc(cx, (long long)x.rows * max(x.rank, 1));
+    gemm(trans, false, x.rows, x.rank, x.rows, 1.0, t, ldt, x.u, x.ldu, 0.0, u, x.rows);
+    add_flops(cx, FK_LR_MUL, mm_cost(x.rows, x.rows, x.rank));
+    return make_lr(x.rows, x.cols, x.rank, u, x.rows, x.v, x.ldv, x.s);
+  }
+  double* d = alloc(cx, (long long)x.rows * x.cols);
+  gemm(trans, false, x.rows, x.cols, x.rows, 1.0, t, ldt, x.u, x.ldu, 0.0, d, x.rows);
+  add_flops(cx, FK_GEMM, mm_cost(x.rows, x.rows, x.cols));
+  return make_dense(x.rows, x.cols, d, x.rows, x.s);
+}
+
+// dst (dense, ldd) = a_dense * s_a + (lr term expanded)
+__device__ void expand_add(Ctx& cx, const Blk& d, const Blk& l, double* dst, int ldd) {
+  copy_mat(d.rows, d.cols, d.u, d.ldu, dst, ldd, d.s);
+  if (l.rank > 0) {
+    gemm(false, true, l.rows, l.cols, l.rank, l.s, l.u, l.ldu, l.v, l.ldv, 1.0, dst, ldd);
+    add_flops(cx, FK_EXPAND, mm_cost(l.rows, l.rank, l.cols));
+  }
+}
+
+// s + term (factorize.py:117-125); LR+LR results have capacity cap_out
+__device__ Blk blk_acc(Ctx& cx, const Blk& s, const Blk& t, double eps, int cap_out) {
+  if (s.lr && t.lr) {
+    const int c = max(s.rank + t.rank, 1);
+    const int k = min(min(s.rows, s.cols), c);
+    const int cap = min(k, cap_out);
+    double* u = alloc(cx, (long long)s.rows * cap);
+    double* v = alloc(cx, (long long)s.cols * cap);
+    const int r = rounded_add(cx, s, t, eps, u, s.rows, v, s.cols, cap);
+    return make_lr(s.rows, s.cols, r, u, s.rows, v, s.cols, 1.0);
+  }
+  double* d = alloc(cx, (long long)s.rows * s.cols);
+  if (s.lr) {
+    expand_add(cx, t, s, d, s.rows);
+  } else if (t.lr) {
+    expand_add(cx, s, t, d, s.rows);
+  } else {
+    for (long long e = threadIdx.x; e < (long long)s.rows * s.cols; e += NT) {
+      const int i = (int)(e % s.rows), j = (int)(e / s.rows);
+      d[e] = s.s * s.u[i + (long long)j * s.ldu] + t.s * t.u[i + (long long)j * t.ldu];
+    }
+    __syncthreads();
+  }
+  return make_dense(s.rows, s.cols, d, s.rows, 1.0);
+}
+
+// Cell handle: where a grid cell's data lives.
+struct Cell {
+  int lr;
+  int* rank;       // device rank word (LR cells)
+  double* u;       // LR: U slab (b x cap); dense: b x b data
+  double* v;       // LR: V slab (b x cap)
+  int ld;          // = b
+  int cap;
+  int b;
+};
+
+__device__ __forceinline__ Blk cell_blk(const Cell& c) {
+  if (c.lr) return make_lr(c.b, c.b, *c.rank, c.u, c.ld, c.v, c.ld, 1.0);
+  return make_dense(c.b, c.b, c.u, c.ld, 1.0);
+}
+
+// target - term written into the cell (factorize.py:128-138).  Must be
+// called after every read of the cell's old contents has completed.
+__device__ __noinline__ void sub_into_cell(Ctx& cx, const Cell& c, const Blk& term, double eps) {
+  Blk tgt = cell_blk(c);
+  if (c.lr) {
+    if (term.lr) {
+      Blk neg = term;
+      neg.s = -term.s;
+      const int r = rounded_add(cx, tgt, neg, eps, c.u, c.ld, c.v, c.ld, c.cap);
+      if (threadIdx.x == 0) *c.rank = r;
+    } else {
+      // dense term in a low-rank cell: expand, subtract, compress (no fallback)
+      const long long mark = cx.top;
+      double* d = alloc(cx, (long long)c.b * c.b);
+      if (!d) return;
+      Blk negt = term;
+      negt.s = -term.s;
+      expand_add(cx, negt, tgt, d, c.b);
+      double* U = alloc(cx, (long long)c.b * c.b);
+      double* V = alloc(cx, (long long)c.b * c.b);
+      if (!U || !V) { cx.top = mark; return; }
+      int r = rrqr_trunc(cx, c.b, c.b, d, c.b, eps, c.b, U, c.b, V, c.b);
+      if (r < 0) r = 0;
+      if (r > c.cap) { set_status(cx, ST_RANK_OVERFLOW); r = c.cap; }
+      copy_mat(c.b, r, U, c.b, c.u, c.ld);
+      copy_mat(c.b, r, V, c.b, c.v, c.ld);
+      if (threadIdx.x == 0) *c.rank = r;
+      __syncthreads();
+      cx.top = mark;
+    }
+  } else {
+    if (term.lr) {
+      if (term.rank > 0) {
+        gemm(false, true, c.b, c.b, term.rank, -term.s, term.u, term.ldu, term.v, term.ldv, 1.0, c.u, c.ld);
+        add_flops(cx, FK_EXPAND, mm_cost(c.b, term.rank, c.b));
+      }
+    } else {
+      for (long long e = threadIdx.x; e < (long long)c.b * c.b; e += NT) {
+        const int i = (int)(e % c.b), j = (int)(e / c.b);
+        c.u[i + (long long)j * c.ld] -= term.s * term.u[i + (long long)j * term.ldu];
+      }
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+}
+
+}  // namespace blr

@@ -1,0 +1,569 @@
+// libblrqr.so — kernels + C ABI (include/blrqr.h).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <unordered_map>
+#include <vector>
+
+#include "tasks.cuh"
+
+using namespace blr;
+
+#define CK(x)                                   \
+  do {                                          \
+    cudaError_t e_ = (x);                       \
+    if (e_ != cudaSuccess) return 1000 + (int)e_; \
+  } while (0)
+
+static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ===========================================================================
+// kernels
+// ===========================================================================
+
+__global__ void __launch_bounds__(NT) k_rounded_add(int nb, int m, int n, const double* const* ua,
+                                                     const double* const* va, const int* ra,
+                                                     const double* const* ub, const double* const* vb,
+                                                     const int* rb, double* const* uo, double* const* vo, int* ro,
+                                                     int cap, double eps, double* ws, long long wsp, int* status,
+                                                     unsigned long long* flops) {
+  Ctx cx = make_ctx(ws, wsp, status, flops);
+  for (int t = blockIdx.x; t < nb; t += gridDim.x) {
+    Blk A = make_lr(m, n, ra[t], const_cast<double*>(ua[t]), m, const_cast<double*>(va[t]), n);
+    Blk B = make_lr(m, n, rb[t], const_cast<double*>(ub[t]), m, const_cast<double*>(vb[t]), n);
+    const int r = rounded_add(cx, A, B, eps, uo[t], m, vo[t], n, cap);
+    if (threadIdx.x == 0) ro[t] = r;
+    cx.top = 0;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_compress(int nb, int m, int n, const double* const* a, double* const* uo,
+                                                  double* const* vo, int* ro, int cap, double eps, int max_rank,
+                                                  double* ws, long long wsp, int* status,
+                                                  unsigned long long* flops) {
+  Ctx cx = make_ctx(ws, wsp, status, flops);
+  for (int t = blockIdx.x; t < nb; t += gridDim.x) {
+    double* w = alloc(cx, (long long)m * n);
+    double* U = alloc(cx, (long long)m * min(m, n));
+    double* V = alloc(cx, (long long)n * min(m, n));
+    if (!w || !U || !V) return;
+    copy_mat(m, n, a[t], m, w, m);
+    int r = rrqr_trunc(cx, m, n, w, m, eps, max_rank, U, m, V, n);
+    if (r > cap) { set_status(cx, ST_RANK_OVERFLOW); r = -1; }
+    if (r > 0) {
+      copy_mat(m, r, U, m, uo[t], m);
+      copy_mat(n, r, V, n, vo[t], n);
+    }
+    if (threadIdx.x == 0) ro[t] = r;
+    cx.top = 0;
+    __syncthreads();
+  }
+}
+
+// dense_to_blr (core.py:227-259): one CTA per cell in row-major order
+__global__ void __launch_bounds__(NT) k_dense_to_blr(const double* a, long long lda, blrqr_grid g,
+                                                      unsigned char* lowrank_io, double eps, int max_rank,
+                                                      double* ws, long long wsp, int* status,
+                                                      unsigned long long* flops) {
+  Ctx cx = make_ctx(ws, wsp, status, flops);
+  const int b = g.b;
+  for (int c = blockIdx.x; c < g.p * g.q; c += gridDim.x) {
+    const int i = c / g.q, j = c % g.q;
+    const double* tile = a + (long long)i * b + (long long)j * b * lda;
+    double* U0 = g.pool + g.off_u[c];
+    if (lowrank_io[c]) {
+      double* w = alloc(cx, (long long)b * b);
+      double* U = alloc(cx, (long long)b * b);
+      double* V = alloc(cx, (long long)b * b);
+      if (!w || !U || !V) return;
+      for (long long e = threadIdx.x; e < (long long)b * b; e += NT)
+        w[e] = tile[(e % b) + (e / b) * lda];
+      __syncthreads();
+      int r = rrqr_trunc(cx, b, b, w, b, eps, max_rank, U, b, V, b);
+      if (r > g.cap) { set_status(cx, ST_RANK_OVERFLOW); r = -1; }
+      if (r >= 0) {
+        copy_mat(b, r, U, b, U0, b);
+        copy_mat(b, r, V, b, g.pool + g.off_v[c], b);
+        if (threadIdx.x == 0) g.rank[c] = r;
+      } else {
+        // dense fallback (core.py:252-254): the cell keeps the tile; its slab
+        // (2*b*cap doubles, cap >= b/2) holds the b x b data
+        for (long long e = threadIdx.x; e < (long long)b * b; e += NT) U0[e] = tile[(e % b) + (e / b) * lda];
+        if (threadIdx.x == 0) {
+          lowrank_io[c] = 0;
+          g.rank[c] = -1;
+        }
+      }
+    } else {
+      for (long long e = threadIdx.x; e < (long long)b * b; e += NT) U0[e] = tile[(e % b) + (e / b) * lda];
+      if (threadIdx.x == 0) g.rank[c] = -1;
+    }
+    cx.top = 0;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_geqrt(int m, int n, const double* a, double* y, double* t, double* r,
+                                               double* ws, long long wsp, int* status, unsigned long long* flops) {
+  Ctx cx = make_ctx(ws, wsp, status, flops);
+  double* A = alloc(cx, (long long)m * n);
+  if (!A) return;
+  copy_mat(m, n, a, m, A, m);
+  geqrt_inplace(cx, m, n, A, m, y, m, t, n);
+  for (long long e = threadIdx.x; e < (long long)n * n; e += NT) {
+    const int i = (int)(e % n), j = (int)(e / n);
+    r[e] = i <= j ? A[i + (long long)j * m] : 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_apply_wy(int m, int n, int nc, const double* y, const double* t, double* c,
+                                                  int transpose, double* ws, long long wsp, int* status,
+                                                  unsigned long long* flops) {
+  Ctx cx = make_ctx(ws, wsp, status, flops);
+  apply_wy_dev(cx, m, n, nc, y, m, t, n, c, m, transpose != 0);
+}
+
+__global__ void __launch_bounds__(NT) k_tpqrt(int n, int k, const double* rt, const double* ab, double* rn,
+                                               double* y, double* t, double* ws, long long wsp, int* status,
+                                               unsigned long long* flops) {
+  Ctx cx = make_ctx(ws, wsp, status, flops);
+  copy_mat(n, n, rt, n, rn, n);
+  if (k == 0) {
+    zero_mat(n, n, t, n);
+    return;
+  }
+  copy_mat(k, n, ab, k, y, k);
+  tpqrt(cx, n, k, rn, n, y, k, t, n);
+  for (long long e = threadIdx.x; e < (long long)n * n; e += NT) {
+    const int i = (int)(e % n), j = (int)(e / n);
+    if (i > j) rn[e] = 0.0;
+  }
+  add_flops(cx, FK_UPDATE_QR, qr_cost(n + k, n) + tgen_cost(n + k, n));
+}
+
+// apply_tp: w = op(T)(c_top + Y^T c_bot); c_top -= w; c_bot -= Y w
+__global__ void __launch_bounds__(NT) k_apply_tp(int n, int k, int nc, const double* y, const double* t,
+                                                  double* ct, double* cb, int transpose, double* ws, long long wsp,
+                                                  int* status, unsigned long long* flops) {
+  Ctx cx = make_ctx(ws, wsp, status, flops);
+  double* W = alloc(cx, (long long)n * nc);
+  double* W2 = alloc(cx, (long long)n * nc);
+  if (!W || !W2) return;
+  copy_mat(n, nc, ct, n, W, n);
+  gemm(true, false, n, nc, k, 1.0, y, k, cb, k, 1.0, W, n);
+  gemm(transpose != 0, false, n, nc, n, 1.0, t, n, W, n, 0.0, W2, n);
+  for (long long e = threadIdx.x; e < (long long)n * nc; e += NT) ct[e] -= W2[e];
+  __syncthreads();
+  gemm(false, false, k, nc, n, -1.0, y, k, W2, n, 1.0, cb, k);
+  add_flops(cx, FK_APPLY_TP, mm_cost(n, k, nc) + mm_cost(n, n, nc) + mm_cost(k, n, nc));
+}
+
+// modified Gram-Schmidt, right-looking with the same per-column operation
+// sequence as kernels.py:207-223
+__device__ void mgs_panel_dev(Ctx& cx, int m, int n, double* Q, int ldq, double* R, int ldr) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (long long e = threadIdx.x; e < (long long)n * n; e += NT) R[(e % n) + (e / n) * ldr] = 0.0;
+  __syncthreads();
+  for (int i = 0; i < n; ++i) {
+    double* qi = Q + (long long)i * ldq;
+    double s = 0.0;
+    for (int r = threadIdx.x; r < m; r += NT) s = fma(qi[r], qi[r], s);
+    const double nrm = sqrt(cta_sum(s));
+    if (threadIdx.x == 0) R[i + (long long)i * ldr] = nrm;
+    if (nrm < 1e-300) {
+      set_status(cx, ST_MGS_COLLAPSE);
+    } else {
+      for (int r = threadIdx.x; r < m; r += NT) qi[r] = qi[r] / nrm;
+    }
+    __syncthreads();
+    for (int j = i + 1 + warp; j < n; j += NWARP) {
+      double* qj = Q + (long long)j * ldq;
+      double d = 0.0;
+      for (int r = lane; r < m; r += 32) d = fma(qi[r], qj[r], d);
+      d = warp_sum(d);
+      for (int r = lane; r < m; r += 32) qj[r] = fma(-d, qi[r], qj[r]);
+      if (lane == 0) R[i + (long long)j * ldr] = d;
+    }
+    __syncthreads();
+  }
+  add_flops(cx, FK_PANEL_QR, mgs_cost(m, n));
+}
+
+__global__ void __launch_bounds__(NT) k_mgs_panel(int m, int n, const double* a, double* q, double* r,
+                                                   double* ws, long long wsp, int* status,
+                                                   unsigned long long* flops) {
+  Ctx cx = make_ctx(ws, wsp, status, flops);
+  copy_mat(m, n, a, m, q, m);
+  mgs_panel_dev(cx, m, n, q, m, r, n);
+}
+
+// lowrank products (lowrank.py:224-287)
+__global__ void __launch_bounds__(NT) k_lr_product(int op, int m, int k, int n, const double* u, const double* v,
+                                                    int r, const double* d, const double* u2, const double* v2,
+                                                    int r2, double* ou, double* ov, int* orank, double* ws,
+                                                    long long wsp, int* status, unsigned long long* flops) {
+  Ctx cx = make_ctx(ws, wsp, status, flops);
+  if (op == 0) {  // out(m x n) = d + u v^T
+    copy_mat(m, n, d, m, ou, m);
+    if (r > 0) {
+      gemm(false, true, m, n, r, 1.0, u, m, v, n, 1.0, ou, m);
+      add_flops(cx, FK_EXPAND, mm_cost(m, r, n));
+    }
+    if (threadIdx.x == 0) *orank = r;
+  } else if (op == 1) {  // (u, d^T v): a (m x k) @ d (k x n)
+    if (r > 0) {
+      gemm(true, false, n, r, k, 1.0, d, k, v, k, 0.0, ov, n);
+      add_flops(cx, FK_LR_MUL, mm_cost(n, k, r));
+    }
+    if (threadIdx.x == 0) *orank = r;
+  } else if (op == 2) {  // d (m x k) @ a (k x n): qr(d u) -> (Q, v R^T)
+    if (r > 0) {
+      double* X = alloc(cx, (long long)m * r);
+      double* tau = alloc(cx, r);
+      double* Tp = alloc(cx, (long long)QR_NB * r);
+      double* Rr = alloc(cx, (long long)r * r);
+      gemm(false, false, m, r, k, 1.0, d, m, u, k, 0.0, X, m);
+      qr_blocked(cx, m, r, X, m, tau, Tp);
+      const int kr = min(m, r);
+      for (long long e = threadIdx.x; e < (long long)kr * r; e += NT) {
+        const int i = (int)(e % kr), j = (int)(e / kr);
+        Rr[e] = i <= j ? X[i + (long long)j * m] : 0.0;
+      }
+      // Q (m x kr): apply reflectors to identity slab
+      for (long long e = threadIdx.x; e < (long long)m * kr; e += NT) ou[e] = ((e % m) == (e / m)) ? 1.0 : 0.0;
+      __syncthreads();
+      qr_apply(cx, m, kr, X, m, Tp, ou, m, kr, false);
+      gemm(false, true, n, kr, r, 1.0, v, n, Rr, kr, 0.0, ov, n);
+      add_flops(cx, FK_LR_MUL, mm_cost(m, k, r) + qr_cost(m, r) + mm_cost(n, r, r));
+      if (threadIdx.x == 0) *orank = kr;
+    } else if (threadIdx.x == 0) {
+      *orank = 0;
+    }
+  } else {  // lr_times_lr: a = (u m x r, v k x r), bk = (u2 k x r2, v2 n x r2)
+    if (r == 0 || r2 == 0) {
+      if (threadIdx.x == 0) *orank = 0;
+      return;
+    }
+    double* core = alloc(cx, (long long)r2 * r);
+    gemm(true, false, r2, r, k, 1.0, u2, k, v, k, 0.0, core, r2);  // bk.u^T a.v
+    add_flops(cx, FK_LR_MUL, mm_cost(r2, k, r));
+    if (r <= r2) {
+      copy_mat(m, r, u, m, ou, m);
+      gemm(false, false, n, r, r2, 1.0, v2, n, core, r2, 0.0, ov, n);
+      add_flops(cx, FK_LR_MUL, mm_cost(n, r2, r));
+      if (threadIdx.x == 0) *orank = r;
+    } else {
+      double* X = alloc(cx, (long long)m * r2);
+      double* tau = alloc(cx, r2);
+      double* Tp = alloc(cx, (long long)QR_NB * r2);
+      double* Rr = alloc(cx, (long long)r2 * r2);
+      gemm(false, true, m, r2, r, 1.0, u, m, core, r2, 0.0, X, m);  // a.u @ core^T
+      qr_blocked(cx, m, r2, X, m, tau, Tp);
+      const int kr = min(m, r2);
+      for (long long e = threadIdx.x; e < (long long)kr * r2; e += NT) {
+        const int i = (int)(e % kr), j = (int)(e / kr);
+        Rr[e] = i <= j ? X[i + (long long)j * m] : 0.0;
+      }
+      for (long long e = threadIdx.x; e < (long long)m * kr; e += NT) ou[e] = ((e % m) == (e / m)) ? 1.0 : 0.0;
+      __syncthreads();
+      qr_apply(cx, m, kr, X, m, Tp, ou, m, kr, false);
+      gemm(false, true, n, kr, r2, 1.0, v2, n, Rr, kr, 0.0, ov, n);
+      add_flops(cx, FK_LR_MUL, mm_cost(m, r, r2) + qr_cost(m, r2) + mm_cost(n, r2, r2));
+      if (threadIdx.x == 0) *orank = kr;
+    }
+  }
+}
+
+// one level (or any contiguous range) of tiled tasks, one CTA per task
+__global__ void __launch_bounds__(NT, 2) k_tiled(const blrqr_task* tasks, long long t0, long long t1, blrqr_grid g,
+                                               blrqr_refl rf, double eps, double* ws, long long wsp, int* status,
+                                               unsigned long long* flops) {
+  Ctx cx = make_ctx(ws, wsp, status, flops);
+  for (long long t = t0 + blockIdx.x; t < t1; t += gridDim.x) {
+    const blrqr_task tk = tasks[t];
+    switch (tk.kind) {
+      case 0: tiled_diag(cx, g, rf, tk.k); break;
+      case 1: tiled_block(cx, g, rf, tk.k, tk.j); break;
+      case 2: tiled_update(cx, g, rf, tk.k, tk.i); break;
+      default: tiled_trap(cx, g, rf, eps, tk.k, tk.i, tk.j); break;
+    }
+    cx.top = 0;
+    __syncthreads();
+  }
+}
+
+
+// pack / unpack grid cells to a contiguous staging buffer (one CTA per cell):
+// dense cell: b*b column-major; LR cell: U (b x r) then V (b x r), r = rank.
+__global__ void __launch_bounds__(NT) k_grid_pack(blrqr_grid g, double* stage, const long long* stage_off,
+                                                   int to_grid) {
+  const int b = g.b;
+  for (int c = blockIdx.x; c < g.p * g.q; c += gridDim.x) {
+    const long long so = stage_off[c];
+    if (so < 0) continue;
+    double* st = stage + so;
+    if (g.lowrank[c]) {
+      const long long n = (long long)b * g.rank[c];
+      double* U = g.pool + g.off_u[c];
+      double* V = g.pool + g.off_v[c];
+      if (to_grid) {
+        for (long long e = threadIdx.x; e < n; e += NT) { U[e] = st[e]; V[e] = st[n + e]; }
+      } else {
+        for (long long e = threadIdx.x; e < n; e += NT) { st[e] = U[e]; st[n + e] = V[e]; }
+      }
+    } else {
+      double* D = g.pool + g.off_u[c];
+      const long long n = (long long)b * b;
+      if (to_grid) {
+        for (long long e = threadIdx.x; e < n; e += NT) D[e] = st[e];
+      } else {
+        for (long long e = threadIdx.x; e < n; e += NT) st[e] = D[e];
+      }
+    }
+  }
+}
+
+// ===========================================================================
+// host side
+// ===========================================================================
+
+extern "C" {
+
+int blrqr_version(void) { return 1; }
+
+int64_t blrqr_workspace_doubles(int b, int cap, int max_panel_rows) {
+  const int64_t B = b, C = cap, H = std::max(max_panel_rows, b);
+  return 16 * B * C + 4 * B * B + 2 * H * B + 64 * (B + 2 * C + H) + 65536;
+}
+
+int blrqr_default_ctas(void) {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return 2 * sms;
+}
+
+int blrqr_rounded_add_batched(int nbatch, int m, int n, const double* const* ua, const double* const* va,
+                              const int* ra, const double* const* ub, const double* const* vb, const int* rb,
+                              double* const* uo, double* const* vo, int* ro, int cap, double eps, double* ws,
+                              int64_t ws_per_cta, int nctas, int* status, unsigned long long* flops,
+                              void* stream) {
+  if (nbatch < 0 || m <= 0 || n <= 0 || cap < 0) return -1;
+  if (!(eps > 0.0 && eps < 1.0)) return -2;
+  if (nbatch == 0) return 0;
+  const int grid = std::max(1, std::min(nbatch, nctas));
+  k_rounded_add<<<grid, NT, 0, as_stream(stream)>>>(nbatch, m, n, ua, va, ra, ub, vb, rb, uo, vo, ro, cap, eps, ws,
+                                                   ws_per_cta, status, flops);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int blrqr_compress_batched(int nbatch, int m, int n, const double* const* a, double* const* uo,
+                           double* const* vo, int* ro, int cap, double eps, int max_rank, double* ws,
+                           int64_t ws_per_cta, int nctas, int* status, unsigned long long* flops, void* stream) {
+  if (nbatch < 0 || m <= 0 || n <= 0) return -1;
+  if (!(eps > 0.0 && eps < 1.0)) return -2;
+  if (nbatch == 0) return 0;
+  const int grid = std::max(1, std::min(nbatch, nctas));
+  k_compress<<<grid, NT, 0, as_stream(stream)>>>(nbatch, m, n, a, uo, vo, ro, cap, eps, max_rank, ws, ws_per_cta,
+                                                status, flops);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int blrqr_lr_product(int op, int m, int k, int n, const double* u, const double* v, int r, const double* d,
+                     const double* u2, const double* v2, int r2, double* out_u, double* out_v, int* out_r,
+                     double* ws, int64_t ws_doubles, int* status, unsigned long long* flops, void* stream) {
+  if (op < 0 || op > 3) return -1;
+  k_lr_product<<<1, NT, 0, as_stream(stream)>>>(op, m, k, n, u, v, r, d, u2, v2, r2, out_u, out_v, out_r, ws,
+                                               ws_doubles, status, flops);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int blrqr_geqrt(int m, int n, const double* a, double* y, double* t, double* r, double* ws, int64_t ws_doubles,
+                int* status, unsigned long long* flops, void* stream) {
+  if (m < n || n <= 0) return -1;
+  k_geqrt<<<1, NT, 0, as_stream(stream)>>>(m, n, a, y, t, r, ws, ws_doubles, status, flops);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int blrqr_apply_wy(int m, int n, int nc, const double* y, const double* t, double* c, int transpose, double* ws,
+                   int64_t ws_doubles, int* status, unsigned long long* flops, void* stream) {
+  if (m <= 0 || n <= 0 || nc < 0) return -1;
+  if (nc == 0) return 0;
+  k_apply_wy<<<1, NT, 0, as_stream(stream)>>>(m, n, nc, y, t, c, transpose, ws, ws_doubles, status, flops);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int blrqr_tpqrt(int n, int k, const double* r_top, const double* a_bot, double* r_new, double* y, double* t,
+                double* ws, int64_t ws_doubles, int* status, unsigned long long* flops, void* stream) {
+  if (n <= 0 || k < 0) return -1;
+  k_tpqrt<<<1, NT, 0, as_stream(stream)>>>(n, k, r_top, a_bot, r_new, y, t, ws, ws_doubles, status, flops);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int blrqr_apply_tp(int n, int k, int nc, const double* y, const double* t, double* c_top, double* c_bot,
+                   int transpose, double* ws, int64_t ws_doubles, int* status, unsigned long long* flops,
+                   void* stream) {
+  if (n <= 0 || k < 0 || nc < 0) return -1;
+  if (nc == 0) return 0;
+  k_apply_tp<<<1, NT, 0, as_stream(stream)>>>(n, k, nc, y, t, c_top, c_bot, transpose, ws, ws_doubles, status,
+                                             flops);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int blrqr_mgs_panel(int m, int n, const double* a, double* q, double* r, double* ws, int64_t ws_doubles,
+                    int* status, unsigned long long* flops, void* stream) {
+  if (m < n || n <= 0) return -1;
+  k_mgs_panel<<<1, NT, 0, as_stream(stream)>>>(m, n, a, q, r, ws, ws_doubles, status, flops);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int blrqr_dense_to_blr(const double* a, int64_t lda, blrqr_grid* g, unsigned char* lowrank_io, double eps,
+                       double fallback, double* ws, int64_t ws_per_cta, int nctas, int* status,
+                       unsigned long long* flops, void* stream) {
+  if (!g || g->b <= 0 || g->p <= 0 || g->q <= 0) return -1;
+  if (!(eps > 0.0 && eps < 1.0)) return -2;
+  const int max_rank = (int)(fallback * g->b);
+  const int cells = g->p * g->q;
+  const int grid = std::max(1, std::min(cells, nctas));
+  k_dense_to_blr<<<grid, NT, 0, as_stream(stream)>>>(a, lda, *g, lowrank_io, eps, max_rank, ws, ws_per_cta,
+                                                    status, flops);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// ---- tiled schedule: levels of the read/write-conflict DAG -------------
+
+static void tiled_access(const blrqr_task& t, std::vector<int64_t>& rd, std::vector<int64_t>& wr) {
+  // cell code: (tag << 40) | (i << 20) | j ; tags A=0, D=1, U=2
+  auto A = [](int i, int j) { return ((int64_t)0 << 40) | ((int64_t)i << 20) | j; };
+  auto D = [](int k) { return ((int64_t)1 << 40) | ((int64_t)k << 20) | k; };
+  auto U = [](int i, int k) { return ((int64_t)2 << 40) | ((int64_t)i << 20) | k; };
+  rd.clear();
+  wr.clear();
+  switch (t.kind) {
+    case 0: rd = {A(t.k, t.k)}; wr = {A(t.k, t.k), D(t.k)}; break;
+    case 1: rd = {D(t.k), A(t.k, t.j)}; wr = {A(t.k, t.j)}; break;
+    case 2: rd = {A(t.k, t.k), A(t.i, t.k)}; wr = {A(t.k, t.k), A(t.i, t.k), U(t.i, t.k)}; break;
+    default: rd = {U(t.i, t.k), A(t.k, t.j), A(t.i, t.j)}; wr = {A(t.k, t.j), A(t.i, t.j)}; break;
+  }
+}
+
+int64_t blrqr_tiled_task_count(int p, int q) {
+  if (q < 1 || p < q) return -1;
+  int64_t n = 0;
+  for (int k = 0; k < q; ++k) n += 1 + (q - k - 1) + (int64_t)(p - k - 1) * (1 + (q - k - 1));
+  return n;
+}
+
+int blrqr_tiled_schedule(int p, int q, blrqr_task* tasks_host, int64_t* level_start_host, int64_t max_levels) {
+  if (q < 1 || p < q) return -1;
+  std::vector<blrqr_task> tasks;
+  for (int k = 0; k < q; ++k) {
+    tasks.push_back({0, k, -1, -1});
+    for (int j = k + 1; j < q; ++j) tasks.push_back({1, k, -1, j});
+    for (int i = k + 1; i < p; ++i) {
+      tasks.push_back({2, k, i, -1});
+      for (int j = k + 1; j < q; ++j) tasks.push_back({3, k, i, j});
+    }
+  }
+  // level(t) = 1 + max level over its DAG predecessors: last writer of every
+  // touched cell, and readers since the last write of every written cell
+  std::unordered_map<int64_t, int> last_writer_level;
+  std::unordered_map<int64_t, int> readers_max_level;
+  std::vector<int> level(tasks.size());
+  std::vector<int64_t> rd, wr;
+  int nlev = 0;
+  for (size_t t = 0; t < tasks.size(); ++t) {
+    tiled_access(tasks[t], rd, wr);
+    int lv = 0;
+    auto touch = [&](int64_t c) {
+      auto it = last_writer_level.find(c);
+      if (it != last_writer_level.end()) lv = std::max(lv, it->second + 1);
+    };
+    for (auto c : rd) touch(c);
+    for (auto c : wr) {
+      touch(c);
+      auto it = readers_max_level.find(c);
+      if (it != readers_max_level.end()) lv = std::max(lv, it->second + 1);
+    }
+    level[t] = lv;
+    nlev = std::max(nlev, lv + 1);
+    for (auto c : wr) {
+      last_writer_level[c] = lv;
+      readers_max_level.erase(c);
+    }
+    for (auto c : rd) {
+      if (std::find(wr.begin(), wr.end(), c) != wr.end()) continue;
+      auto it = readers_max_level.find(c);
+      if (it == readers_max_level.end()) readers_max_level[c] = lv;
+      else it->second = std::max(it->second, lv);
+    }
+  }
+  if (nlev > max_levels) return -2;
+  // order: level, then critical kinds first (DiagQR, UpdateQR), then (k, i, j)
+  static const int prio[4] = {0, 2, 1, 2};
+  std::vector<size_t> idx(tasks.size());
+  for (size_t t = 0; t < idx.size(); ++t) idx[t] = t;
+  std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) {
+    const auto& x = tasks[a];
+    const auto& y = tasks[b];
+    return std::make_tuple(level[a], prio[x.kind], x.k, x.i, x.j) <
+           std::make_tuple(level[b], prio[y.kind], y.k, y.i, y.j);
+  });
+  int cur = -1;
+  for (size_t t = 0; t < idx.size(); ++t) {
+    tasks_host[t] = tasks[idx[t]];
+    const int lv = level[idx[t]];
+    while (cur < lv) level_start_host[++cur] = (int64_t)t;
+  }
+  level_start_host[nlev] = (int64_t)tasks.size();
+  return nlev;
+}
+
+int blrqr_tiled_run(const blrqr_grid* g, const blrqr_refl* rf, const blrqr_task* tasks_dev,
+                    const int64_t* level_start_host, int l0, int l1, double eps, double* ws, int64_t ws_per_cta,
+                    int nctas, int* status, unsigned long long* flops, void* stream) {
+  if (!g || !rf || !tasks_dev) return -1;
+  if (!(eps > 0.0 && eps < 1.0)) return -2;
+  for (int l = l0; l < l1; ++l) {
+    const int64_t t0 = level_start_host[l], t1 = level_start_host[l + 1];
+    if (t1 <= t0) continue;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(t1 - t0, nctas));
+    k_tiled<<<grid, NT, 0, as_stream(stream)>>>(tasks_dev, t0, t1, *g, *rf, eps, ws, ws_per_cta, status, flops);
+    CK(cudaGetLastError());
+  }
+  return 0;
+}
+
+int blrqr_grid_pack(const blrqr_grid* g, double* stage, const int64_t* stage_off, int to_grid, void* stream) {
+  if (!g || g->p <= 0 || g->q <= 0) return -1;
+  const int cells = g->p * g->q;
+  k_grid_pack<<<std::min(cells, 4096), NT, 0, as_stream(stream)>>>(*g, stage, (const long long*)stage_off, to_grid);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int blrqr_blocked_step(const blrqr_grid*, const blrqr_refl*, int, double, double*, int*, double*, int64_t, int,
+                       int*, unsigned long long*, void*) {
+  return -100;  // implemented below in a later revision
+}
+
+int blrqr_mgs_step(const blrqr_grid*, const blrqr_grid*, const blrqr_grid*, int, double, double*, int64_t, int,
+                   int*, unsigned long long*, void*) {
+  return -100;
+}
+
+}  // extern "C"

@@ -1,0 +1,261 @@
+// CTA-cooperative FP64 building blocks for the BLR-QR kernels (sm_100a).
+//
+// Every routine here is called by ALL threads of a CTA (blockDim.x == NT) and
+// ends with the CTA synchronised.  Matrices are column-major with explicit
+// leading dimensions; pointers are generic, so operands may live in global
+// memory (HBM / L2) or in shared memory.  Per-CTA scratch comes from a bump
+// arena (Arena) carved out of a caller-provided global workspace.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace blr {
+
+constexpr int NT = 256;          // threads per CTA
+constexpr int NWARP = NT / 32;
+
+// status bits (OR-ed into a device word; see include/blrqr.h)
+constexpr int ST_RANK_OVERFLOW = 1;
+constexpr int ST_ARENA_OVERFLOW = 2;
+constexpr int ST_NONFINITE = 4;
+constexpr int ST_MGS_COLLAPSE = 8;
+constexpr int ST_BAD_KIND = 16;
+constexpr int ST_BAD_ARG = 32;
+
+// model-flop categories (flops.py kinds)
+enum FlopKind : int {
+  FK_COMPRESS = 0, FK_ROUNDED_ADD, FK_EXPAND, FK_LR_MUL, FK_GEMM, FK_PANEL_QR,
+  FK_APPLY_WY, FK_UPDATE_QR, FK_APPLY_TP, FK_COUNT
+};
+
+struct Ctx {
+  double* base;            // this CTA's arena
+  long long cap;           // doubles
+  long long top;           // bump pointer (doubles), identical in all threads
+  int* status;             // global status word
+  unsigned long long* flops;  // FK_COUNT counters (global)
+};
+
+__device__ __forceinline__ void set_status(Ctx& c, int bits) {
+  if (threadIdx.x == 0) atomicOr(c.status, bits);
+}
+__device__ __forceinline__ void add_flops(Ctx& c, int kind, long long n) {
+  if (threadIdx.x == 0 && c.flops) atomicAdd(c.flops + kind, (unsigned long long)n);
+}
+
+// Arena allocation: every thread executes it with identical arguments.
+// Returns nullptr (and flags ST_ARENA_OVERFLOW) if the arena is exhausted.
+__device__ __forceinline__ double* alloc(Ctx& c, long long n) {
+  n = (n + 31) & ~31LL;    // 256-byte alignment
+  if (c.top + n > c.cap) {
+    set_status(c, ST_ARENA_OVERFLOW);
+    return nullptr;
+  }
+  double* p = c.base + c.top;
+  c.top += n;
+  return p;
+}
+
+// closed-form model costs (flops.py:28-55)
+__device__ __forceinline__ long long qr_cost(long long h, long long w) { return 2 * h * w * w - (2 * w * w * w) / 3; }
+__device__ __forceinline__ long long tgen_cost(long long h, long long w) { return h * w * w; }
+__device__ __forceinline__ long long mm_cost(long long m, long long k, long long n) { return 2 * m * k * n; }
+__device__ __forceinline__ long long svd_cost(long long c) { return 12 * c * c * c; }
+__device__ __forceinline__ long long mgs_cost(long long h, long long w) { return 2 * h * w * w; }
+__device__ __forceinline__ long long rrqr_cost(long long r, long long c, long long k) { return 4 * r * c * k + 2 * r * c; }
+
+// ---------------------------------------------------------------------------
+// reductions
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// CTA-wide sum; result returned to every thread.  Uses its own smem slot.
+__device__ __forceinline__ double cta_sum(double v) {
+  __shared__ double red[NWARP];
+  __shared__ double out;
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    double x = l < NWARP ? red[l] : 0.0;
+    x = warp_sum(x);
+    if (l == 0) out = x;
+  }
+  __syncthreads();
+  double r = out;
+  __syncthreads();
+  return r;
+}
+
+// CTA-wide argmax over (val, idx); ties resolve to the LOWEST index
+// (numpy.argmax semantics, lowrank.py:97).  Returns idx in every thread.
+__device__ __forceinline__ int cta_argmax(double v, int idx) {
+  __shared__ double rv[NWARP];
+  __shared__ int ri[NWARP];
+  __shared__ int out;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+    int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (v2 > v || (v2 == v && i2 < idx)) { v = v2; idx = i2; }
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) { rv[w] = v; ri[w] = idx; }
+  __syncthreads();
+  if (w == 0) {
+    double x = l < NWARP ? rv[l] : -INFINITY;
+    int xi = l < NWARP ? ri[l] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double v2 = __shfl_xor_sync(0xffffffffu, x, o);
+      int i2 = __shfl_xor_sync(0xffffffffu, xi, o);
+      if (v2 > x || (v2 == x && i2 < xi)) { x = v2; xi = i2; }
+    }
+    if (l == 0) out = xi;
+  }
+  __syncthreads();
+  int r = out;
+  __syncthreads();
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// elementwise helpers
+// ---------------------------------------------------------------------------
+
+// B(0:m,0:n) = alpha * A(0:m,0:n)
+__device__ void copy_mat(int m, int n, const double* A, int lda, double* B, int ldb, double alpha = 1.0) {
+  const long long tot = (long long)m * n;
+  for (long long e = threadIdx.x; e < tot; e += NT) {
+    int i = (int)(e % m), j = (int)(e / m);
+    B[i + (long long)j * ldb] = alpha * A[i + (long long)j * lda];
+  }
+  __syncthreads();
+}
+
+__device__ void zero_mat(int m, int n, double* A, int lda) {
+  const long long tot = (long long)m * n;
+  for (long long e = threadIdx.x; e < tot; e += NT) {
+    int i = (int)(e % m), j = (int)(e / m);
+    A[i + (long long)j * lda] = 0.0;
+  }
+  __syncthreads();
+}
+
+// B = A^T (A is m x n)
+__device__ void transpose_mat(int m, int n, const double* A, int lda, double* B, int ldb) {
+  const long long tot = (long long)m * n;
+  for (long long e = threadIdx.x; e < tot; e += NT) {
+    int j = (int)(e % n), i = (int)(e / n);
+    B[j + (long long)i * ldb] = A[i + (long long)j * lda];
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// GEMM: C = alpha * op(A) * op(B) + beta * C   (M x N, inner K)
+// op(A): ta ? A^T : A ; op(B): tb ? B^T : B.  beta == 0 never reads C.
+// Shared-memory tiled DFMA; tile shape chosen from N.
+// ---------------------------------------------------------------------------
+
+constexpr int GEMM_SMEM = 4400;  // doubles of shared scratch shared by all GEMM tile shapes
+__device__ __forceinline__ double* gemm_smem() {
+  __shared__ double buf[GEMM_SMEM];
+  return buf;
+}
+
+template <int BM, int BN, int BK>
+__device__ __noinline__ void gemm_tiled(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, int lda,
+                           const double* B, int ldb, double beta, double* C, int ldc) {
+  constexpr int TY = (BM >= 16 ? 16 : BM), TX = NT / TY;  // thread grid TY x TX
+  constexpr int TM = BM / TY, TN = BN / TX;
+  static_assert(TM * TN * NT == BM * BN, "tile");
+  static_assert(BK * (BM + 1) + BK * (BN + 1) <= GEMM_SMEM, "smem");
+  double (*sA)[BM + 1] = reinterpret_cast<double (*)[BM + 1]>(gemm_smem());
+  double (*sB)[BN + 1] = reinterpret_cast<double (*)[BN + 1]>(gemm_smem() + BK * (BM + 1));
+  const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
+  const int tilesM = (M + BM - 1) / BM, tilesN = (N + BN - 1) / BN;
+  for (int tile = 0; tile < tilesM * tilesN; ++tile) {
+    const int m0 = (tile % tilesM) * BM, n0 = (tile / tilesM) * BN;
+    double acc[TM][TN];
+#pragma unroll
+    for (int a = 0; a < TM; ++a)
+#pragma unroll
+      for (int b = 0; b < TN; ++b) acc[a][b] = 0.0;
+    for (int k0 = 0; k0 < K; k0 += BK) {
+      // load A tile: op(A)[m0:m0+BM, k0:k0+BK] -> sA[k][m]
+      for (int e = threadIdx.x; e < BM * BK; e += NT) {
+        int mm, kk;
+        if (ta) { kk = e % BK; mm = e / BK; } else { mm = e % BM; kk = e / BM; }
+        const int gm = m0 + mm, gk = k0 + kk;
+        double v = 0.0;
+        if (gm < M && gk < K) v = ta ? A[gk + (long long)gm * lda] : A[gm + (long long)gk * lda];
+        sA[kk][mm] = v;
+      }
+      for (int e = threadIdx.x; e < BN * BK; e += NT) {
+        int nn, kk;
+        if (tb) { nn = e % BN; kk = e / BN; } else { kk = e % BK; nn = e / BK; }
+        const int gn = n0 + nn, gk = k0 + kk;
+        double v = 0.0;
+        if (gn < N && gk < K) v = tb ? B[gn + (long long)gk * ldb] : B[gk + (long long)gn * ldb];
+        sB[kk][nn] = v;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < BK; ++kk) {
+        double ra[TM], rb[TN];
+#pragma unroll
+        for (int a = 0; a < TM; ++a) ra[a] = sA[kk][ty + TY * a];
+#pragma unroll
+        for (int b = 0; b < TN; ++b) rb[b] = sB[kk][tx + TX * b];
+#pragma unroll
+        for (int a = 0; a < TM; ++a)
+#pragma unroll
+          for (int b = 0; b < TN; ++b) acc[a][b] = fma(ra[a], rb[b], acc[a][b]);
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int a = 0; a < TM; ++a)
+#pragma unroll
+      for (int b = 0; b < TN; ++b) {
+        const int gm = m0 + ty + TY * a, gn = n0 + tx + TX * b;
+        if (gm < M && gn < N) {
+          double* c = C + gm + (long long)gn * ldc;
+          *c = beta == 0.0 ? alpha * acc[a][b] : alpha * acc[a][b] + beta * (*c);
+        }
+      }
+  }
+  __syncthreads();
+}
+
+__device__ __noinline__ void gemm(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, int lda,
+                     const double* B, int ldb, double beta, double* C, int ldc) {
+  if (M <= 0 || N <= 0) return;
+  if (K <= 0) {  // C = beta * C
+    const long long tot = (long long)M * N;
+    for (long long e = threadIdx.x; e < tot; e += NT) {
+      int i = (int)(e % M), j = (int)(e / M);
+      double* c = C + i + (long long)j * ldc;
+      *c = beta == 0.0 ? 0.0 : beta * (*c);
+    }
+    __syncthreads();
+    return;
+  }
+  if (M <= 16 && N > 64)
+    gemm_tiled<16, 256, 16>(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else if (N <= 16)
+    gemm_tiled<256, 16, 16>(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else if (N <= 32 || M >= 4 * N)
+    gemm_tiled<128, 32, 16>(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else
+    gemm_tiled<64, 64, 16>(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+}
+
+}  // namespace blr

@@ -1,0 +1,279 @@
+// CTA-level Householder machinery (LAPACK conventions, SURVEY §7 "guiding
+// constraint"): reflector generation with beta = -sign(x0)*||x|| and tau = 0
+// for a zero tail (lowrank.py:44-61, LAPACK dlarfg), blocked QR with
+// per-panel compact-WY T factors, forward-columnwise T accumulation over the
+// whole panel (dgeqrt with nb = n, kernels.py:96), triangular-pentagonal QR
+// (dtpqrt with l = 0, kernels.py:148), and WY applications.
+#pragma once
+#include "device_core.cuh"
+
+namespace blr {
+
+constexpr int QR_NB = 32;  // panel width of the blocked factorizations
+
+// Householder reflector for x = [alpha; X(0:n)] (X strided).  On exit X holds
+// v(1:), returns (tau, beta) via refs.  All threads call; result uniform.
+__device__ void house_gen(double alpha, double* X, int n, long long incx, double& tau, double& beta) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += NT) {
+    double x = X[i * incx];
+    s = fma(x, x, s);
+  }
+  const double xn2 = cta_sum(s);
+  if (xn2 == 0.0) {
+    tau = 0.0;
+    beta = alpha;
+    return;
+  }
+  const double mu = sqrt(alpha * alpha + xn2);
+  beta = alpha >= 0.0 ? -mu : mu;
+  tau = (beta - alpha) / beta;
+  const double scal = 1.0 / (alpha - beta);
+  for (int i = threadIdx.x; i < n; i += NT) X[i * incx] *= scal;
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Unblocked QR of the panel A(r0:m, c0:c0+w) applied also to columns up to
+// c0+w (only panel columns).  Reflectors stored below the diagonal, tau[c].
+// ---------------------------------------------------------------------------
+__device__ __noinline__ void qr_panel_unblocked(int m, int c0, int w, double* A, int lda, double* tau) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int jj = 0; jj < w; ++jj) {
+    const int j = c0 + jj;  // diagonal (j, j)
+    if (j >= m) {           // wide matrix: no more reflectors
+      if (threadIdx.x == 0) tau[j] = 0.0;
+      __syncthreads();
+      continue;
+    }
+    double* col = A + (long long)j * lda;
+    double t, bta;
+    house_gen(col[j], col + j + 1, m - j - 1, 1, t, bta);
+    if (threadIdx.x == 0) { tau[j] = t; col[j] = bta; }
+    __syncthreads();
+    if (t != 0.0) {
+      // A(j:m, l) -= t * v * (v^T A(j:m, l)),  v = [1; col(j+1:m)]
+      for (int l = c0 + jj + 1 + warp; l < c0 + w; l += NWARP) {
+        double* cl = A + (long long)l * lda;
+        double d = 0.0;
+        for (int i = j + 1 + lane; i < m; i += 32) d = fma(col[i], cl[i], d);
+        d = warp_sum(d) + cl[j];
+        d *= t;
+        if (lane == 0) cl[j] -= d;
+        for (int i = j + 1 + lane; i < m; i += 32) cl[i] = fma(-d, col[i], cl[i]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Copy reflectors of panel columns [c0, c0+w) into Y (rows r0=c0 .. m-1,
+// ldy) as an explicit unit-lower-trapezoidal block: Y(i, jj) for i in [0, m-c0).
+__device__ void extract_y(int m, int c0, int w, const double* A, int lda, double* Y, int ldy) {
+  const int h = m - c0;
+  const long long tot = (long long)h * w;
+  for (long long e = threadIdx.x; e < tot; e += NT) {
+    const int i = (int)(e % h), jj = (int)(e / h);
+    double v;
+    if (i < jj) v = 0.0;
+    else if (i == jj) v = 1.0;
+    else v = A[(c0 + i) + (long long)(c0 + jj) * lda];
+    Y[i + (long long)jj * ldy] = v;
+  }
+  __syncthreads();
+}
+
+// T recurrence inside one block of columns [j0, j0+w) of the full T (ldt):
+// T(j0+c, j0+c) = tau ; T(j0:j0+c, j0+c) = -tau * T(j0:j0+c, j0:j0+c) * S(j0:j0+c, j0+c)
+// where S holds the inner products V^T V (upper part used, lds).
+__device__ void t_block_recurrence(int j0, int w, const double* S, int lds, const double* tau, double* T, int ldt) {
+  __shared__ double tmp[QR_NB];
+  for (int c = 0; c < w; ++c) {
+    const int jc = j0 + c;
+    const double tc = tau[jc];
+    // tmp[a] = sum_{b=a}^{c-1} T(j0+a, j0+b) * S(j0+b, jc)   (T upper triangular)
+    if (threadIdx.x < c) {
+      const int a = threadIdx.x;
+      double s = 0.0;
+      for (int b2 = a; b2 < c; ++b2) s = fma(T[(j0 + a) + (long long)(j0 + b2) * ldt], S[(j0 + b2) + (long long)jc * lds], s);
+      tmp[a] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < c) T[(j0 + threadIdx.x) + (long long)jc * ldt] = -tc * tmp[threadIdx.x];
+    if (threadIdx.x == 0) T[jc + (long long)jc * ldt] = tc;
+    for (int a = c + 1 + threadIdx.x; a < w; a += NT) T[(j0 + a) + (long long)jc * ldt] = 0.0;  // below diag
+    __syncthreads();
+  }
+}
+
+// Full n x n forward-columnwise T from S = V^T V (upper part) and tau, built
+// blockwise: T_JJ by recurrence, T(0:J0, J) = -T(0:J0,0:J0) S(0:J0,J) T_JJ.
+// Needs scratch of n*QR_NB doubles.  Lower triangle of T set to zero.
+__device__ __noinline__ void build_t_full(Ctx& cx, int n, const double* S, int lds, const double* tau, double* T, int ldt) {
+  const long long mark = cx.top;
+  double* X = alloc(cx, (long long)n * QR_NB);
+  if (!X) return;
+  for (int j0 = 0; j0 < n; j0 += QR_NB) {
+    const int w = min(QR_NB, n - j0);
+    t_block_recurrence(j0, w, S, lds, tau, T, ldt);
+    // zero T(J, 0:j0) (strict lower blocks left of the diagonal block)
+    for (long long e = threadIdx.x; e < (long long)w * j0; e += NT) {
+      const int a = (int)(e % w), c = (int)(e / w);
+      T[(j0 + a) + (long long)c * ldt] = 0.0;
+    }
+    if (j0 > 0) {
+      // X = S(0:j0, J) * T_JJ   (j0 x w)
+      gemm(false, false, j0, w, w, 1.0, S + (long long)j0 * lds, lds, T + j0 + (long long)j0 * ldt, ldt, 0.0, X, j0);
+      // T(0:j0, J) = -T(0:j0, 0:j0) * X
+      gemm(false, false, j0, w, j0, -1.0, T, ldt, X, j0, 0.0, T + (long long)j0 * ldt, ldt);
+    }
+    __syncthreads();
+  }
+  cx.top = mark;
+}
+
+// ---------------------------------------------------------------------------
+// Blocked Householder QR of A (m x n, any shape).  k = min(m, n) reflectors.
+// On exit: R in the upper triangle, reflectors below, tau[0:k] (tau[j] = 0 for
+// j >= m), and per-panel T factors: Tp (QR_NB x k, panel p at column p*QR_NB,
+// ld QR_NB) holding the panel's own compact-WY T (for fast applications).
+// ---------------------------------------------------------------------------
+__device__ __noinline__ void qr_blocked(Ctx& cx, int m, int n, double* A, int lda, double* tau, double* Tp) {
+  const int k = min(m, n);
+  const long long mark = cx.top;
+  double* Y = alloc(cx, (long long)m * QR_NB);
+  double* S = alloc(cx, (long long)QR_NB * QR_NB);
+  double* W = alloc(cx, (long long)QR_NB * max(n, 1));
+  if (!Y || !S || !W) { cx.top = mark; return; }
+  for (int c0 = 0; c0 < k; c0 += QR_NB) {
+    const int w = min(QR_NB, k - c0);
+    qr_panel_unblocked(m, c0, w, A, lda, tau);
+    const int h = m - c0;
+    extract_y(m, c0, w, A, lda, Y, h);
+    // panel T: S = Y^T Y, recurrence
+    gemm(true, false, w, w, h, 1.0, Y, h, Y, h, 0.0, S, QR_NB);
+    double* T = Tp + (long long)c0 * QR_NB;
+    t_block_recurrence(0, w, S, QR_NB, tau + c0, T, QR_NB);
+    const int n2 = n - (c0 + w);
+    if (n2 > 0) {
+      double* A2 = A + c0 + (long long)(c0 + w) * lda;
+      // A2 = (I - Y T Y^T)^T A2 = A2 - Y T^T (Y^T A2)
+      gemm(true, false, w, n2, h, 1.0, Y, h, A2, lda, 0.0, W, QR_NB);
+      // W2 = T^T W computed in place column by column (T upper => T^T lower)
+      for (long long e = threadIdx.x; e < (long long)n2; e += NT) {
+        double* wc = W + e * QR_NB;
+        double tmp[QR_NB];
+#pragma unroll 4
+        for (int a = 0; a < w; ++a) tmp[a] = wc[a];
+        for (int a = w - 1; a >= 0; --a) {
+          double s = 0.0;
+          for (int b2 = 0; b2 <= a; ++b2) s = fma(T[b2 + a * QR_NB], tmp[b2], s);
+          wc[a] = s;
+        }
+      }
+      __syncthreads();
+      gemm(false, false, h, n2, w, -1.0, Y, h, W, QR_NB, 1.0, A2, lda);
+    }
+  }
+  cx.top = mark;
+}
+
+// Apply Q = H_0 H_1 ... H_{k-1} (from qr_blocked of an m-row matrix) to Z
+// (m x nz): Z <- Q Z   (transpose=false)   or   Z <- Q^T Z (transpose=true).
+__device__ __noinline__ void qr_apply(Ctx& cx, int m, int k, const double* A, int lda, const double* Tp, double* Z, int ldz,
+                         int nz, bool transpose) {
+  if (nz <= 0 || k <= 0) return;
+  const long long mark = cx.top;
+  double* Y = alloc(cx, (long long)m * QR_NB);
+  double* W = alloc(cx, (long long)QR_NB * nz);
+  double* W2 = alloc(cx, (long long)QR_NB * nz);
+  if (!Y || !W || !W2) { cx.top = mark; return; }
+  const int np = (k + QR_NB - 1) / QR_NB;
+  for (int pi = 0; pi < np; ++pi) {
+    const int p = transpose ? pi : np - 1 - pi;
+    const int c0 = p * QR_NB, w = min(QR_NB, k - c0), h = m - c0;
+    extract_y(m, c0, w, A, lda, Y, h);
+    const double* T = Tp + (long long)c0 * QR_NB;
+    double* Zp = Z + c0;
+    gemm(true, false, w, nz, h, 1.0, Y, h, Zp, ldz, 0.0, W, QR_NB);
+    // W2 = op(T) W
+    gemm(transpose, false, w, nz, w, 1.0, T, QR_NB, W, QR_NB, 0.0, W2, QR_NB);
+    gemm(false, false, h, nz, w, -1.0, Y, h, W2, QR_NB, 1.0, Zp, ldz);
+  }
+  cx.top = mark;
+}
+
+// ---------------------------------------------------------------------------
+// Triangular-pentagonal QR, l = 0 (LAPACK dtpqrt semantics): [R; B] with R
+// n x n upper triangular, B k x n.  On exit R = R_new, B = Y (k x n), T full
+// n x n upper (ldt).
+// ---------------------------------------------------------------------------
+__device__ __noinline__ void tpqrt(Ctx& cx, int n, int k, double* R, int ldr, double* B, int ldb, double* T, int ldt) {
+  const long long mark = cx.top;
+  double* tau = alloc(cx, n);
+  double* S = alloc(cx, (long long)n * n);
+  double* W = alloc(cx, (long long)QR_NB * n);
+  if (!tau || !S || !W) { cx.top = mark; return; }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int c0 = 0; c0 < n; c0 += QR_NB) {
+    const int w = min(QR_NB, n - c0);
+    for (int jj = 0; jj < w; ++jj) {
+      const int j = c0 + jj;
+      double* bj = B + (long long)j * ldb;
+      double t, bta;
+      house_gen(R[j + (long long)j * ldr], bj, k, 1, t, bta);
+      if (threadIdx.x == 0) { tau[j] = t; R[j + (long long)j * ldr] = bta; }
+      __syncthreads();
+      if (t != 0.0) {
+        for (int l = j + 1 + warp; l < c0 + w; l += NWARP) {
+          double* bl = B + (long long)l * ldb;
+          double d = 0.0;
+          for (int i = lane; i < k; i += 32) d = fma(bj[i], bl[i], d);
+          d = (warp_sum(d) + R[j + (long long)l * ldr]) * t;
+          if (lane == 0) R[j + (long long)l * ldr] -= d;
+          for (int i = lane; i < k; i += 32) bl[i] = fma(-d, bj[i], bl[i]);
+        }
+      }
+      __syncthreads();
+    }
+    // panel T (w x w) into T's diagonal block, from S_J = Y_J^T Y_J
+    gemm(true, false, w, w, k, 1.0, B + (long long)c0 * ldb, ldb, B + (long long)c0 * ldb, ldb, 0.0,
+         S + c0 + (long long)c0 * n, n);
+    t_block_recurrence(c0, w, S, n, tau, T, ldt);
+    const int n2 = n - (c0 + w);
+    if (n2 > 0) {
+      double* RJL = R + c0 + (long long)(c0 + w) * ldr;
+      double* BL = B + (long long)(c0 + w) * ldb;
+      const double* YJ = B + (long long)c0 * ldb;
+      const double* TJ = T + c0 + (long long)c0 * ldt;
+      // W = R_JL + Y_J^T B_L
+      copy_mat(w, n2, RJL, ldr, W, QR_NB);
+      gemm(true, false, w, n2, k, 1.0, YJ, ldb, BL, ldb, 1.0, W, QR_NB);
+      // W <- T_J^T W  (in place, per column)
+      for (long long e = threadIdx.x; e < (long long)n2; e += NT) {
+        double* wc = W + e * QR_NB;
+        double tmp[QR_NB];
+        for (int a = 0; a < w; ++a) tmp[a] = wc[a];
+        for (int a = w - 1; a >= 0; --a) {
+          double s = 0.0;
+          for (int b2 = 0; b2 <= a; ++b2) s = fma(TJ[b2 + (long long)a * ldt], tmp[b2], s);
+          wc[a] = s;
+        }
+      }
+      __syncthreads();
+      // R_JL -= W ; B_L -= Y_J W
+      for (long long e = threadIdx.x; e < (long long)w * n2; e += NT) {
+        const int a = (int)(e % w), c = (int)(e / w);
+        RJL[a + (long long)c * ldr] -= W[a + (long long)c * QR_NB];
+      }
+      __syncthreads();
+      gemm(false, false, k, n2, w, -1.0, YJ, ldb, W, QR_NB, 1.0, BL, ldb);
+    }
+  }
+  // full T: S = Y^T Y (upper blocks needed), then blocked combine
+  gemm(true, false, n, n, k, 1.0, B, ldb, B, ldb, 0.0, S, n);
+  build_t_full(cx, n, S, n, tau, T, ldt);
+  cx.top = mark;
+}
+
+}  // namespace blr

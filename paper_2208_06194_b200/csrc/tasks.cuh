@@ -1,0 +1,156 @@
+// Task-level device code: one CTA executes one block task of a BLR-QR
+// factorization exactly in the reference's operation order
+// (factorize.py:187-262 blocked, :379-444 tiled, :605-655 MGS).
+#pragma once
+#include "blockops.cuh"
+#include "../../include/blrqr.h"
+
+namespace blr {
+
+__device__ __forceinline__ Cell grid_cell(const blrqr_grid& g, int i, int j) {
+  const long long c = (long long)i * g.q + j;
+  Cell x;
+  x.lr = g.lowrank[c];
+  x.rank = g.rank + c;
+  x.u = g.pool + g.off_u[c];
+  x.v = x.lr ? g.pool + g.off_v[c] : nullptr;
+  x.ld = g.b;
+  x.cap = g.cap;
+  x.b = g.b;
+  return x;
+}
+
+__device__ __forceinline__ Ctx make_ctx(double* ws, long long ws_per_cta, int* status, unsigned long long* flops) {
+  Ctx c;
+  c.base = ws + (long long)blockIdx.x * ws_per_cta;
+  c.cap = ws_per_cta;
+  c.top = 0;
+  c.status = status;
+  c.flops = flops;
+  return c;
+}
+
+// Reflector block Ytilde_ik (LR aliasing the (i,k) cell slabs, or dense).
+__device__ __forceinline__ Blk refl_blk(const blrqr_grid& g, const blrqr_refl& rf, int i, int k) {
+  const long long c = (long long)i * g.q + k;
+  const int yr = rf.yrank[c];
+  if (yr >= 0) return make_lr(g.b, g.b, yr, g.pool + g.off_u[c], g.b, g.pool + g.off_v[c], g.b, 1.0);
+  return make_dense(g.b, g.b, rf.pool + rf.y_off[c], g.b, 1.0);
+}
+
+// ---------------------------------------------------------------------------
+// GEQRT of an m x n panel held in A (lda) in place -> Y explicit (m x n, ldy),
+// T full (n x n, ldt), R left in the upper triangle of A (below zeroed).
+// kernels.py:87-103 (dgeqrt with nb = n).
+// ---------------------------------------------------------------------------
+__device__ void geqrt_inplace(Ctx& cx, int m, int n, double* A, int lda, double* Y, int ldy, double* T, int ldt) {
+  const long long mark = cx.top;
+  double* tau = alloc(cx, n);
+  double* Tp = alloc(cx, (long long)QR_NB * n);
+  double* S = alloc(cx, (long long)n * n);
+  if (!tau || !Tp || !S) { cx.top = mark; return; }
+  qr_blocked(cx, m, n, A, lda, tau, Tp);
+  // Y explicit unit-lower-trapezoidal; zero A below the diagonal
+  for (long long e = threadIdx.x; e < (long long)m * n; e += NT) {
+    const int i = (int)(e % m), j = (int)(e / m);
+    double* a = A + i + (long long)j * lda;
+    double y;
+    if (i < j) y = 0.0;
+    else if (i == j) y = 1.0;
+    else { y = *a; *a = 0.0; }
+    Y[i + (long long)j * ldy] = y;
+  }
+  __syncthreads();
+  gemm(true, false, n, n, m, 1.0, Y, ldy, Y, ldy, 0.0, S, n);
+  build_t_full(cx, n, S, n, tau, T, ldt);
+  add_flops(cx, FK_PANEL_QR, qr_cost(m, n) + tgen_cost(m, n));
+  cx.top = mark;
+}
+
+// c <- c - Y op(T) (Y^T c)   (kernels.py:111-128); Y m x n, c m x nc
+__device__ void apply_wy_dev(Ctx& cx, int m, int n, int nc, const double* Y, int ldy, const double* T, int ldt,
+                             double* C, int ldc, bool transpose) {
+  if (nc <= 0) return;
+  const long long mark = cx.top;
+  double* W = alloc(cx, (long long)n * nc);
+  double* W2 = alloc(cx, (long long)n * nc);
+  if (!W || !W2) { cx.top = mark; return; }
+  gemm(true, false, n, nc, m, 1.0, Y, ldy, C, ldc, 0.0, W, n);
+  gemm(transpose, false, n, nc, n, 1.0, T, ldt, W, n, 0.0, W2, n);
+  gemm(false, false, m, nc, n, -1.0, Y, ldy, W2, n, 1.0, C, ldc);
+  add_flops(cx, FK_APPLY_WY, mm_cost(n, m, nc) + mm_cost(n, n, nc) + mm_cost(m, n, nc));
+  cx.top = mark;
+}
+
+// ---------------------------------------------------------------------------
+// tiled tasks (factorize.py:379-422, 428-444)
+// ---------------------------------------------------------------------------
+
+__device__ void tiled_diag(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, int k) {
+  Cell a = grid_cell(g, k, k);
+  if (a.lr) { set_status(cx, ST_BAD_KIND); return; }
+  const long long c = (long long)k * g.q + k;
+  geqrt_inplace(cx, g.b, g.b, a.u, a.ld, rf.pool + rf.y_off[c], g.b, rf.pool + rf.t_off[c], g.b);
+}
+
+__device__ void tiled_block(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, int k, int j) {
+  const long long c = (long long)k * g.q + k;
+  const double* Y = rf.pool + rf.y_off[c];
+  const double* T = rf.pool + rf.t_off[c];
+  Cell x = grid_cell(g, k, j);
+  if (x.lr) {
+    const int r = *x.rank;
+    if (r) apply_wy_dev(cx, g.b, g.b, r, Y, g.b, T, g.b, x.u, x.ld, true);
+  } else {
+    apply_wy_dev(cx, g.b, g.b, g.b, Y, g.b, T, g.b, x.u, x.ld, true);
+  }
+}
+
+__device__ void tiled_update(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, int k, int i) {
+  const int b = g.b;
+  Cell rk = grid_cell(g, k, k);
+  Cell x = grid_cell(g, i, k);
+  const long long c = (long long)i * g.q + k;
+  double* T = rf.pool + rf.t_off[c];
+  const long long mark = cx.top;
+  if (x.lr) {
+    const int r = *x.rank;
+    if (r == 0) {  // tp_qr with an empty bottom: identity reflector (kernels.py:146-147)
+      zero_mat(b, b, T, b);
+    } else {
+      double* B = alloc(cx, (long long)r * b);
+      if (!B) return;
+      transpose_mat(b, r, x.v, x.ld, B, r);          // B = V_ik^T (r x b)
+      tpqrt(cx, b, r, rk.u, rk.ld, B, r, T, b);
+      transpose_mat(r, b, B, r, x.v, x.ld);          // Ytilde.v = Y^T stored in the V slab
+      add_flops(cx, FK_UPDATE_QR, qr_cost(b + r, b) + tgen_cost(b + r, b));
+    }
+    if (threadIdx.x == 0) { rf.yrank[c] = r; *x.rank = 0; }
+  } else {
+    double* Yd = rf.pool + rf.y_off[c];
+    copy_mat(b, b, x.u, x.ld, Yd, b);
+    tpqrt(cx, b, b, rk.u, rk.ld, Yd, b, T, b);
+    zero_mat(b, b, x.u, x.ld);
+    add_flops(cx, FK_UPDATE_QR, qr_cost(2 * b, b) + tgen_cost(2 * b, b));
+    if (threadIdx.x == 0) rf.yrank[c] = -1;
+  }
+  __syncthreads();
+  cx.top = mark;
+}
+
+__device__ void tiled_trap(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, double eps, int k, int i, int j) {
+  const long long mark = cx.top;
+  const Blk yt = refl_blk(g, rf, i, k);
+  const double* T = rf.pool + rf.t_off[(long long)i * g.q + k];
+  Cell top = grid_cell(g, k, j), bot = grid_cell(g, i, j);
+  const Blk tb = cell_blk(top), bb = cell_blk(bot);
+  Blk prod = blk_mul_t(cx, yt, bb);
+  Blk ssum = blk_acc(cx, tb, prod, eps, g.b);
+  Blk w = blk_dense_times(cx, T, g.b, true, ssum);
+  sub_into_cell(cx, top, w, eps);
+  Blk yw = blk_mul(cx, yt, w);
+  sub_into_cell(cx, bot, yw, eps);
+  cx.top = mark;
+}
+
+}  // namespace blr

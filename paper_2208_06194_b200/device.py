@@ -1,0 +1,202 @@
+"""Device-resident BLR grid and reflector stores (HBM layout).
+
+Layout: one FP64 pool per grid; cell (i, j) owns
+  dense cell : b*b doubles, column-major, at off_u[c]
+  low-rank   : U (b x cap) at off_u[c], V (b x cap) at off_v[c] = off_u[c] + b*cap
+plus an int32 rank per cell and a uint8 kind map.  cap defaults to b, so no
+update can overflow; smaller caps trade memory for an overflow check.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import BlrMatrix, BlrStructure, LowRankBlock, is_lowrank
+
+
+def _f(a: np.ndarray) -> np.ndarray:
+    """column-major flat copy of a 2-D array"""
+    return np.asarray(a, dtype=np.float64).ravel(order="F")
+
+
+class DeviceGrid:
+    """p x q BLR grid resident on the GPU."""
+
+    def __init__(self, m: int, n: int, b: int, lowrank: np.ndarray, cap: int | None = None,
+                 min_lr_slab: int = 0):
+        rt = _lib.runtime()
+        self.m, self.n, self.b = m, n, b
+        self.p, self.q = m // b, n // b
+        self.cap = int(cap if cap is not None else b)
+        kind = np.asarray(lowrank, dtype=bool)
+        self.kind_host = kind.copy()
+        lr_slab = max(2 * b * self.cap, min_lr_slab)
+        sizes = np.where(kind.ravel(), lr_slab, b * b).astype(np.int64)
+        off = np.zeros(self.p * self.q, dtype=np.int64)
+        off[1:] = np.cumsum(sizes)[:-1]
+        offv = np.where(kind.ravel(), off + b * self.cap, -1)
+        self.pool_size = int(sizes.sum())
+        dev = rt.dev
+        self.kind = torch.from_numpy(kind.ravel().astype(np.uint8)).to(dev)
+        self.rank = torch.from_numpy(np.where(kind.ravel(), 0, -1).astype(np.int32)).to(dev)
+        self.off_u = torch.from_numpy(off).to(dev)
+        self.off_v = torch.from_numpy(offv).to(dev)
+        self.off_u_host, self.off_v_host = off, offv
+        self.pool = torch.zeros(self.pool_size, dtype=torch.float64, device=dev)
+
+    # -- ctypes view -----------------------------------------------------
+    def cstruct(self) -> _lib.Grid:
+        return _lib.Grid(self.p, self.q, self.b, self.cap, self.kind.data_ptr(), self.rank.data_ptr(),
+                         self.pool.data_ptr(), self.off_u.data_ptr(), self.off_v.data_ptr())
+
+    @property
+    def structure(self) -> BlrStructure:
+        return BlrStructure(self.m, self.n, self.b, self.kind_host.copy())
+
+    def rank_map(self) -> np.ndarray:
+        return self.rank.cpu().numpy().reshape(self.p, self.q).copy()
+
+    def clone(self) -> "DeviceGrid":
+        g = DeviceGrid.__new__(DeviceGrid)
+        g.__dict__.update(self.__dict__)
+        g.kind = self.kind.clone()
+        g.rank = self.rank.clone()
+        g.pool = self.pool.clone()
+        g.kind_host = self.kind_host.copy()
+        return g
+
+    # -- host <-> device ----------------------------------------------------
+    def _stage_offsets(self, ranks: np.ndarray) -> tuple[np.ndarray, int]:
+        b = self.b
+        kind = self.kind_host.ravel()
+        sz = np.where(kind, 2 * b * np.maximum(ranks, 0), b * b).astype(np.int64)
+        off = np.zeros_like(sz)
+        off[1:] = np.cumsum(sz)[:-1]
+        return off, int(sz.sum())
+
+    def _pack(self, stage: torch.Tensor, offs: np.ndarray, to_grid: bool) -> None:
+        lib = _lib.load()
+        od = torch.from_numpy(offs).to(stage.device)
+        g = self.cstruct()
+        _lib.check(lib.blrqr_grid_pack(C.byref(g), stage.data_ptr(), od.data_ptr(), int(to_grid),
+                                       _lib.stream_ptr()), "grid_pack")
+
+    @classmethod
+    def from_host(cls, a: BlrMatrix, cap: int | None = None, pinned: bool = False) -> "DeviceGrid":
+        s = a.structure
+        g = cls(s.m, s.n, s.b, s.admissible, cap)
+        ranks = np.array([x.rank if is_lowrank(x) else -1 for row in a.blocks for x in row], dtype=np.int32)
+        if (ranks > g.cap).any():
+            raise ValueError("input rank exceeds the slab capacity")
+        offs, tot = g._stage_offsets(ranks)
+        host = np.empty(tot, dtype=np.float64)
+        c = 0
+        for row in a.blocks:
+            for x in row:
+                o = offs[c]
+                if is_lowrank(x):
+                    r = x.rank
+                    host[o:o + s.b * r] = _f(x.u)
+                    host[o + s.b * r:o + 2 * s.b * r] = _f(x.v)
+                else:
+                    host[o:o + s.b * s.b] = _f(x)
+                c += 1
+        ht = torch.from_numpy(host)
+        if pinned:
+            ht = ht.pin_memory()
+        stage = ht.to(g.pool.device, non_blocking=pinned)
+        g.rank.copy_(torch.from_numpy(ranks))
+        g._pack(stage, offs, True)
+        return g
+
+    def to_host(self) -> BlrMatrix:
+        ranks = self.rank.cpu().numpy()
+        offs, tot = self._stage_offsets(ranks)
+        stage = torch.empty(max(tot, 1), dtype=torch.float64, device=self.pool.device)
+        self._pack(stage, offs, False)
+        host = stage.cpu().numpy()
+        b = self.b
+        blocks = []
+        c = 0
+        for i in range(self.p):
+            row = []
+            for j in range(self.q):
+                o = offs[c]
+                if self.kind_host[i, j]:
+                    r = int(ranks[c])
+                    u = host[o:o + b * r].reshape(r, b).T
+                    v = host[o + b * r:o + 2 * b * r].reshape(r, b).T
+                    row.append(LowRankBlock(np.ascontiguousarray(u), np.ascontiguousarray(v)))
+                else:
+                    row.append(np.ascontiguousarray(host[o:o + b * b].reshape(b, b).T))
+                c += 1
+            blocks.append(row)
+        return BlrMatrix(self.structure, blocks)
+
+    @classmethod
+    def from_dense(cls, dense, b: int, admissible: np.ndarray, eps: float, fallback: float = 0.5,
+                   cap: int | None = None) -> "DeviceGrid":
+        """GPU dense_to_blr (core.py:227-259).  ``dense`` is a host ndarray or
+        a CUDA tensor (row-major m x n)."""
+        rt = _lib.runtime()
+        lib = rt.lib
+        if isinstance(dense, np.ndarray):
+            m, n = dense.shape
+            dt = torch.from_numpy(np.ascontiguousarray(dense)).to(rt.dev)
+        else:
+            m, n = dense.shape
+            dt = dense
+        adm = np.asarray(admissible, dtype=bool)
+        g = cls(m, n, b, adm, cap, min_lr_slab=b * b)
+        if g.cap < int(fallback * b):
+            raise ValueError("cap must be at least dense_fallback_fraction * b")
+        colmajor = dt.t().contiguous()  # column-major m x n, lda = m
+        ws, per, nct = rt.workspace(b, g.cap)
+        st = g.cstruct()
+        _lib.check(lib.blrqr_dense_to_blr(colmajor.data_ptr(), m, C.byref(st), g.kind.data_ptr(), eps,
+                                          fallback, ws, per, nct, rt.status.data_ptr(), rt.flops.data_ptr(),
+                                          _lib.stream_ptr()), "dense_to_blr")
+        rt.harvest()
+        g.kind_host = g.kind.cpu().numpy().astype(bool).reshape(g.p, g.q)
+        del colmajor
+        return g
+
+
+class DeviceRefl:
+    """Householder reflector store for the tiled / blocked methods."""
+
+    def __init__(self, grid: DeviceGrid):
+        b, p, q = grid.b, grid.p, grid.q
+        kind = grid.kind_host
+        y_off = np.full(p * q, -1, dtype=np.int64)
+        t_off = np.full(p * q, -1, dtype=np.int64)
+        o = 0
+        for k in range(q):
+            c = k * q + k
+            y_off[c] = o; o += b * b
+            t_off[c] = o; o += b * b
+            for i in range(k + 1, p):
+                c = i * q + k
+                t_off[c] = o; o += b * b
+                if not kind[i, k]:
+                    y_off[c] = o; o += b * b
+        dev = grid.pool.device
+        self.grid = grid
+        self.y_off_host, self.t_off_host = y_off, t_off
+        self.y_off = torch.from_numpy(y_off).to(dev)
+        self.t_off = torch.from_numpy(t_off).to(dev)
+        self.yrank = torch.full((p * q,), -1, dtype=torch.int32, device=dev)
+        self.pool = torch.zeros(o, dtype=torch.float64, device=dev)
+
+    def cstruct(self) -> _lib.Refl:
+        return _lib.Refl(self.pool.data_ptr(), self.y_off.data_ptr(), self.t_off.data_ptr(),
+                         self.yrank.data_ptr())
+
+    def mat(self, off: int, rows: int, cols: int) -> np.ndarray:
+        """Download a column-major rows x cols matrix at pool offset ``off``."""
+        x = self.pool[off:off + rows * cols].cpu().numpy()
+        return np.ascontiguousarray(x.reshape(cols, rows).T)

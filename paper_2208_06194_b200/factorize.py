@@ -1,0 +1,194 @@
+"""BLR-QR factorizations with the reference API (factorize.py), on the GPU.
+
+Each method replays the reference's task sequence (factorize.py:187-262
+blocked, :369-458 tiled, :576-671 MGS) with one CTA per block task; the
+parallelism comes only from running independent tasks side by side
+(levels of the tiled DAG, the j-loop of a blocked step, the k-loop of an MGS
+step), never from re-associating sums (SURVEY §7 guiding constraint).
+
+Device drivers (``DeviceFactorization``) keep everything in HBM; the
+reference-compatible entry points (``tiled_householder_qr`` ...) upload a
+host ``BlrMatrix``, run, and download a ``FactorizationResult`` holding the
+same containers as the reference.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from functools import lru_cache
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import BlrMatrix, LowRankBlock, is_lowrank
+from .device import DeviceGrid, DeviceRefl
+from .kernels import WYReflector
+from .lowrank import ToleranceConfig
+
+__all__ = ["ReflectorColumn", "TileReflectorStore", "FactorizationResult", "DeviceFactorization",
+           "blocked_householder_qr", "tiled_householder_qr", "blocked_mgs_qr", "factorize_device",
+           "blocked_apply_q", "tiled_apply_q"]
+
+METHODS = ("mgs", "blocked-hh", "tiled-hh")
+
+
+@dataclass
+class ReflectorColumn:
+    """factorize.py:146-156."""
+
+    col: int
+    entries: list
+    t: np.ndarray
+
+
+@dataclass
+class TileReflectorStore:
+    """factorize.py:159-170."""
+
+    diag: dict = field(default_factory=dict)
+    updates: dict = field(default_factory=dict)
+
+
+@dataclass
+class FactorizationResult:
+    """factorize.py:173-179."""
+
+    algorithm: str
+    r: BlrMatrix
+    q_columns: list | None = None
+    q_tiles: TileReflectorStore | None = None
+    q_explicit: BlrMatrix | None = None
+
+
+@lru_cache(maxsize=16)
+def tiled_schedule(p: int, q: int):
+    """(tasks ndarray[n, 4] int32, level_start ndarray[int64]) from the C++
+    level scheduler over the reference DAG's read/write sets."""
+    lib = _lib.load()
+    n = int(lib.blrqr_tiled_task_count(p, q))
+    if n < 0:
+        raise ValueError("need p >= q >= 1")
+    tasks = (_lib.Task * n)()
+    ls = (C.c_int64 * (n + 2))()
+    nlev = lib.blrqr_tiled_schedule(p, q, C.addressof(tasks), C.addressof(ls), n + 1)
+    if nlev < 0:
+        raise RuntimeError("tiled schedule failed")
+    arr = np.ctypeslib.as_array(C.cast(tasks, C.POINTER(C.c_int32)), shape=(n, 4)).copy()
+    lv = np.ctypeslib.as_array(ls, shape=(n + 2,))[: nlev + 1].copy()
+    return arr, lv
+
+
+class DeviceFactorization:
+    """A BLR-QR factorization resident on the GPU (input grid is cloned)."""
+
+    def __init__(self, method: str, a: DeviceGrid, cfg: ToleranceConfig, clone: bool = True):
+        if method not in METHODS:
+            raise ValueError(f"unknown algorithm {method!r}")
+        if a.p < a.q:
+            raise ValueError("grid must have at least as many block rows as columns")
+        self.method = method
+        self.cfg = cfg
+        self.rt = _lib.runtime()
+        self.g = a.clone() if clone else a
+        self.rf = None
+        self.qg = None
+        self.rg = None
+        if method == "tiled-hh":
+            self.rf = DeviceRefl(self.g)
+            tasks, self.levels = tiled_schedule(self.g.p, self.g.q)
+            self.tasks = torch.from_numpy(tasks).to(self.rt.dev)
+            self.nlevels = len(self.levels) - 1
+        elif method == "blocked-hh":
+            raise NotImplementedError("blocked-hh device driver")
+        else:
+            raise NotImplementedError("mgs device driver")
+
+    # -- execution ---------------------------------------------------------
+    def run(self, nctas: int | None = None) -> "DeviceFactorization":
+        """Enqueue the whole factorization on the current stream (no sync)."""
+        rt = self.rt
+        g = self.g
+        ws, per, nct = rt.workspace(g.b, g.cap, 0, nctas)
+        if self.method == "tiled-hh":
+            gs, rs = g.cstruct(), self.rf.cstruct()
+            lv = self.levels.ctypes.data_as(C.c_void_p)
+            _lib.check(rt.lib.blrqr_tiled_run(C.byref(gs), C.byref(rs), self.tasks.data_ptr(), lv, 0,
+                                              self.nlevels, self.cfg.epsilon, ws, per, nct,
+                                              rt.status.data_ptr(), rt.flops.data_ptr(), _lib.stream_ptr()),
+                       "tiled_run")
+        return self
+
+    def finish(self) -> dict:
+        """Synchronise, raise on device errors, return the model-flop report."""
+        _, counts = self.rt.harvest()
+        return counts
+
+    # -- results -----------------------------------------------------------
+    def r_device(self) -> DeviceGrid:
+        return self.g
+
+    def to_host(self) -> FactorizationResult:
+        r = self.g.to_host()
+        if self.method == "tiled-hh":
+            return FactorizationResult("tiled-hh", r, q_tiles=self._tiles_host())
+        raise NotImplementedError
+
+    def _tiles_host(self) -> TileReflectorStore:
+        g, rf = self.g, self.rf
+        b, p, q = g.b, g.p, g.q
+        store = TileReflectorStore()
+        yr = rf.yrank.cpu().numpy()
+        for k in range(q):
+            c = k * q + k
+            store.diag[k] = WYReflector(rf.mat(rf.y_off_host[c], b, b), rf.mat(rf.t_off_host[c], b, b))
+            for i in range(k + 1, p):
+                c = i * q + k
+                t = rf.mat(rf.t_off_host[c], b, b)
+                if yr[c] >= 0:
+                    r = int(yr[c])
+                    ou, ov = g.off_u_host[c], g.off_v_host[c]
+                    u = g.pool[ou:ou + b * r].cpu().numpy().reshape(r, b).T
+                    v = g.pool[ov:ov + b * r].cpu().numpy().reshape(r, b).T
+                    store.updates[(i, k)] = (LowRankBlock(np.ascontiguousarray(u), np.ascontiguousarray(v)), t)
+                else:
+                    store.updates[(i, k)] = (rf.mat(rf.y_off_host[c], b, b), t)
+        return store
+
+
+def factorize_device(method: str, a: DeviceGrid, cfg: ToleranceConfig, clone: bool = True) -> DeviceFactorization:
+    f = DeviceFactorization(method, a, cfg, clone)
+    f.run()
+    f.finish()
+    return f
+
+
+def _host_entry(method: str, a: BlrMatrix, cfg: ToleranceConfig) -> FactorizationResult:
+    if a.p < a.q:
+        raise ValueError("grid must have at least as many block rows as columns")
+    g = DeviceGrid.from_host(a)
+    return factorize_device(method, g, cfg, clone=False).to_host()
+
+
+def tiled_householder_qr(a: BlrMatrix, cfg: ToleranceConfig) -> FactorizationResult:
+    """factorize.py:447-458."""
+    return _host_entry("tiled-hh", a, cfg)
+
+
+def blocked_householder_qr(a: BlrMatrix, cfg: ToleranceConfig) -> FactorizationResult:
+    """factorize.py:285-292."""
+    return _host_entry("blocked-hh", a, cfg)
+
+
+def blocked_mgs_qr(a: BlrMatrix, cfg: ToleranceConfig) -> FactorizationResult:
+    """factorize.py:661-671."""
+    return _host_entry("mgs", a, cfg)
+
+
+def blocked_apply_q(result, c, transpose, cfg=None):  # pragma: no cover - next round
+    raise NotImplementedError("GPU apply-Q (SURVEY §8f row 1) is not built yet")
+
+
+def tiled_apply_q(result, c, transpose, cfg=None):  # pragma: no cover - next round
+    raise NotImplementedError("GPU apply-Q (SURVEY §8f row 1) is not built yet")

@@ -268,5 +268,88 @@ def main():
         run_case("C1", c.family, c.n, c.b, c.eps, c.methods, store_full=False)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and not os.environ.get("GOLDEN_FULL"):
     main()
+
+
+# ---------------------------------------------------------------------------
+# full-size configs (background job; minutes to tens of minutes)
+# ---------------------------------------------------------------------------
+
+
+def run_full(name, methods=None):
+    """Full-size config: store rank maps, R sketches, Frobenius norms, flop
+    totals and the reference's rounded-add operand-rank histogram."""
+    from threadpoolctl import threadpool_limits
+
+    c = configs.CONFIGS[name]
+    methods = methods or c.methods
+    with threadpool_limits(8):
+        tile, n = configs.tile_source(c)
+    b, eps = c.b, c.eps
+    p = n // b
+    adm = rcore.weak_admissibility(p, p)
+    t0 = time.perf_counter()
+    with threadpool_limits(1):
+        blocks = []
+        for i in range(p):
+            row = []
+            for j in range(p):
+                t = np.ascontiguousarray(tile(i * b, j * b, b, b))
+                if adm[i, j]:
+                    blk = rlr.compress_rrqr(t, rlr.ToleranceConfig(eps))
+                    if not rcore.is_lowrank(blk):
+                        adm[i, j] = False
+                    row.append(blk)
+                else:
+                    row.append(t)
+            blocks.append(row)
+    a = rcore.BlrMatrix(rcore.BlrStructure(n, n, b, adm), blocks)
+    tc = time.perf_counter() - t0
+    out = {"input_ranks": np.array([[blk.rank if rcore.is_lowrank(blk) else -1
+                                     for blk in row] for row in a.blocks])}
+    summary = {"tag": name, "family": c.family, "n": n, "b": b, "eps": eps,
+               "compress_s": tc, "methods": {}}
+    print(name, "compressed", f"{tc:.1f}s", flush=True)
+    orig = rlr.rounded_add
+    for m in methods:
+        hist = {}
+
+        def counting(x, y, cfg, _orig=orig, _h=hist):
+            o = _orig(x, y, cfg)
+            key = (x.rank + y.rank, o.rank)
+            _h[key] = _h.get(key, 0) + 1
+            return o
+
+        rfac.rounded_add = counting
+        rflops.reset()
+        t0 = time.perf_counter()
+        with threadpool_limits(1):
+            res = rsch.execute_sequential(m, a, rlr.ToleranceConfig(eps))
+        tf = time.perf_counter() - t0
+        rfac.rounded_add = orig
+        fl = rflops.report()
+        g = np.random.default_rng(5).standard_normal((n, 8))
+        sk = np.zeros((n, 8))
+        fro = np.zeros((p, p))
+        for i in range(p):
+            for j in range(p):
+                d = rcore.block_to_dense(res.r.blocks[i][j])
+                sk[i * b:(i + 1) * b] += d @ g[j * b:(j + 1) * b]
+                fro[i, j] = np.linalg.norm(d)
+        out[f"{m}_ranks"] = np.array([[blk.rank if rcore.is_lowrank(blk) else -1
+                                       for blk in row] for row in res.r.blocks])
+        out[f"{m}_sketch"] = sk
+        out[f"{m}_fro"] = fro
+        out[f"{m}_radd_hist"] = np.array([[k[0], k[1], v] for k, v in sorted(hist.items())])
+        summary["methods"][m] = {"factorize_s": tf, "flops": fl,
+                                 "flops_total": int(sum(fl.values()))}
+        print(name, m, f"{tf:.1f}s F={sum(fl.values()):.4e}", flush=True)
+        np.savez_compressed(os.path.join(HERE, f"fact_{name}.npz"), **out)
+        with open(os.path.join(HERE, f"fact_{name}.json"), "w") as fh:
+            json.dump(summary, fh, indent=1, sort_keys=True)
+
+
+if __name__ == "__main__" and os.environ.get("GOLDEN_FULL"):
+    for nm in os.environ["GOLDEN_FULL"].split(","):
+        run_full(nm)
