@@ -76,7 +76,8 @@ def qr_compact_wy(a: np.ndarray):
     rt = _lib.runtime()
     y, t, r = _buf(m * n), _buf(n * n), _buf(n * n)
     ws, per, _ = rt.workspace(max(m, 64), n, m)
-    _lib.check(rt.lib.blrqr_geqrt(m, n, _dev(a).data_ptr(), y.data_ptr(), t.data_ptr(), r.data_ptr(), ws, per,
+    ad = _dev(a)  # keep operands alive until the (async) launch has consumed them
+    _lib.check(rt.lib.blrqr_geqrt(m, n, ad.data_ptr(), y.data_ptr(), t.data_ptr(), r.data_ptr(), ws, per,
                                   rt.status.data_ptr(), rt.flops.data_ptr(), _lib.stream_ptr()), "geqrt")
     rt.harvest()
     return WYReflector(_host(y, m, n), _host(t, n, n)), _host(r, n, n)
@@ -95,7 +96,8 @@ def _apply_wy(ref: WYReflector, c: np.ndarray, transpose: bool) -> np.ndarray:
     rt = _lib.runtime()
     cd = _dev(c)
     ws, per, _ = rt.workspace(max(m, 64), max(n, nc), m)
-    _lib.check(rt.lib.blrqr_apply_wy(m, n, nc, _dev(ref.y).data_ptr(), _dev(ref.t).data_ptr(), cd.data_ptr(),
+    yd, td = _dev(ref.y), _dev(ref.t)
+    _lib.check(rt.lib.blrqr_apply_wy(m, n, nc, yd.data_ptr(), td.data_ptr(), cd.data_ptr(),
                                      int(transpose), ws, per, rt.status.data_ptr(), rt.flops.data_ptr(),
                                      _lib.stream_ptr()), "apply_wy")
     rt.harvest()
@@ -124,7 +126,8 @@ def tp_qr(r_top: np.ndarray, a_bot: np.ndarray):
     rt = _lib.runtime()
     rn, y, t = _buf(n * n), _buf(k * n), _buf(n * n)
     ws, per, _ = rt.workspace(max(n, k, 64), n, n + k)
-    _lib.check(rt.lib.blrqr_tpqrt(n, k, _dev(r_top).data_ptr(), _dev(a_bot).data_ptr(), rn.data_ptr(),
+    rtd, abd = _dev(r_top), _dev(a_bot)
+    _lib.check(rt.lib.blrqr_tpqrt(n, k, rtd.data_ptr(), abd.data_ptr(), rn.data_ptr(),
                                   y.data_ptr(), t.data_ptr(), ws, per, rt.status.data_ptr(), rt.flops.data_ptr(),
                                   _lib.stream_ptr()), "tpqrt")
     rt.harvest()
@@ -142,7 +145,8 @@ def _apply_tp(ref: TPReflector, c_top: np.ndarray, c_bot: np.ndarray, transpose:
     ct, cb = _dev(c_top), _dev(c_bot) if k else _buf(1)
     yd = _dev(ref.y) if k else _buf(1)
     ws, per, _ = rt.workspace(max(n, k, 64), max(n, nc), n + k)
-    _lib.check(rt.lib.blrqr_apply_tp(n, k, nc, yd.data_ptr(), _dev(ref.t).data_ptr(), ct.data_ptr(),
+    td = _dev(ref.t)
+    _lib.check(rt.lib.blrqr_apply_tp(n, k, nc, yd.data_ptr(), td.data_ptr(), ct.data_ptr(),
                                      cb.data_ptr(), int(transpose), ws, per, rt.status.data_ptr(),
                                      rt.flops.data_ptr(), _lib.stream_ptr()), "apply_tp")
     rt.harvest()
@@ -164,7 +168,8 @@ def mgs_panel_qr(a: np.ndarray):
     rt = _lib.runtime()
     q, r = _buf(m * n), _buf(n * n)
     ws, per, _ = rt.workspace(max(m, 64), n, m)
-    _lib.check(rt.lib.blrqr_mgs_panel(m, n, _dev(a).data_ptr(), q.data_ptr(), r.data_ptr(), ws, per,
+    ad = _dev(a)
+    _lib.check(rt.lib.blrqr_mgs_panel(m, n, ad.data_ptr(), q.data_ptr(), r.data_ptr(), ws, per,
                                       rt.status.data_ptr(), rt.flops.data_ptr(), _lib.stream_ptr()), "mgs_panel")
     rt.harvest()
     return _host(q, m, n), _host(r, n, n)

@@ -82,9 +82,10 @@ def rounded_add_batched(pairs, cfg: ToleranceConfig) -> list[LowRankBlock]:
     ro = torch.zeros(len(pairs), dtype=torch.int32, device=rt.dev)
     ws, per, nct = rt.workspace(max(m, n), cap)
     lib = rt.lib
+    pa = [_ptrs(x) for x in (ua, va, ub, vb, uo, vo)]  # held until the launch is enqueued
     _lib.check(lib.blrqr_rounded_add_batched(
-        len(pairs), m, n, _ptrs(ua).data_ptr(), _ptrs(va).data_ptr(), ra.data_ptr(), _ptrs(ub).data_ptr(),
-        _ptrs(vb).data_ptr(), rb.data_ptr(), _ptrs(uo).data_ptr(), _ptrs(vo).data_ptr(), ro.data_ptr(), cap,
+        len(pairs), m, n, pa[0].data_ptr(), pa[1].data_ptr(), ra.data_ptr(), pa[2].data_ptr(),
+        pa[3].data_ptr(), rb.data_ptr(), pa[4].data_ptr(), pa[5].data_ptr(), ro.data_ptr(), cap,
         cfg.epsilon, ws, per, nct, rt.status.data_ptr(), rt.flops.data_ptr(), _lib.stream_ptr()),
         "rounded_add")
     rt.harvest()
@@ -118,8 +119,9 @@ def compress_batched(tiles, epsilon: float, max_rank: int) -> list:
     vo = [torch.empty(n * k, dtype=torch.float64, device=rt.dev) for _ in tiles]
     ro = torch.zeros(len(tiles), dtype=torch.int32, device=rt.dev)
     ws, per, nct = rt.workspace(max(m, n), k)
+    pa = [_ptrs(x) for x in (a, uo, vo)]
     _lib.check(rt.lib.blrqr_compress_batched(
-        len(tiles), m, n, _ptrs(a).data_ptr(), _ptrs(uo).data_ptr(), _ptrs(vo).data_ptr(), ro.data_ptr(), k,
+        len(tiles), m, n, pa[0].data_ptr(), pa[1].data_ptr(), pa[2].data_ptr(), ro.data_ptr(), k,
         epsilon, max_rank, ws, per, nct, rt.status.data_ptr(), rt.flops.data_ptr(), _lib.stream_ptr()),
         "compress")
     rt.harvest()
