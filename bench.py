@@ -1,0 +1,351 @@
+"""BLR-QR benchmark (driver contract: one JSON line on rank 0).
+
+Workload: BASELINE.json's metric config C3 -- spatial-statistics exponential
+covariance, n = 32768, b = 512, eps = 1e-8, tiled Householder BLR-QR --
+synthetic seeded input generated on the GPU, compressed on the GPU
+(untimed), then factorized K times.  A "step" is one whole factorization:
+clone of the compressed input (the reference's ``a.copy()`` inside
+``TiledState``, factorize.py:375) + every task of the tiled DAG.
+
+metric: effective FP64 GFLOP/s = F_model / t_factorize, where F_model is the
+reference's own flop model (flops.py) accumulated on the device from the
+realised ranks (equal to the reference's flops.total() when ranks match).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C3]
+
+--impl reference times the reference algorithm on the host cores (the CPU
+oracle port in oracle/, which replays the reference numpy/LAPACK calls),
+on a bounded sample of the same workload: the first block-column sweep
+(k = 0) restricted to block rows 1..I.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+FP64_PEAK_TFLOPS = 37.07  # measured DMMA m8n8k4 loop on this pool's B200 (profiles/fp64_peaks_r01.txt)
+FP64_PEAK_SRC = "measured: tools/fp64_peak.cu DMMA loop (MEASURED_PEAKS.json has no FP64 entry)"
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([x.strip() for x in out.split(",")])
+                except Exception:  # noqa: BLE001
+                    pass
+                self._stop.wait(0.2)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        import statistics
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and "Active" in s[3 + i]
+                          and not s[3 + i].startswith("Not")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference sample (oracle port of the reference algorithm)
+# ---------------------------------------------------------------------------
+
+
+def cpu_reference_sample(cfg_name: str, rows: int, threads: int, grid_host=None):
+    """Time the reference tiled algorithm on the first sweep (k = 0) over block
+    rows 1..rows of the config, with a fork-join thread pool over j
+    (scheduler.py:279-332 semantics).  Returns (gflops, seconds, flops, sample)."""
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    from concurrent.futures import ThreadPoolExecutor
+
+    import numpy as np
+
+    from oracle import algorithms as oalg, blr as oblr, configs as ocfg, flops as ofl, lowrank as olr
+
+    c = ocfg.CONFIGS[cfg_name]
+    b, p = c.b, c.n // c.b
+    if grid_host is None:
+        tile, _ = ocfg.tile_source(c)
+        need = [(i, j) for i in range(rows + 1) for j in range(p)]
+
+        def comp(ij):
+            i, j = ij
+            t = np.ascontiguousarray(tile(i * b, j * b, b, b))
+            return ij, (t if i == j else olr.compress(t, c.eps))
+
+        cells = {}
+        with ThreadPoolExecutor(max_workers=threads) as pool:
+            for ij, x in pool.map(comp, need):
+                cells[ij] = x
+    else:
+        cells = grid_host
+    lowrank = oblr.weak_map(p, p)
+    grid = oblr.Grid(c.n, c.n, b, lowrank, [[cells.get((i, j)) for j in range(p)] for i in range(p)])
+    st = oalg.TiledState(grid, c.eps)  # no clone: the sample owns its cells
+    ofl.reset()
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as pool:
+        st.diag_qr(0)
+        list(pool.map(lambda j: st.apply_block(0, j), range(1, p)))
+        for i in range(1, rows + 1):
+            st.update_qr(0, i)
+            list(pool.map(lambda j, i=i: st.apply_trap(0, i, j), range(1, p)))
+    dt = time.perf_counter() - t0
+    fl = ofl.total()
+    sample = (f"{cfg_name} tiled-hh sweep k=0, block rows 1..{rows} of {p - 1}: DiagQR(0), {p - 1} ApplyBlock, "
+              f"{rows} UpdateQR, {rows * (p - 1)} ApplyTrap; fork-join pool of {threads} threads over j")
+    return fl / dt / 1e9, dt, fl, sample
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import __graft_entry__ as ge
+
+    ws_, rank, local = _dist()
+    ge.build()
+    torch.cuda.set_device(local)
+    if ws_ > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2208_06194_b200 import _lib, configs
+    from paper_2208_06194_b200.core import weak_admissibility
+    from paper_2208_06194_b200.device import DeviceGrid
+    from paper_2208_06194_b200.factorize import DeviceFactorization, tiled_schedule
+    from paper_2208_06194_b200.lowrank import ToleranceConfig
+
+    cfg = configs.CONFIGS[args.config]
+    method = args.method or cfg.method
+    rt = _lib.runtime()
+    t0 = time.perf_counter()
+    dense = configs.dense_device(cfg)
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    g0 = DeviceGrid.from_dense(dense, cfg.b, weak_admissibility(cfg.n // cfg.b, cfg.n // cfg.b), cfg.eps, 0.5,
+                               colmajor=True)
+    torch.cuda.synchronize()
+    t_comp = time.perf_counter() - t0
+    del dense
+    torch.cuda.empty_cache()
+    in_ranks = g0.rank_map()
+    tol = ToleranceConfig(cfg.eps)
+
+    def barrier():
+        if ws_ > 1:
+            torch.distributed.barrier()
+
+    def step():
+        f = DeviceFactorization(method, g0, tol, clone=True)
+        f.run()
+        return f
+
+    # warm-up (also builds the schedule and grows the workspace)
+    for _ in range(args.warmup):
+        f = step()
+        f.finish()
+    nlev = f.nlevels if method == "tiled-hh" else 0
+    flops_rep = f.finish() or {}
+    # timed region: K steps bracketed by barrier + synchronize
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    F = 0
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for s in range(args.steps):
+            ev[s][0].record()
+            f = step()
+            ev[s][1].record()
+        torch.cuda.synchronize()
+    barrier()
+    counts = f.finish()
+    F_step = sum(counts.values()) // 1  # counters accumulate only the last harvest window
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    # harvest() is called once after K steps: counters summed all K steps
+    F_step = sum(counts.values()) / args.steps
+    ms = sum(step_ms) / args.steps
+    if ws_ > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    gflops = F_step / (ms * 1e-3) / 1e9
+
+    # ---- e2e: reference-facing path with HOST buffers -----------------------
+    e2e = None
+    if args.e2e_steps > 0:
+        host = g0.to_host()  # the compressed BLR as the reference's BlrMatrix (numpy)
+        from paper_2208_06194_b200.device import DeviceGrid as DG
+        # pinned staging prepared once (the caller's host buffers)
+        e2e_ms = []
+        h2d = d2h = 0
+        for _ in range(args.e2e_steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            gd = DG.from_host(host, pinned=True)
+            fe = DeviceFactorization(method, gd, tol, clone=False)
+            fe.run()
+            r_host = fe.g.to_host()
+            fe.finish()
+            torch.cuda.synchronize()
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+            h2d = int(sum(x.u.nbytes + x.v.nbytes if hasattr(x, "u") else x.nbytes for row in host.blocks for x in row))
+            d2h = int(sum(x.u.nbytes + x.v.nbytes if hasattr(x, "u") else x.nbytes for row in r_host.blocks for x in row))
+        e_ms = sum(e2e_ms) / len(e2e_ms)
+        e2e = {"value": F_step / (e_ms * 1e-3) / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": e_ms,
+               "path": "BlrMatrix (host numpy) -> DeviceGrid.from_host (pinned H2D + unpack kernel) -> "
+                       "factorize -> R to host BlrMatrix (pack kernel + D2H)"}
+
+    out_ranks = f.g.rank_map()
+    res = {
+        "metric": f"BLR-QR effective FP64 GFLOP/s (F_model / t_factorize), {cfg.name} {method}",
+        "value": gflops * ws_,
+        "unit": "GFLOP/s",
+        "n_gpus": ws_,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "factorize_s": ms / 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded, generated on GPU: BASELINE.json config recipe)",
+        "config": {"workload": f"{cfg.name}: {cfg.family} n={cfg.n} b={cfg.b} eps={cfg.eps} {method}",
+                   "n": cfg.n, "b": cfg.b, "eps": cfg.eps, "method": method,
+                   "parallelism": f"replicas x{ws_}" if ws_ > 1 else "1 GPU",
+                   "l2_note": "inputs larger than L2 (BLR pool > 126 MB)"},
+        "F_model_per_step": F_step,
+        "flops_by_kind": {k: v / args.steps for k, v in counts.items()},
+        "input_ranks": {"min": int(in_ranks[in_ranks >= 0].min()), "median": float(np.median(in_ranks[in_ranks >= 0])),
+                        "max": int(in_ranks.max())},
+        "r_ranks": {"median": float(np.median(out_ranks[out_ranks >= 0])), "max": int(out_ranks.max())},
+        "setup_s": {"generate": t_gen, "compress": t_comp},
+        "gpu_launches": nlev * args.steps,
+        "roofline": {"bound": "tensor", "achieved": F_step / (ms * 1e-3) / 1e12, "peak": FP64_PEAK_TFLOPS,
+                     "unit": "TFLOP/s", "frac": F_step / (ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+                     "traffic": None, "kernel": "k_tiled (level-batched task kernel)",
+                     "peak_source": FP64_PEAK_SRC,
+                     "note": "achieved = reference flop model per factorization / device time of the step"},
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "impl": "ours",
+    }
+    if rank == 0 and not args.no_cpu:
+        g, dt, fl, sample = cpu_reference_sample(cfg.name, args.cpu_rows, os.cpu_count() or 1,
+                                                 grid_host=_host_cells(f0=g0, rows=args.cpu_rows))
+        res["cpu_baseline"] = {"value": g, "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": "port",
+                               "sample": sample, "seconds": dt, "flops": fl}
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if ws_ > 1:
+        torch.distributed.destroy_process_group()
+
+
+def _host_cells(f0, rows):
+    """Cells (i, j), i <= rows, of the GPU-compressed input as oracle blocks."""
+    from oracle import blr as oblr
+    h = f0.to_host()
+    out = {}
+    for i in range(rows + 1):
+        for j in range(h.q):
+            x = h.blocks[i][j]
+            out[(i, j)] = oblr.LR(x.u, x.v) if hasattr(x, "u") else x
+    return out
+
+
+def run_reference(args):
+    ws_, rank, _ = _dist()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    vals, secs = [], []
+    for _ in range(args.warmup):
+        cpu_reference_sample(args.config, args.cpu_rows, threads)
+    for _ in range(args.steps):
+        g, dt, fl, sample = cpu_reference_sample(args.config, args.cpu_rows, threads)
+        vals.append(g)
+        secs.append(dt)
+    v = sum(vals) / len(vals)
+    res = {
+        "metric": f"BLR-QR effective FP64 GFLOP/s (F_model / t_factorize), {args.config} tiled-hh",
+        "value": v, "unit": "GFLOP/s", "n_gpus": ws_, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(secs) / len(secs), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json config recipe)",
+        "config": {"workload": f"{args.config} tiled-hh (bounded CPU sample)"},
+        "impl": "reference",
+        "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(res), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--method", default=None)
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--cpu-rows", type=int, default=12)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

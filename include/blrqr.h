@@ -81,7 +81,7 @@ typedef struct {
 int blrqr_version(void);
 /* doubles of per-CTA scratch the kernels need for block size b, capacity cap */
 int64_t blrqr_workspace_doubles(int b, int cap, int max_panel_rows);
-/* recommended number of resident CTAs (2 per SM) on the current device */
+/* recommended number of resident CTAs (1 per SM) on the current device */
 int blrqr_default_ctas(void);
 
 /* ---- low-rank arithmetic (lowrank.py) ---------------------------------- */

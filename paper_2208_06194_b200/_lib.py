@@ -19,6 +19,8 @@ LIB_PATH = os.path.join(_HERE, "lib", "libblrqr.so")
 
 FLOP_KINDS = ("compress", "rounded_add", "expand", "lr_mul", "gemm", "panel_qr",
               "apply_wy", "update_qr", "apply_tp")
+PHASES = ("norm", "qr", "core", "svd", "back", "product", "tpqrt", "geqrt", "apply_wy", "rrqr", "expand", "task",
+          "qrcp", "jacobi_sweeps", "jacobi_calls")
 ST_RANK_OVERFLOW, ST_ARENA_OVERFLOW, ST_NONFINITE, ST_MGS_COLLAPSE, ST_BAD_KIND, ST_BAD_ARG = (
     1, 2, 4, 8, 16, 32)
 
@@ -117,7 +119,9 @@ class Runtime:
         self.dev = require_cuda()
         self.lib = load()
         self.status = torch.zeros(1, dtype=torch.int32, device=self.dev)
-        self.flops = torch.zeros(len(FLOP_KINDS), dtype=torch.int64, device=self.dev)
+        # [0:9] model flops per kind, [16:32] per-phase SM cycles (see PHASES)
+        self.flops = torch.zeros(32, dtype=torch.int64, device=self.dev)
+        self.last_phases = {}
         self.nctas = int(self.lib.blrqr_default_ctas())
         self._ws = None
         self._ws_per_cta = 0
@@ -144,6 +148,7 @@ class Runtime:
         self.status.zero_()
         self.flops.zero_()
         counts = {k: int(v) for k, v in zip(FLOP_KINDS, fl) if v}
+        self.last_phases = {k: int(v) for k, v in zip(PHASES, fl[16:]) if v}
         from . import flops as _fl
         for k, v in counts.items():
             _fl.add(k, v)

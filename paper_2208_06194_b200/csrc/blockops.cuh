@@ -51,75 +51,140 @@ __device__ __noinline__ double lr_norm(Ctx& cx, const Blk& a) {
   return fabs(a.s) * sqrt(fmax(s, 0.0));
 }
 
-// Rounded addition C = A + B (lowrank.py:173-221).  Output factors are written
-// to (du, ldu_, dv, ldv_) with capacity `cap` columns (may alias A or B: the
-// inputs are consumed first).  Returns the output rank.
-__device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, double eps, double* du, int lddu, double* dv,
-                           int lddv, int cap) {
+// Rounded addition C = A + B (lowrank.py:173-221, Alg. 6).  Output factors
+// are written to (du, lddu, dv, lddv) with capacity `cap` columns (may alias
+// A or B: the inputs are consumed first).  Returns the output rank.
+//
+// Same mathematics as the reference, GPU-shaped:
+//  1. U = [U_A U_B], V = [s_A V_A, s_B V_B]; Householder QR of both (panels
+//     staged in shared memory).
+//  2. core = R_U R_V^T computed as C_A + C_B with C_A = R_U[:, :ra] R_V[:, :ra]^T:
+//     ||A||_F = ||C_A||_F and ||B||_F = ||C_B||_F exactly (Q_U, Q_V orthonormal),
+//     which replaces the factor Gram products of _lr_norm (lowrank.py:161-166).
+//  3. SVD of the core by QR with column pivoting (stopped once the remainder
+//     is below eps_mach*||core||_F, i.e. rounding level) followed by one-sided
+//     Jacobi on R1^T (Drmac-Veselic preconditioning: 2-4 sweeps).
+//  4. Truncation exactly as lowrank.py:204-213 (noise floor, Frobenius tail).
+//  5. U_C = Q_U [Q_core J_r; 0], V_C = Q_V [W_r; 0] (sigma folded into V).
+__device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, double eps, double* du, int lddu,
+                                        double* dv, int lddv, int cap) {
   const int m = A.rows, n = A.cols;
   if (A.rank == 0 && B.rank == 0) return 0;
-  const int c = A.rank + B.rank;
-  const long long mark = cx.top;
-  const double nA = lr_norm(cx, A), nB = lr_norm(cx, B);
+  const int ra = A.rank, rb = B.rank, c = ra + rb;
+  const Mark mk = mark(cx);
+  PhaseTimer tq;
   double* Uc = alloc(cx, (long long)m * c);
   double* Vc = alloc(cx, (long long)n * c);
-  double* tauU = alloc(cx, c);
-  double* tauV = alloc(cx, c);
+  double* tauU = alloc_fast(cx, c);
+  double* tauV = alloc_fast(cx, c);
   double* TpU = alloc(cx, (long long)QR_NB * c);
   double* TpV = alloc(cx, (long long)QR_NB * c);
-  if (!Uc || !Vc || !tauU || !tauV || !TpU || !TpV) { cx.top = mark; return 0; }
-  copy_mat(m, A.rank, A.u, A.ldu, Uc, m);
-  copy_mat(m, B.rank, B.u, B.ldu, Uc + (long long)A.rank * m, m);
-  copy_mat(n, A.rank, A.v, A.ldv, Vc, n, A.s);
-  copy_mat(n, B.rank, B.v, B.ldv, Vc + (long long)A.rank * n, n, B.s);
+  if (!Uc || !Vc || !tauU || !tauV || !TpU || !TpV) { release(cx, mk); return 0; }
+  copy_mat(m, ra, A.u, A.ldu, Uc, m);
+  copy_mat(m, rb, B.u, B.ldu, Uc + (long long)ra * m, m);
+  copy_mat(n, ra, A.v, A.ldv, Vc, n, A.s);
+  copy_mat(n, rb, B.v, B.ldv, Vc + (long long)ra * n, n, B.s);
   qr_blocked(cx, m, c, Uc, m, tauU, TpU);
   qr_blocked(cx, n, c, Vc, n, tauV, TpV);
+  tq.stop(cx, PH_QR);
+  PhaseTimer tc;
   const int kU = min(m, c), kV = min(n, c);
   const int k = kU;  // square blocks: kU == kV
-  double* RU = alloc(cx, (long long)kU * c);
-  double* RV = alloc(cx, (long long)kV * c);
-  double* G = alloc(cx, (long long)k * k);
-  double* J = alloc(cx, (long long)k * k);
-  double* sig = alloc(cx, k);
-  int* perm = reinterpret_cast<int*>(alloc(cx, k));
-  double* tail = alloc(cx, k + 1);
-  if (!RU || !RV || !G || !J || !sig || !perm || !tail) { cx.top = mark; return 0; }
-  for (long long e = threadIdx.x; e < (long long)kU * c; e += NT) {
-    const int i = (int)(e % kU), j = (int)(e / kU);
+  double* G = alloc_fast(cx, (long long)k * k);
+  const Mark after_g = mark(cx);  // H, RU, RV are released once the core is formed
+  double* H = alloc_fast(cx, (long long)k * k);
+  double* RU = alloc_fast(cx, (long long)kU * c);
+  double* RV = alloc_fast(cx, (long long)kV * c);
+  if (!G || !H || !RU || !RV) { release(cx, mk); return 0; }
+  for (int j = threadIdx.x >> 5; j < c; j += NWARP)
+    for (int i = threadIdx.x & 31; i < kU; i += 32) {
+    const long long e = (long long)j * kU + i;
     RU[e] = i <= j ? Uc[i + (long long)j * m] : 0.0;
   }
-  for (long long e = threadIdx.x; e < (long long)kV * c; e += NT) {
-    const int i = (int)(e % kV), j = (int)(e / kV);
+  for (int j = threadIdx.x >> 5; j < c; j += NWARP)
+    for (int i = threadIdx.x & 31; i < kV; i += 32) {
+    const long long e = (long long)j * kV + i;
     RV[e] = i <= j ? Vc[i + (long long)j * n] : 0.0;
   }
   __syncthreads();
-  gemm(false, true, kU, kV, c, 1.0, RU, kU, RV, kV, 0.0, G, k);
-  jacobi_svd(k, G, J, sig, perm);
+  gemm(false, true, kU, kV, ra, 1.0, RU, kU, RV, kV, 0.0, G, k);
+  gemm(false, true, kU, kV, rb, 1.0, RU + (long long)ra * kU, kU, RV + (long long)ra * kV, kV, 0.0, H, k);
+  double sa = 0.0, sb = 0.0, sc = 0.0;
+  for (long long e = threadIdx.x; e < (long long)k * k; e += NT) {
+    const double x = G[e], y = H[e];
+    sa = fma(x, x, sa);
+    sb = fma(y, y, sb);
+    const double z = x + y;
+    G[e] = z;
+    sc = fma(z, z, sc);
+  }
+  const double nA = sqrt(cta_sum(sa)), nB = sqrt(cta_sum(sb));
+  const double core2 = cta_sum(sc);
+  release(cx, after_g);
+  tc.stop(cx, PH_CORE);
   add_flops(cx, FK_ROUNDED_ADD, qr_cost(m, c) + qr_cost(n, c) + mm_cost(kU, c, kV) + svd_cost(kU));
-  // truncation (lowrank.py:204-213), decided by one thread
+  if (core2 == 0.0) { release(cx, mk); return 0; }
+  PhaseTimer ts;
+  // (3) QRCP of the core, truncated at rounding level
+  double* col2 = alloc_fast(cx, k);
+  double* col2o = alloc_fast(cx, k);
+  double* taus = alloc_fast(cx, k);
+  int* piv = reinterpret_cast<int*>(alloc_fast(cx, k));
+  if (!col2 || !col2o || !taus || !piv) { release(cx, mk); return 0; }
+  {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int cc = warp; cc < k; cc += NWARP) {
+      const double* gc = G + (long long)cc * k;
+      double s = 0.0;
+      for (int i = lane; i < k; i += 32) s = fma(gc[i], gc[i], s);
+      s = warp_sum(s);
+      if (lane == 0) { col2[cc] = s; col2o[cc] = s; piv[cc] = cc; }
+    }
+    __syncthreads();
+  }
+  const double eps_m = 2.220446049250313e-16;
+  double rem2 = 0.0;
+  PhaseTimer tqp;
+  const int kp = pivoted_qr(k, k, G, k, eps_m * eps_m * core2, k, core2, col2, col2o, piv, taus, &rem2);
+  tqp.stop(cx, PH_QRCP);
+  // X = P R1^T (k x kp): X[piv[j], a] = R1[a, j] for j >= a
+  double* X = alloc_fast(cx, (long long)k * max(kp, 1));
+  double* J = alloc_fast(cx, (long long)max(kp, 1) * max(kp, 1));
+  double* sig = alloc_fast(cx, max(kp, 1));
+  int* perm = reinterpret_cast<int*>(alloc_fast(cx, max(kp, 1)));
+  if (!X || !J || !sig || !perm) { release(cx, mk); return 0; }
+  for (int a = threadIdx.x >> 5; a < kp; a += NWARP)
+    for (int j = threadIdx.x & 31; j < k; j += 32) {
+    const long long e = (long long)a * k + j;
+    X[piv[j] + (long long)a * k] = j >= a ? G[a + (long long)j * k] : 0.0;
+  }
+  __syncthreads();
+  jacobi_cols(k, kp, X, k, J, kp, sig, perm, cx.flops);
+  ts.stop(cx, PH_SVD);
+  // (4) truncation (lowrank.py:204-213); the dropped QRCP remainder rem2
+  // (<= (eps_mach ||core||)^2) is counted in the total and in every tail
   __shared__ int s_rank;
   if (threadIdx.x == 0) {
     const double floor_ = NOISE_FLOOR * hypot(nA, nB);
     int significant = 0;
-    double total2 = 0.0;
-    for (int i = 0; i < k; ++i) {
+    double total2 = rem2;
+    for (int i = 0; i < kp; ++i) {
       const double si = sig[perm[i]];
       significant += si > floor_;
       total2 += si * si;
     }
     int rank = 0;
     if (total2 != 0.0 && significant != 0) {
-      tail[k] = 0.0;
-      double acc = 0.0;
-      for (int i = k - 1; i >= 0; --i) {
+      const double thresh2 = (eps * eps) * total2;
+      double acc = rem2;  // tail2[kp] (the reference's singular values below kp)
+      int first = (acc <= thresh2) ? kp : -1;
+      for (int i = kp - 1; i >= 0; --i) {
         const double si = sig[perm[i]];
         acc += si * si;
-        tail[i] = acc;
+        if (acc <= thresh2) first = i;
+        else break;
       }
-      const double thresh2 = (eps * eps) * total2;
-      int first = k;
-      for (int i = 0; i <= k; ++i)
-        if (tail[i] <= thresh2) { first = i; break; }
+      if (first < 0) first = kp;  // unreachable: tail2[k] = 0 <= thresh in the reference
       rank = min(first, significant);
     }
     s_rank = rank;
@@ -131,27 +196,31 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
     rank = cap;
   }
   if (rank > 0) {
+    PhaseTimer tb;
     double* ZU = alloc(cx, (long long)m * rank);
     double* ZV = alloc(cx, (long long)n * rank);
-    if (!ZU || !ZV) { cx.top = mark; return 0; }
-    for (long long e = threadIdx.x; e < (long long)m * rank; e += NT) {
-      const int i = (int)(e % m), j = (int)(e / m);
-      const int pj = perm[j];
-      ZU[e] = i < k ? G[i + (long long)pj * k] / sig[pj] : 0.0;
+    if (!ZU || !ZV) { release(cx, mk); return 0; }
+    // ZU(0:k) = [J_r; 0] then Q_core, ZV(0:k) = W_r
+    for (int j = threadIdx.x >> 5; j < rank; j += NWARP)
+      for (int i = threadIdx.x & 31; i < m; i += 32) {
+      const long long e = (long long)j * m + i;
+      ZU[e] = i < kp ? J[i + (long long)perm[j] * kp] : 0.0;
     }
-    for (long long e = threadIdx.x; e < (long long)n * rank; e += NT) {
-      const int i = (int)(e % n), j = (int)(e / n);
-      const int pj = perm[j];
-      ZV[e] = i < k ? J[i + (long long)pj * k] * sig[pj] : 0.0;
+    for (int j = threadIdx.x >> 5; j < rank; j += NWARP)
+      for (int i = threadIdx.x & 31; i < n; i += 32) {
+      const long long e = (long long)j * n + i;
+      ZV[e] = i < k ? X[i + (long long)perm[j] * k] : 0.0;
     }
     __syncthreads();
+    apply_reflectors(k, kp, G, k, taus, ZU, m, rank);
     qr_apply(cx, m, kU, Uc, m, TpU, ZU, m, rank, false);
     qr_apply(cx, n, kV, Vc, n, TpV, ZV, n, rank, false);
     copy_mat(m, rank, ZU, m, du, lddu);
     copy_mat(n, rank, ZV, n, dv, lddv);
     add_flops(cx, FK_ROUNDED_ADD, mm_cost(m, kU, rank) + mm_cost(n, kV, rank));
+    tb.stop(cx, PH_BACK);
   }
-  cx.top = mark;
+  release(cx, mk);
   return rank;
 }
 

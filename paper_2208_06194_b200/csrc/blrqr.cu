@@ -22,6 +22,14 @@ using namespace blr;
 
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+static constexpr int SMEM_BYTES = SMEM_ARENA * (int)sizeof(double);
+
+// every kernel below uses the dynamic shared-memory arena (> 48 KB opt-in)
+template <class K>
+static void smem_optin(K kernel) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+}
+
 // ===========================================================================
 // kernels
 // ===========================================================================
@@ -39,6 +47,7 @@ __global__ void __launch_bounds__(NT) k_rounded_add(int nb, int m, int n, const 
     const int r = rounded_add(cx, A, B, eps, uo[t], m, vo[t], n, cap);
     if (threadIdx.x == 0) ro[t] = r;
     cx.top = 0;
+    cx.stop = 0;
     __syncthreads();
   }
 }
@@ -62,6 +71,7 @@ __global__ void __launch_bounds__(NT) k_compress(int nb, int m, int n, const dou
     }
     if (threadIdx.x == 0) ro[t] = r;
     cx.top = 0;
+    cx.stop = 0;
     __syncthreads();
   }
 }
@@ -105,6 +115,7 @@ __global__ void __launch_bounds__(NT) k_dense_to_blr(const double* a, long long 
       if (threadIdx.x == 0) g.rank[c] = -1;
     }
     cx.top = 0;
+    cx.stop = 0;
     __syncthreads();
   }
 }
@@ -116,8 +127,9 @@ __global__ void __launch_bounds__(NT) k_geqrt(int m, int n, const double* a, dou
   if (!A) return;
   copy_mat(m, n, a, m, A, m);
   geqrt_inplace(cx, m, n, A, m, y, m, t, n);
-  for (long long e = threadIdx.x; e < (long long)n * n; e += NT) {
-    const int i = (int)(e % n), j = (int)(e / n);
+  for (int j = threadIdx.x >> 5; j < n; j += NWARP)
+    for (int i = threadIdx.x & 31; i < n; i += 32) {
+    const long long e = (long long)j * n + i;
     r[e] = i <= j ? A[i + (long long)j * m] : 0.0;
   }
 }
@@ -140,8 +152,9 @@ __global__ void __launch_bounds__(NT) k_tpqrt(int n, int k, const double* rt, co
   }
   copy_mat(k, n, ab, k, y, k);
   tpqrt(cx, n, k, rn, n, y, k, t, n);
-  for (long long e = threadIdx.x; e < (long long)n * n; e += NT) {
-    const int i = (int)(e % n), j = (int)(e / n);
+  for (int j = threadIdx.x >> 5; j < n; j += NWARP)
+    for (int i = threadIdx.x & 31; i < n; i += 32) {
+    const long long e = (long long)j * n + i;
     if (i > j) rn[e] = 0.0;
   }
   add_flops(cx, FK_UPDATE_QR, qr_cost(n + k, n) + tgen_cost(n + k, n));
@@ -231,8 +244,9 @@ __global__ void __launch_bounds__(NT) k_lr_product(int op, int m, int k, int n, 
       gemm(false, false, m, r, k, 1.0, d, m, u, k, 0.0, X, m);
       qr_blocked(cx, m, r, X, m, tau, Tp);
       const int kr = min(m, r);
-      for (long long e = threadIdx.x; e < (long long)kr * r; e += NT) {
-        const int i = (int)(e % kr), j = (int)(e / kr);
+      for (int j = threadIdx.x >> 5; j < r; j += NWARP)
+        for (int i = threadIdx.x & 31; i < kr; i += 32) {
+        const long long e = (long long)j * kr + i;
         Rr[e] = i <= j ? X[i + (long long)j * m] : 0.0;
       }
       // Q (m x kr): apply reflectors to identity slab
@@ -266,8 +280,9 @@ __global__ void __launch_bounds__(NT) k_lr_product(int op, int m, int k, int n, 
       gemm(false, true, m, r2, r, 1.0, u, m, core, r2, 0.0, X, m);  // a.u @ core^T
       qr_blocked(cx, m, r2, X, m, tau, Tp);
       const int kr = min(m, r2);
-      for (long long e = threadIdx.x; e < (long long)kr * r2; e += NT) {
-        const int i = (int)(e % kr), j = (int)(e / kr);
+      for (int j = threadIdx.x >> 5; j < r2; j += NWARP)
+        for (int i = threadIdx.x & 31; i < kr; i += 32) {
+        const long long e = (long long)j * kr + i;
         Rr[e] = i <= j ? X[i + (long long)j * m] : 0.0;
       }
       for (long long e = threadIdx.x; e < (long long)m * kr; e += NT) ou[e] = ((e % m) == (e / m)) ? 1.0 : 0.0;
@@ -281,7 +296,7 @@ __global__ void __launch_bounds__(NT) k_lr_product(int op, int m, int k, int n, 
 }
 
 // one level (or any contiguous range) of tiled tasks, one CTA per task
-__global__ void __launch_bounds__(NT, 2) k_tiled(const blrqr_task* tasks, long long t0, long long t1, blrqr_grid g,
+__global__ void __launch_bounds__(NT, 1) k_tiled(const blrqr_task* tasks, long long t0, long long t1, blrqr_grid g,
                                                blrqr_refl rf, double eps, double* ws, long long wsp, int* status,
                                                unsigned long long* flops) {
   Ctx cx = make_ctx(ws, wsp, status, flops);
@@ -294,6 +309,7 @@ __global__ void __launch_bounds__(NT, 2) k_tiled(const blrqr_task* tasks, long l
       default: tiled_trap(cx, g, rf, eps, tk.k, tk.i, tk.j); break;
     }
     cx.top = 0;
+    cx.stop = 0;
     __syncthreads();
   }
 }
@@ -333,6 +349,23 @@ __global__ void __launch_bounds__(NT) k_grid_pack(blrqr_grid g, double* stage, c
 // host side
 // ===========================================================================
 
+static std::once_flag g_optin_once;
+static void init_kernels() {
+  std::call_once(g_optin_once, [] {
+    smem_optin(k_rounded_add);
+    smem_optin(k_compress);
+    smem_optin(k_dense_to_blr);
+    smem_optin(k_geqrt);
+    smem_optin(k_apply_wy);
+    smem_optin(k_tpqrt);
+    smem_optin(k_apply_tp);
+    smem_optin(k_mgs_panel);
+    smem_optin(k_lr_product);
+    smem_optin(k_tiled);
+  });
+}
+#define INIT_KERNELS() init_kernels()
+
 extern "C" {
 
 int blrqr_version(void) { return 1; }
@@ -345,7 +378,7 @@ int64_t blrqr_workspace_doubles(int b, int cap, int max_panel_rows) {
 int blrqr_default_ctas(void) {
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return 2 * sms;
+  return sms;  // one 512-thread CTA per SM (180 KB shared arena each)
 }
 
 int blrqr_rounded_add_batched(int nbatch, int m, int n, const double* const* ua, const double* const* va,
@@ -357,7 +390,8 @@ int blrqr_rounded_add_batched(int nbatch, int m, int n, const double* const* ua,
   if (!(eps > 0.0 && eps < 1.0)) return -2;
   if (nbatch == 0) return 0;
   const int grid = std::max(1, std::min(nbatch, nctas));
-  k_rounded_add<<<grid, NT, 0, as_stream(stream)>>>(nbatch, m, n, ua, va, ra, ub, vb, rb, uo, vo, ro, cap, eps, ws,
+  INIT_KERNELS();
+  k_rounded_add<<<grid, NT, SMEM_BYTES, as_stream(stream)>>>(nbatch, m, n, ua, va, ra, ub, vb, rb, uo, vo, ro, cap, eps, ws,
                                                    ws_per_cta, status, flops);
   CK(cudaGetLastError());
   return 0;
@@ -370,7 +404,8 @@ int blrqr_compress_batched(int nbatch, int m, int n, const double* const* a, dou
   if (!(eps > 0.0 && eps < 1.0)) return -2;
   if (nbatch == 0) return 0;
   const int grid = std::max(1, std::min(nbatch, nctas));
-  k_compress<<<grid, NT, 0, as_stream(stream)>>>(nbatch, m, n, a, uo, vo, ro, cap, eps, max_rank, ws, ws_per_cta,
+  INIT_KERNELS();
+  k_compress<<<grid, NT, SMEM_BYTES, as_stream(stream)>>>(nbatch, m, n, a, uo, vo, ro, cap, eps, max_rank, ws, ws_per_cta,
                                                 status, flops);
   CK(cudaGetLastError());
   return 0;
@@ -380,7 +415,8 @@ int blrqr_lr_product(int op, int m, int k, int n, const double* u, const double*
                      const double* u2, const double* v2, int r2, double* out_u, double* out_v, int* out_r,
                      double* ws, int64_t ws_doubles, int* status, unsigned long long* flops, void* stream) {
   if (op < 0 || op > 3) return -1;
-  k_lr_product<<<1, NT, 0, as_stream(stream)>>>(op, m, k, n, u, v, r, d, u2, v2, r2, out_u, out_v, out_r, ws,
+  INIT_KERNELS();
+  k_lr_product<<<1, NT, SMEM_BYTES, as_stream(stream)>>>(op, m, k, n, u, v, r, d, u2, v2, r2, out_u, out_v, out_r, ws,
                                                ws_doubles, status, flops);
   CK(cudaGetLastError());
   return 0;
@@ -389,7 +425,8 @@ int blrqr_lr_product(int op, int m, int k, int n, const double* u, const double*
 int blrqr_geqrt(int m, int n, const double* a, double* y, double* t, double* r, double* ws, int64_t ws_doubles,
                 int* status, unsigned long long* flops, void* stream) {
   if (m < n || n <= 0) return -1;
-  k_geqrt<<<1, NT, 0, as_stream(stream)>>>(m, n, a, y, t, r, ws, ws_doubles, status, flops);
+  INIT_KERNELS();
+  k_geqrt<<<1, NT, SMEM_BYTES, as_stream(stream)>>>(m, n, a, y, t, r, ws, ws_doubles, status, flops);
   CK(cudaGetLastError());
   return 0;
 }
@@ -398,7 +435,8 @@ int blrqr_apply_wy(int m, int n, int nc, const double* y, const double* t, doubl
                    int64_t ws_doubles, int* status, unsigned long long* flops, void* stream) {
   if (m <= 0 || n <= 0 || nc < 0) return -1;
   if (nc == 0) return 0;
-  k_apply_wy<<<1, NT, 0, as_stream(stream)>>>(m, n, nc, y, t, c, transpose, ws, ws_doubles, status, flops);
+  INIT_KERNELS();
+  k_apply_wy<<<1, NT, SMEM_BYTES, as_stream(stream)>>>(m, n, nc, y, t, c, transpose, ws, ws_doubles, status, flops);
   CK(cudaGetLastError());
   return 0;
 }
@@ -406,7 +444,8 @@ int blrqr_apply_wy(int m, int n, int nc, const double* y, const double* t, doubl
 int blrqr_tpqrt(int n, int k, const double* r_top, const double* a_bot, double* r_new, double* y, double* t,
                 double* ws, int64_t ws_doubles, int* status, unsigned long long* flops, void* stream) {
   if (n <= 0 || k < 0) return -1;
-  k_tpqrt<<<1, NT, 0, as_stream(stream)>>>(n, k, r_top, a_bot, r_new, y, t, ws, ws_doubles, status, flops);
+  INIT_KERNELS();
+  k_tpqrt<<<1, NT, SMEM_BYTES, as_stream(stream)>>>(n, k, r_top, a_bot, r_new, y, t, ws, ws_doubles, status, flops);
   CK(cudaGetLastError());
   return 0;
 }
@@ -416,7 +455,8 @@ int blrqr_apply_tp(int n, int k, int nc, const double* y, const double* t, doubl
                    void* stream) {
   if (n <= 0 || k < 0 || nc < 0) return -1;
   if (nc == 0) return 0;
-  k_apply_tp<<<1, NT, 0, as_stream(stream)>>>(n, k, nc, y, t, c_top, c_bot, transpose, ws, ws_doubles, status,
+  INIT_KERNELS();
+  k_apply_tp<<<1, NT, SMEM_BYTES, as_stream(stream)>>>(n, k, nc, y, t, c_top, c_bot, transpose, ws, ws_doubles, status,
                                              flops);
   CK(cudaGetLastError());
   return 0;
@@ -425,7 +465,8 @@ int blrqr_apply_tp(int n, int k, int nc, const double* y, const double* t, doubl
 int blrqr_mgs_panel(int m, int n, const double* a, double* q, double* r, double* ws, int64_t ws_doubles,
                     int* status, unsigned long long* flops, void* stream) {
   if (m < n || n <= 0) return -1;
-  k_mgs_panel<<<1, NT, 0, as_stream(stream)>>>(m, n, a, q, r, ws, ws_doubles, status, flops);
+  INIT_KERNELS();
+  k_mgs_panel<<<1, NT, SMEM_BYTES, as_stream(stream)>>>(m, n, a, q, r, ws, ws_doubles, status, flops);
   CK(cudaGetLastError());
   return 0;
 }
@@ -438,7 +479,8 @@ int blrqr_dense_to_blr(const double* a, int64_t lda, blrqr_grid* g, unsigned cha
   const int max_rank = (int)(fallback * g->b);
   const int cells = g->p * g->q;
   const int grid = std::max(1, std::min(cells, nctas));
-  k_dense_to_blr<<<grid, NT, 0, as_stream(stream)>>>(a, lda, *g, lowrank_io, eps, max_rank, ws, ws_per_cta,
+  INIT_KERNELS();
+  k_dense_to_blr<<<grid, NT, SMEM_BYTES, as_stream(stream)>>>(a, lda, *g, lowrank_io, eps, max_rank, ws, ws_per_cta,
                                                     status, flops);
   CK(cudaGetLastError());
   return 0;
@@ -542,7 +584,8 @@ int blrqr_tiled_run(const blrqr_grid* g, const blrqr_refl* rf, const blrqr_task*
     const int64_t t0 = level_start_host[l], t1 = level_start_host[l + 1];
     if (t1 <= t0) continue;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(t1 - t0, nctas));
-    k_tiled<<<grid, NT, 0, as_stream(stream)>>>(tasks_dev, t0, t1, *g, *rf, eps, ws, ws_per_cta, status, flops);
+    INIT_KERNELS();
+    k_tiled<<<grid, NT, SMEM_BYTES, as_stream(stream)>>>(tasks_dev, t0, t1, *g, *rf, eps, ws, ws_per_cta, status, flops);
     CK(cudaGetLastError());
   }
   return 0;

@@ -11,7 +11,7 @@
 
 namespace blr {
 
-constexpr int NT = 256;          // threads per CTA
+constexpr int NT = 512;          // threads per CTA (one CTA per SM)
 constexpr int NWARP = NT / 32;
 
 // status bits (OR-ed into a device word; see include/blrqr.h)
@@ -29,12 +29,28 @@ enum FlopKind : int {
 };
 
 struct Ctx {
-  double* base;            // this CTA's arena
+  double* base;            // this CTA's global (L2/HBM) arena
   long long cap;           // doubles
   long long top;           // bump pointer (doubles), identical in all threads
+  double* sbase;           // this CTA's shared-memory arena (dynamic smem)
+  int scap, stop;          // doubles
   int* status;             // global status word
   unsigned long long* flops;  // FK_COUNT counters (global)
 };
+
+// dynamic shared-memory arena per CTA (doubles): one 512-thread CTA per SM
+// owns ~180 KB next to the static GEMM scratch (see GEMM_SMEM)
+constexpr int SMEM_ARENA = 23040;  // 180 KB
+
+struct Mark {
+  long long g;
+  int s;
+};
+__device__ __forceinline__ Mark mark(const Ctx& c) { return Mark{c.top, c.stop}; }
+__device__ __forceinline__ void release(Ctx& c, Mark m) {
+  c.top = m.g;
+  c.stop = m.s;
+}
 
 __device__ __forceinline__ void set_status(Ctx& c, int bits) {
   if (threadIdx.x == 0) atomicOr(c.status, bits);
@@ -42,6 +58,26 @@ __device__ __forceinline__ void set_status(Ctx& c, int bits) {
 __device__ __forceinline__ void add_flops(Ctx& c, int kind, long long n) {
   if (threadIdx.x == 0 && c.flops) atomicAdd(c.flops + kind, (unsigned long long)n);
 }
+
+// Phase cycle counters (SM clock, thread 0) in flops[16 + phase]: cheap
+// always-on attribution of where a task's time goes.
+enum Phase : int {
+  PH_NORM = 0, PH_QR, PH_CORE, PH_SVD, PH_BACK, PH_PRODUCT, PH_TPQRT, PH_GEQRT, PH_APPLYWY, PH_RRQR,
+  PH_EXPAND, PH_TASK, PH_QRCP, PH_JSWEEPS, PH_JCALLS, PH_COUNT
+};
+constexpr int PROF_BASE = 16;
+__device__ __forceinline__ long long sm_clock() {
+  long long t;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+  return t;
+}
+struct PhaseTimer {
+  long long t0;
+  __device__ __forceinline__ PhaseTimer() : t0(sm_clock()) {}
+  __device__ __forceinline__ void stop(Ctx& c, int ph) {
+    if (threadIdx.x == 0 && c.flops) atomicAdd(c.flops + PROF_BASE + ph, (unsigned long long)(sm_clock() - t0));
+  }
+};
 
 // Arena allocation: every thread executes it with identical arguments.
 // Returns nullptr (and flags ST_ARENA_OVERFLOW) if the arena is exhausted.
@@ -54,6 +90,21 @@ __device__ __forceinline__ double* alloc(Ctx& c, long long n) {
   double* p = c.base + c.top;
   c.top += n;
   return p;
+}
+
+// Shared-memory allocation (nullptr when it does not fit; no status).
+__device__ __forceinline__ double* salloc(Ctx& c, long long n) {
+  n = (n + 3) & ~3LL;  // 32-byte alignment
+  if (c.stop + n > c.scap) return nullptr;
+  double* p = c.sbase + c.stop;
+  c.stop += (int)n;
+  return p;
+}
+
+// Shared memory when it fits, else the global arena.
+__device__ __forceinline__ double* alloc_fast(Ctx& c, long long n) {
+  double* p = salloc(c, n);
+  return p ? p : alloc(c, n);
 }
 
 // closed-form model costs (flops.py:28-55)
@@ -129,33 +180,37 @@ __device__ __forceinline__ int cta_argmax(double v, int idx) {
 // elementwise helpers
 // ---------------------------------------------------------------------------
 
-// B(0:m,0:n) = alpha * A(0:m,0:n)
+// B(0:m,0:n) = alpha * A(0:m,0:n)   (warp per column, lanes down the rows)
 __device__ void copy_mat(int m, int n, const double* A, int lda, double* B, int ldb, double alpha = 1.0) {
-  const long long tot = (long long)m * n;
-  for (long long e = threadIdx.x; e < tot; e += NT) {
-    int i = (int)(e % m), j = (int)(e / m);
-    B[i + (long long)j * ldb] = alpha * A[i + (long long)j * lda];
+  for (int j = threadIdx.x >> 5; j < n; j += NWARP) {
+    const double* a = A + (long long)j * lda;
+    double* b = B + (long long)j * ldb;
+    for (int i = threadIdx.x & 31; i < m; i += 32) b[i] = alpha * a[i];
   }
   __syncthreads();
 }
 
 __device__ void zero_mat(int m, int n, double* A, int lda) {
-  const long long tot = (long long)m * n;
-  for (long long e = threadIdx.x; e < tot; e += NT) {
-    int i = (int)(e % m), j = (int)(e / m);
-    A[i + (long long)j * lda] = 0.0;
+  for (int j = threadIdx.x >> 5; j < n; j += NWARP) {
+    double* a = A + (long long)j * lda;
+    for (int i = threadIdx.x & 31; i < m; i += 32) a[i] = 0.0;
   }
   __syncthreads();
 }
 
-// B = A^T (A is m x n)
+// B = A^T (A is m x n); 32x32 tiles through shared memory
 __device__ void transpose_mat(int m, int n, const double* A, int lda, double* B, int ldb) {
-  const long long tot = (long long)m * n;
-  for (long long e = threadIdx.x; e < tot; e += NT) {
-    int j = (int)(e % n), i = (int)(e / n);
-    B[j + (long long)i * ldb] = A[i + (long long)j * lda];
-  }
-  __syncthreads();
+  __shared__ double tile[32][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i0 = 0; i0 < m; i0 += 32)
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      for (int jj = warp; jj < 32; jj += NWARP)
+        if (j0 + jj < n && i0 + lane < m) tile[jj][lane] = A[(i0 + lane) + (long long)(j0 + jj) * lda];
+      __syncthreads();
+      for (int ii = warp; ii < 32; ii += NWARP)
+        if (i0 + ii < m && j0 + lane < n) B[(j0 + lane) + (long long)(i0 + ii) * ldb] = tile[lane][ii];
+      __syncthreads();
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -164,16 +219,16 @@ __device__ void transpose_mat(int m, int n, const double* A, int lda, double* B,
 // Shared-memory tiled DFMA; tile shape chosen from N.
 // ---------------------------------------------------------------------------
 
-constexpr int GEMM_SMEM = 4400;  // doubles of shared scratch shared by all GEMM tile shapes
+constexpr int GEMM_SMEM = 2600;  // doubles of shared scratch shared by all GEMM tile shapes
 __device__ __forceinline__ double* gemm_smem() {
   __shared__ double buf[GEMM_SMEM];
   return buf;
 }
 
-template <int BM, int BN, int BK>
+template <int BM, int BN, int BK, int TY>
 __device__ __noinline__ void gemm_tiled(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, int lda,
                            const double* B, int ldb, double beta, double* C, int ldc) {
-  constexpr int TY = (BM >= 16 ? 16 : BM), TX = NT / TY;  // thread grid TY x TX
+  constexpr int TX = NT / TY;  // thread grid TY x TX
   constexpr int TM = BM / TY, TN = BN / TX;
   static_assert(TM * TN * NT == BM * BN, "tile");
   static_assert(BK * (BM + 1) + BK * (BN + 1) <= GEMM_SMEM, "smem");
@@ -235,8 +290,65 @@ __device__ __noinline__ void gemm_tiled(bool ta, bool tb, int M, int N, int K, d
   __syncthreads();
 }
 
+// Inner-product GEMM C = alpha A^T B + beta C for long K and few outputs:
+// each warp owns a 4x4 output block, lanes stride over K (coalesced column
+// reads), butterfly reduction.  Avoids the tile path's zero-padded K-steps.
+__device__ __noinline__ void gemm_tn_dot(int M, int N, int K, double alpha, const double* A, int lda,
+                                         const double* B, int ldb, double beta, double* C, int ldc) {
+  constexpr int R = 4;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nbm = (M + R - 1) / R, nbn = (N + R - 1) / R;
+  for (int blk = warp; blk < nbm * nbn; blk += NWARP) {
+    const int i0 = (blk % nbm) * R, j0 = (blk / nbm) * R;
+    double acc[R][R];
+#pragma unroll
+    for (int a = 0; a < R; ++a)
+#pragma unroll
+      for (int b = 0; b < R; ++b) acc[a][b] = 0.0;
+    const double* Ac[R];
+    const double* Bc[R];
+#pragma unroll
+    for (int a = 0; a < R; ++a) {
+      Ac[a] = A + (long long)min(i0 + a, M - 1) * lda;
+      Bc[a] = B + (long long)min(j0 + a, N - 1) * ldb;
+    }
+    for (int k = lane; k < K; k += 32) {
+      double av[R], bv[R];
+#pragma unroll
+      for (int a = 0; a < R; ++a) { av[a] = Ac[a][k]; bv[a] = Bc[a][k]; }
+#pragma unroll
+      for (int a = 0; a < R; ++a)
+#pragma unroll
+        for (int b = 0; b < R; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+    }
+#pragma unroll
+    for (int a = 0; a < R; ++a)
+#pragma unroll
+      for (int b = 0; b < R; ++b) acc[a][b] = warp_sum(acc[a][b]);
+    if (lane < R * R) {
+      const int a = lane / R, b = lane % R;
+      double v = 0.0;
+#pragma unroll
+      for (int x = 0; x < R; ++x)
+#pragma unroll
+        for (int y = 0; y < R; ++y)
+          if (x == a && y == b) v = acc[x][y];
+      const int gi = i0 + a, gj = j0 + b;
+      if (gi < M && gj < N) {
+        double* c = C + gi + (long long)gj * ldc;
+        *c = beta == 0.0 ? alpha * v : alpha * v + beta * (*c);
+      }
+    }
+  }
+  __syncthreads();
+}
+
 __device__ __noinline__ void gemm(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, int lda,
                      const double* B, int ldb, double beta, double* C, int ldc) {
+  if (ta && !tb && M > 0 && N > 0 && K >= 64 && (long long)M * N <= 4096) {
+    gemm_tn_dot(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    return;
+  }
   if (M <= 0 || N <= 0) return;
   if (K <= 0) {  // C = beta * C
     const long long tot = (long long)M * N;
@@ -249,13 +361,13 @@ __device__ __noinline__ void gemm(bool ta, bool tb, int M, int N, int K, double 
     return;
   }
   if (M <= 16 && N > 64)
-    gemm_tiled<16, 256, 16>(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    gemm_tiled<16, 256, 8, 16>(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
   else if (N <= 16)
-    gemm_tiled<256, 16, 16>(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    gemm_tiled<256, 16, 8, 32>(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
   else if (N <= 32 || M >= 4 * N)
-    gemm_tiled<128, 32, 16>(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    gemm_tiled<128, 32, 16, 16>(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
   else
-    gemm_tiled<64, 64, 16>(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    gemm_tiled<64, 64, 16, 16>(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
 }
 
 }  // namespace blr

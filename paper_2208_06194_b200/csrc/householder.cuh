@@ -9,7 +9,7 @@
 
 namespace blr {
 
-constexpr int QR_NB = 32;  // panel width of the blocked factorizations
+constexpr int QR_NB = 16;  // panel width of the blocked factorizations (smem-staged)
 
 // Householder reflector for x = [alpha; X(0:n)] (X strided).  On exit X holds
 // v(1:), returns (tau, beta) via refs.  All threads call; result uniform.
@@ -117,8 +117,9 @@ __device__ __noinline__ void build_t_full(Ctx& cx, int n, const double* S, int l
     const int w = min(QR_NB, n - j0);
     t_block_recurrence(j0, w, S, lds, tau, T, ldt);
     // zero T(J, 0:j0) (strict lower blocks left of the diagonal block)
-    for (long long e = threadIdx.x; e < (long long)w * j0; e += NT) {
-      const int a = (int)(e % w), c = (int)(e / w);
+    for (int c = threadIdx.x >> 5; c < j0; c += NWARP)
+      for (int a = threadIdx.x & 31; a < w; a += 32) {
+      const long long e = (long long)c * w + a;
       T[(j0 + a) + (long long)c * ldt] = 0.0;
     }
     if (j0 > 0) {
@@ -140,16 +141,36 @@ __device__ __noinline__ void build_t_full(Ctx& cx, int n, const double* S, int l
 // ---------------------------------------------------------------------------
 __device__ __noinline__ void qr_blocked(Ctx& cx, int m, int n, double* A, int lda, double* tau, double* Tp) {
   const int k = min(m, n);
-  const long long mark = cx.top;
-  double* Y = alloc(cx, (long long)m * QR_NB);
-  double* S = alloc(cx, (long long)QR_NB * QR_NB);
+  const Mark mk = mark(cx);
+  double* S = alloc_fast(cx, (long long)QR_NB * QR_NB);
   double* W = alloc(cx, (long long)QR_NB * max(n, 1));
-  if (!Y || !S || !W) { cx.top = mark; return; }
+  if (!S || !W) { release(cx, mk); return; }
   for (int c0 = 0; c0 < k; c0 += QR_NB) {
     const int w = min(QR_NB, k - c0);
-    qr_panel_unblocked(m, c0, w, A, lda, tau);
     const int h = m - c0;
-    extract_y(m, c0, w, A, lda, Y, h);
+    // stage the h x w panel in shared memory when it fits; factor it there
+    const Mark pm = mark(cx);
+    double* P = salloc(cx, (long long)h * w);
+    double* Y;
+    if (P) {
+      copy_mat(h, w, A + c0 + (long long)c0 * lda, lda, P, h);
+      qr_panel_unblocked(h, 0, w, P, h, tau + c0);
+      copy_mat(h, w, P, h, A + c0 + (long long)c0 * lda, lda);
+      // P becomes the explicit unit-lower-trapezoidal Y in place
+      for (int jj = threadIdx.x >> 5; jj < w; jj += NWARP)
+        for (int i = threadIdx.x & 31; i < h; i += 32) {
+        const long long e = (long long)jj * h + i;
+        if (i < jj) P[e] = 0.0;
+        else if (i == jj) P[e] = 1.0;
+      }
+      __syncthreads();
+      Y = P;
+    } else {
+      qr_panel_unblocked(m, c0, w, A, lda, tau);
+      Y = alloc(cx, (long long)h * QR_NB);
+      if (!Y) { release(cx, mk); return; }
+      extract_y(m, c0, w, A, lda, Y, h);
+    }
     // panel T: S = Y^T Y, recurrence
     gemm(true, false, w, w, h, 1.0, Y, h, Y, h, 0.0, S, QR_NB);
     double* T = Tp + (long long)c0 * QR_NB;
@@ -159,23 +180,26 @@ __device__ __noinline__ void qr_blocked(Ctx& cx, int m, int n, double* A, int ld
       double* A2 = A + c0 + (long long)(c0 + w) * lda;
       // A2 = (I - Y T Y^T)^T A2 = A2 - Y T^T (Y^T A2)
       gemm(true, false, w, n2, h, 1.0, Y, h, A2, lda, 0.0, W, QR_NB);
-      // W2 = T^T W computed in place column by column (T upper => T^T lower)
+      // W <- T^T W in place per column (T upper => T^T lower)
       for (long long e = threadIdx.x; e < (long long)n2; e += NT) {
         double* wc = W + e * QR_NB;
         double tmp[QR_NB];
-#pragma unroll 4
-        for (int a = 0; a < w; ++a) tmp[a] = wc[a];
-        for (int a = w - 1; a >= 0; --a) {
+#pragma unroll
+        for (int a = 0; a < QR_NB; ++a) tmp[a] = a < w ? wc[a] : 0.0;
+#pragma unroll
+        for (int a = QR_NB - 1; a >= 0; --a) {
           double s = 0.0;
+#pragma unroll
           for (int b2 = 0; b2 <= a; ++b2) s = fma(T[b2 + a * QR_NB], tmp[b2], s);
-          wc[a] = s;
+          if (a < w) wc[a] = s;
         }
       }
       __syncthreads();
       gemm(false, false, h, n2, w, -1.0, Y, h, W, QR_NB, 1.0, A2, lda);
     }
+    release(cx, pm);
   }
-  cx.top = mark;
+  release(cx, mk);
 }
 
 // Apply Q = H_0 H_1 ... H_{k-1} (from qr_blocked of an m-row matrix) to Z
@@ -262,8 +286,9 @@ __device__ __noinline__ void tpqrt(Ctx& cx, int n, int k, double* R, int ldr, do
       }
       __syncthreads();
       // R_JL -= W ; B_L -= Y_J W
-      for (long long e = threadIdx.x; e < (long long)w * n2; e += NT) {
-        const int a = (int)(e % w), c = (int)(e / w);
+      for (int c = threadIdx.x >> 5; c < n2; c += NWARP)
+        for (int a = threadIdx.x & 31; a < w; a += 32) {
+        const long long e = (long long)c * w + a;
         RJL[a + (long long)c * ldr] -= W[a + (long long)c * QR_NB];
       }
       __syncthreads();

@@ -10,31 +10,36 @@
 
 namespace blr {
 
-// One-sided Jacobi on G (k x k, ld k).  On exit G holds W = U*Sigma
-// (unsorted), J (k x k, ld k) the accumulated right rotations, sigma[k] the
-// column norms, perm[k] the indices sorted by descending sigma (stable).
-__device__ __noinline__ void jacobi_svd(int k, double* G, double* J, double* sigma, int* perm) {
+// One-sided Jacobi (Hestenes) on the ncols columns of X (rows x ncols, ldx):
+// X J = W with J (ncols x ncols, ldj) orthogonal and W's columns mutually
+// orthogonal.  On exit X holds W, sigma[c] = ||W_c||, perm = indices sorted by
+// descending sigma (stable).  Round-robin pair ordering, one warp per pair.
+__device__ __noinline__ void jacobi_cols(int rows, int ncols, double* X, int ldx, double* J, int ldj, double* sigma,
+                                         int* perm, unsigned long long* prof = nullptr) {
   __shared__ int s_rot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (long long e = threadIdx.x; e < (long long)k * k; e += NT) J[e] = (e % k == e / k) ? 1.0 : 0.0;
+  for (int j = threadIdx.x >> 5; j < ncols; j += NWARP)
+    for (int i = threadIdx.x & 31; i < ncols; i += 32) {
+    const long long e = (long long)j * ncols + i;
+    J[i + (long long)j * ldj] = (i == j) ? 1.0 : 0.0;
+  }
   __syncthreads();
-  const double tol = 2.220446049250313e-16 * (double)max(k, 1);
-  const int kk = (k + 1) & ~1;  // even number of players (one dummy when k odd)
+  const double tol = 2.220446049250313e-16 * (double)max(rows, 1);
+  const int kk = (ncols + 1) & ~1;  // even number of players (one dummy when odd)
   const int npairs = kk / 2;
-  for (int sweep = 0; sweep < 40 && k > 1; ++sweep) {
+  for (int sweep = 0; sweep < 40 && ncols > 1; ++sweep) {
     if (threadIdx.x == 0) s_rot = 0;
     __syncthreads();
     for (int rnd = 0; rnd < kk - 1; ++rnd) {
       for (int pi = warp; pi < npairs; pi += NWARP) {
-        // round-robin: player 0 fixed, others rotate
-        auto player = [&](int pos) { return pos == 0 ? 0 : 1 + (pos - 1 + rnd) % (kk - 1); };
-        int p = player(pi), q = player(kk - 1 - pi);
-        if (p >= k || q >= k) continue;
-        if (p > q) { int t = p; p = q; q = t; }
-        double* gp = G + (long long)p * k;
-        double* gq = G + (long long)q * k;
+        int p = pi == 0 ? 0 : 1 + (pi - 1 + rnd) % (kk - 1);
+        int q = 1 + (kk - 2 - pi + rnd) % (kk - 1);
+        if (p >= ncols || q >= ncols) continue;
+        if (p > q) { const int t = p; p = q; q = t; }
+        double* gp = X + (long long)p * ldx;
+        double* gq = X + (long long)q * ldx;
         double a = 0.0, b = 0.0, g = 0.0;
-        for (int i = lane; i < k; i += 32) {
+        for (int i = lane; i < rows; i += 32) {
           const double x = gp[i], y = gq[i];
           a = fma(x, x, a);
           b = fma(y, y, b);
@@ -48,14 +53,14 @@ __device__ __noinline__ void jacobi_svd(int k, double* G, double* J, double* sig
         const double zeta = (b - a) / (2.0 * g);
         const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
         const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-        for (int i = lane; i < k; i += 32) {
+        for (int i = lane; i < rows; i += 32) {
           const double x = gp[i], y = gq[i];
           gp[i] = c * x - s * y;
           gq[i] = s * x + c * y;
         }
-        double* jp = J + (long long)p * k;
-        double* jq = J + (long long)q * k;
-        for (int i = lane; i < k; i += 32) {
+        double* jp = J + (long long)p * ldj;
+        double* jq = J + (long long)q * ldj;
+        for (int i = lane; i < ncols; i += 32) {
           const double x = jp[i], y = jq[i];
           jp[i] = c * x - s * y;
           jq[i] = s * x + c * y;
@@ -66,22 +71,22 @@ __device__ __noinline__ void jacobi_svd(int k, double* G, double* J, double* sig
     }
     const int rot = s_rot;
     __syncthreads();
+    if (prof && threadIdx.x == 0) atomicAdd(prof + PROF_BASE + PH_JSWEEPS, 1ull);
     if (!rot) break;
   }
-  // column norms
-  for (int c = warp; c < k; c += NWARP) {
-    const double* gc = G + (long long)c * k;
+  if (prof && threadIdx.x == 0) atomicAdd(prof + PROF_BASE + PH_JCALLS, 1ull);
+  for (int c = warp; c < ncols; c += NWARP) {
+    const double* gc = X + (long long)c * ldx;
     double a = 0.0;
-    for (int i = lane; i < k; i += 32) a = fma(gc[i], gc[i], a);
+    for (int i = lane; i < rows; i += 32) a = fma(gc[i], gc[i], a);
     a = warp_sum(a);
     if (lane == 0) sigma[c] = sqrt(a);
   }
   __syncthreads();
-  // stable descending rank sort
-  for (int i = threadIdx.x; i < k; i += NT) {
+  for (int i = threadIdx.x; i < ncols; i += NT) {
     const double si = sigma[i];
     int r = 0;
-    for (int j = 0; j < k; ++j) {
+    for (int j = 0; j < ncols; ++j) {
       const double sj = sigma[j];
       r += (sj > si) || (sj == si && j < i);
     }
@@ -90,62 +95,39 @@ __device__ __noinline__ void jacobi_svd(int k, double* G, double* J, double* sig
   __syncthreads();
 }
 
-// ---------------------------------------------------------------------------
-// Truncated column-pivoted QR (lowrank.py:64-135): A (m x n, lda) is
-// overwritten.  Returns the rank (>= 0), or -1 when the rank would exceed
-// max_rank.  On success U (m x rank, ldu) = first rank columns of Q and
-// V (n x rank, ldv) with V[piv, :] = R[:rank, :]^T.
-// ---------------------------------------------------------------------------
-__device__ __noinline__ int rrqr_trunc(Ctx& cx, int m, int n, double* A, int lda, double eps, int max_rank, double* U, int ldu,
-                          double* V, int ldv) {
+// Column-pivoted Householder QR steps on A (m x n, lda), in place: pivot on
+// the largest running squared column norm (lowest index on ties), LAPACK
+// reflector, rank-1 trailing update, norm downdating with exact recompute
+// on cancellation (lowrank.py:89-120).  Stops when the remaining squared norm
+// is <= stop2, when min(m, n) steps are done, or (returning -1) when another
+// step would exceed max_steps.  col2/col2o/piv/taus are caller scratch
+// (n, n, n, min(m,n)).  *remaining2 receives the final remainder.
+__device__ __noinline__ int pivoted_qr(int m, int n, double* A, int lda, double stop2, int max_steps, double fro2,
+                                       double* col2, double* col2o, int* piv, double* taus, double* remaining2) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long mark = cx.top;
-  double* col2 = alloc(cx, n);
-  double* col2o = alloc(cx, n);
-  double* taus = alloc(cx, min(m, n) + 1);
-  int* piv = reinterpret_cast<int*>(alloc(cx, n));
-  if (!col2 || !col2o || !taus || !piv) { cx.top = mark; return -2; }
-  // squared column norms and ||A||_F^2 (sum of column norms, as np.sum(a*a))
-  for (int c = warp; c < n; c += NWARP) {
-    const double* ac = A + (long long)c * lda;
-    double s = 0.0;
-    for (int i = lane; i < m; i += 32) s = fma(ac[i], ac[i], s);
-    s = warp_sum(s);
-    if (lane == 0) { col2[c] = s; col2o[c] = s; piv[c] = c; }
-  }
-  __syncthreads();
-  double fro2 = 0.0;
-  {
-    double s = 0.0;
-    for (int c = threadIdx.x; c < n; c += NT) s += col2[c];
-    fro2 = cta_sum(s);
-  }
-  if (fro2 == 0.0) { cx.top = mark; return 0; }
-  const double thresh2 = (eps * eps) * fro2;
   const int limit = min(m, n);
   int rank = 0;
   double remaining = fro2;
   int result = 0;
-  while (remaining > thresh2) {
+  while (remaining > stop2) {
     if (rank >= limit) break;
-    if (rank >= max_rank) { result = -1; break; }
+    if (rank >= max_steps) { result = -1; break; }
     const int k = rank;
-    // pivot: argmax col2[k:] (lowest index on ties)
     double bv = -INFINITY;
     int bi = 0x7fffffff;
     for (int c = k + threadIdx.x; c < n; c += NT) {
       const double v = col2[c];
-      if (v > bv) { bv = v; bi = c; }  // ascending c per thread: first max kept
+      if (v > bv) { bv = v; bi = c; }
     }
     const int j = cta_argmax(bv, bi);
     if (j != k) {
       double* ak = A + (long long)k * lda;
       double* aj = A + (long long)j * lda;
-      for (int i = threadIdx.x; i < m; i += NT) { double t = ak[i]; ak[i] = aj[i]; aj[i] = t; }
+      for (int i = threadIdx.x; i < m; i += NT) { const double t = ak[i]; ak[i] = aj[i]; aj[i] = t; }
       if (threadIdx.x == 0) {
         double t = col2[k]; col2[k] = col2[j]; col2[j] = t;
         t = col2o[k]; col2o[k] = col2o[j]; col2o[j] = t;
-        int ti = piv[k]; piv[k] = piv[j]; piv[j] = ti;
+        const int ti = piv[k]; piv[k] = piv[j]; piv[j] = ti;
       }
       __syncthreads();
     }
@@ -164,11 +146,8 @@ __device__ __noinline__ int rrqr_trunc(Ctx& cx, int m, int n, double* A, int lda
     }
     __syncthreads();
     if (threadIdx.x == 0) { ak[k] = beta; taus[k] = tau; }
-    // reflector v(1:) stays in ak[k+1:] (needed for U); the reference zeroes
-    // R(k+1:, k) which we never read as R.
     __syncthreads();
     rank += 1;
-    // downdate col2, recomputing cancelled norms exactly
     if (k + 1 < n) {
       for (int l = k + 1 + threadIdx.x; l < n; l += NT) {
         const double r = A[k + (long long)l * lda];
@@ -191,36 +170,83 @@ __device__ __noinline__ int rrqr_trunc(Ctx& cx, int m, int n, double* A, int lda
     s = cta_sum(s);
     remaining = rank < n ? fmax(s, 0.0) : 0.0;
   }
-  if (result < 0) { cx.top = mark; return -1; }
-  // U = Q[:, :rank]: back-accumulate reflectors into the identity slab
-  for (long long e = threadIdx.x; e < (long long)m * rank; e += NT) {
-    const int i = (int)(e % m), c = (int)(e / m);
-    U[i + (long long)c * ldu] = (i == c) ? 1.0 : 0.0;
-  }
-  __syncthreads();
-  for (int k = rank - 1; k >= 0; --k) {
+  *remaining2 = remaining;
+  return result < 0 ? -1 : rank;
+}
+
+// Apply the first nref reflectors of a pivoted_qr factorization (vectors
+// below the diagonal of A, taus) to Z (m x nz): Z <- H_0 ... H_{nref-1} Z.
+__device__ __noinline__ void apply_reflectors(int m, int nref, const double* A, int lda, const double* taus, double* Z,
+                                              int ldz, int nz) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = nref - 1; k >= 0; --k) {
     const double tau = taus[k];
     if (tau == 0.0) continue;
-    const double* vk = A + (long long)k * lda;  // v = [1; vk[k+1:]]
-    for (int c = warp; c < rank; c += NWARP) {
-      double* uc = U + (long long)c * ldu;
+    const double* vk = A + (long long)k * lda;
+    for (int c = warp; c < nz; c += NWARP) {
+      double* zc = Z + (long long)c * ldz;
       double d = 0.0;
-      for (int i = k + 1 + lane; i < m; i += 32) d = fma(vk[i], uc[i], d);
-      d = (warp_sum(d) + uc[k]) * tau;
-      if (lane == 0) uc[k] -= d;
-      for (int i = k + 1 + lane; i < m; i += 32) uc[i] = fma(-d, vk[i], uc[i]);
+      for (int i = k + 1 + lane; i < m; i += 32) d = fma(vk[i], zc[i], d);
+      d = (warp_sum(d) + zc[k]) * tau;
+      if (lane == 0) zc[k] -= d;
+      for (int i = k + 1 + lane; i < m; i += 32) zc[i] = fma(-d, vk[i], zc[i]);
     }
     __syncthreads();
   }
-  // V[piv[c], r] = R[r, c] for c in [0,n), r < rank (R upper: zero for c < r)
-  for (long long e = threadIdx.x; e < (long long)n * rank; e += NT) {
-    const int c = (int)(e % n), r = (int)(e / n);
-    const double val = (c >= r) ? A[r + (long long)c * lda] : 0.0;
-    V[piv[c] + (long long)r * ldv] = val;
+}
+
+// ---------------------------------------------------------------------------
+// Truncated column-pivoted QR (lowrank.py:64-135): A (m x n, lda) is
+// overwritten.  Returns the rank (>= 0), or -1 when the rank would exceed
+// max_rank.  On success U (m x rank, ldu) = first rank columns of Q and
+// V (n x rank, ldv) with V[piv, :] = R[:rank, :]^T.
+// ---------------------------------------------------------------------------
+__device__ __noinline__ int rrqr_trunc(Ctx& cx, int m, int n, double* A, int lda, double eps, int max_rank, double* U,
+                                       int ldu, double* V, int ldv) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Mark mk = mark(cx);
+  double* col2 = alloc_fast(cx, n);
+  double* col2o = alloc_fast(cx, n);
+  double* taus = alloc_fast(cx, min(m, n) + 1);
+  int* piv = reinterpret_cast<int*>(alloc_fast(cx, n));
+  if (!col2 || !col2o || !taus || !piv) { release(cx, mk); return -2; }
+  PhaseTimer pt;
+  for (int c = warp; c < n; c += NWARP) {
+    const double* ac = A + (long long)c * lda;
+    double s = 0.0;
+    for (int i = lane; i < m; i += 32) s = fma(ac[i], ac[i], s);
+    s = warp_sum(s);
+    if (lane == 0) { col2[c] = s; col2o[c] = s; piv[c] = c; }
+  }
+  __syncthreads();
+  double fro2;
+  {
+    double s = 0.0;
+    for (int c = threadIdx.x; c < n; c += NT) s += col2[c];
+    fro2 = cta_sum(s);
+  }
+  if (fro2 == 0.0) { release(cx, mk); return 0; }
+  double rem;
+  const int rank = pivoted_qr(m, n, A, lda, (eps * eps) * fro2, max_rank, fro2, col2, col2o, piv, taus, &rem);
+  if (rank < 0) { pt.stop(cx, PH_RRQR); release(cx, mk); return -1; }
+  // U = Q[:, :rank]: reflectors applied to the identity slab
+  for (int c = threadIdx.x >> 5; c < rank; c += NWARP)
+    for (int i = threadIdx.x & 31; i < m; i += 32) {
+    const long long e = (long long)c * m + i;
+    U[i + (long long)c * ldu] = (i == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  apply_reflectors(m, rank, A, lda, taus, U, ldu, rank);
+  // V[piv[c], r] = R[r, c] (R upper: zero for c < r)
+  for (int r = threadIdx.x >> 5; r < rank; r += NWARP)
+    for (int c = threadIdx.x & 31; c < n; c += 32) {
+    const long long e = (long long)r * n + c;
+    V[piv[c] + (long long)r * ldv] = (c >= r) ? A[r + (long long)c * lda] : 0.0;
   }
   __syncthreads();
   add_flops(cx, FK_COMPRESS, rrqr_cost(m, n, rank));
-  cx.top = mark;
+  pt.stop(cx, PH_RRQR);
+  release(cx, mk);
   return rank;
 }
 

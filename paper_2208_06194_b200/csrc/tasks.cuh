@@ -25,6 +25,10 @@ __device__ __forceinline__ Ctx make_ctx(double* ws, long long ws_per_cta, int* s
   c.base = ws + (long long)blockIdx.x * ws_per_cta;
   c.cap = ws_per_cta;
   c.top = 0;
+  extern __shared__ double dyn_smem[];
+  c.sbase = dyn_smem;
+  c.scap = SMEM_ARENA;
+  c.stop = 0;
   c.status = status;
   c.flops = flops;
   return c;
@@ -51,8 +55,9 @@ __device__ void geqrt_inplace(Ctx& cx, int m, int n, double* A, int lda, double*
   if (!tau || !Tp || !S) { cx.top = mark; return; }
   qr_blocked(cx, m, n, A, lda, tau, Tp);
   // Y explicit unit-lower-trapezoidal; zero A below the diagonal
-  for (long long e = threadIdx.x; e < (long long)m * n; e += NT) {
-    const int i = (int)(e % m), j = (int)(e / m);
+  for (int j = threadIdx.x >> 5; j < n; j += NWARP)
+    for (int i = threadIdx.x & 31; i < m; i += 32) {
+    const long long e = (long long)j * m + i;
     double* a = A + i + (long long)j * lda;
     double y;
     if (i < j) y = 0.0;
@@ -90,7 +95,9 @@ __device__ void tiled_diag(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, i
   Cell a = grid_cell(g, k, k);
   if (a.lr) { set_status(cx, ST_BAD_KIND); return; }
   const long long c = (long long)k * g.q + k;
+  PhaseTimer t;
   geqrt_inplace(cx, g.b, g.b, a.u, a.ld, rf.pool + rf.y_off[c], g.b, rf.pool + rf.t_off[c], g.b);
+  t.stop(cx, PH_GEQRT);
 }
 
 __device__ void tiled_block(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, int k, int j) {
@@ -98,12 +105,14 @@ __device__ void tiled_block(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, 
   const double* Y = rf.pool + rf.y_off[c];
   const double* T = rf.pool + rf.t_off[c];
   Cell x = grid_cell(g, k, j);
+  PhaseTimer t;
   if (x.lr) {
     const int r = *x.rank;
     if (r) apply_wy_dev(cx, g.b, g.b, r, Y, g.b, T, g.b, x.u, x.ld, true);
   } else {
     apply_wy_dev(cx, g.b, g.b, g.b, Y, g.b, T, g.b, x.u, x.ld, true);
   }
+  t.stop(cx, PH_APPLYWY);
 }
 
 __device__ void tiled_update(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, int k, int i) {
@@ -113,6 +122,7 @@ __device__ void tiled_update(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf,
   const long long c = (long long)i * g.q + k;
   double* T = rf.pool + rf.t_off[c];
   const long long mark = cx.top;
+  PhaseTimer pt;
   if (x.lr) {
     const int r = *x.rank;
     if (r == 0) {  // tp_qr with an empty bottom: identity reflector (kernels.py:146-147)
@@ -135,6 +145,7 @@ __device__ void tiled_update(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf,
     if (threadIdx.x == 0) rf.yrank[c] = -1;
   }
   __syncthreads();
+  pt.stop(cx, PH_TPQRT);
   cx.top = mark;
 }
 
@@ -144,11 +155,17 @@ __device__ void tiled_trap(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, d
   const double* T = rf.pool + rf.t_off[(long long)i * g.q + k];
   Cell top = grid_cell(g, k, j), bot = grid_cell(g, i, j);
   const Blk tb = cell_blk(top), bb = cell_blk(bot);
+  PhaseTimer t1;
   Blk prod = blk_mul_t(cx, yt, bb);
+  t1.stop(cx, PH_PRODUCT);
   Blk ssum = blk_acc(cx, tb, prod, eps, g.b);
+  PhaseTimer t2;
   Blk w = blk_dense_times(cx, T, g.b, true, ssum);
+  t2.stop(cx, PH_PRODUCT);
   sub_into_cell(cx, top, w, eps);
+  PhaseTimer t3;
   Blk yw = blk_mul(cx, yt, w);
+  t3.stop(cx, PH_PRODUCT);
   sub_into_cell(cx, bot, yw, eps);
   cx.top = mark;
 }

@@ -139,9 +139,10 @@ class DeviceGrid:
 
     @classmethod
     def from_dense(cls, dense, b: int, admissible: np.ndarray, eps: float, fallback: float = 0.5,
-                   cap: int | None = None) -> "DeviceGrid":
+                   cap: int | None = None, colmajor: bool = False) -> "DeviceGrid":
         """GPU dense_to_blr (core.py:227-259).  ``dense`` is a host ndarray or
-        a CUDA tensor (row-major m x n)."""
+        a CUDA tensor (row-major m x n; ``colmajor=True`` if its storage is
+        already column-major, e.g. a symmetric matrix)."""
         rt = _lib.runtime()
         lib = rt.lib
         if isinstance(dense, np.ndarray):
@@ -154,15 +155,15 @@ class DeviceGrid:
         g = cls(m, n, b, adm, cap, min_lr_slab=b * b)
         if g.cap < int(fallback * b):
             raise ValueError("cap must be at least dense_fallback_fraction * b")
-        colmajor = dt.t().contiguous()  # column-major m x n, lda = m
+        cm = dt if colmajor else dt.t().contiguous()  # column-major m x n, lda = m
         ws, per, nct = rt.workspace(b, g.cap)
         st = g.cstruct()
-        _lib.check(lib.blrqr_dense_to_blr(colmajor.data_ptr(), m, C.byref(st), g.kind.data_ptr(), eps,
+        _lib.check(lib.blrqr_dense_to_blr(cm.data_ptr(), m, C.byref(st), g.kind.data_ptr(), eps,
                                           fallback, ws, per, nct, rt.status.data_ptr(), rt.flops.data_ptr(),
                                           _lib.stream_ptr()), "dense_to_blr")
         rt.harvest()
         g.kind_host = g.kind.cpu().numpy().astype(bool).reshape(g.p, g.q)
-        del colmajor
+        del cm
         return g
 
 
