@@ -157,18 +157,24 @@ int blrqr_tiled_run(const blrqr_grid* g, const blrqr_refl* rf, const blrqr_task*
                     const int64_t* level_start_host, int l0, int l1, double eps, double* ws, int64_t ws_per_cta,
                     int nctas, int* status, unsigned long long* flops, void* stream);
 
-/* Blocked Householder (factorize.py:187-292): one panel + its column updates.
- * zbuf: per-column scratch for z_j = T^T s_j: (q * 2 * b * cap) doubles + q ints
- * (zrank). panel_ws: (b + sum_i rows_i) x b panel scratch sized by caller. */
+/* Blocked Householder (factorize.py:187-292), one step k: panel GEQRT of
+ * block column k (triangularize_block_column, :187-229; one CTA), then for
+ * every j > k the ascending-i accumulation chain z_j = T_k^T sum_i Y_ik^T A_ij
+ * (one CTA per j) and the independent updates A_ij -= Y_ik z_j (one CTA per
+ * (i, j)) (apply_block_column_reflector, :232-262).
+ * zbuf: q * 2 * b * b doubles (z_j factors), zrank: q ints.
+ * panel_ws: >= 2 * p * b * b doubles (stacked panel + explicit Y). */
 int blrqr_blocked_step(const blrqr_grid* g, const blrqr_refl* rf, int k, double eps, double* zbuf, int* zrank,
-                       double* ws, int64_t ws_per_cta, int nctas, int* status, unsigned long long* flops,
-                       void* stream);
+                       double* panel_ws, int64_t panel_doubles, double* ws, int64_t ws_per_cta, int nctas,
+                       int* status, unsigned long long* flops, void* stream);
 
-/* Blocked MGS (factorize.py:576-671): step j = panel(j), project(j, k>j),
- * update(j, i, k>j).  qg: explicit Q grid (same kind map as a); rg: R grid (q x q). */
+/* Blocked MGS (factorize.py:576-671), one step j: panel MGS of block column j
+ * into the explicit Q grid qg (same kind map as a) and R_jj (rg, q x q),
+ * projections R_jk (one CTA per k > j, ascending-i chain) and updates
+ * A_ik -= Q_ij R_jk (one CTA per (i, k)).  panel_ws >= p * b * b doubles. */
 int blrqr_mgs_step(const blrqr_grid* a, const blrqr_grid* qg, const blrqr_grid* rg, int j, double eps,
-                   double* ws, int64_t ws_per_cta, int nctas, int* status, unsigned long long* flops,
-                   void* stream);
+                   double* panel_ws, int64_t panel_doubles, double* ws, int64_t ws_per_cta, int nctas, int* status,
+                   unsigned long long* flops, void* stream);
 
 #ifdef __cplusplus
 }

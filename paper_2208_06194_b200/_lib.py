@@ -65,8 +65,9 @@ _SIGS = {
     "blrqr_tiled_task_count": ([_I, _I], _L),
     "blrqr_tiled_schedule": ([_I, _I, _P, _P, _L], _I),
     "blrqr_tiled_run": ([C.POINTER(Grid), C.POINTER(Refl), _P, _P, _I, _I, _D, _P, _L, _I, _P, _P, _P], _I),
-    "blrqr_blocked_step": ([C.POINTER(Grid), C.POINTER(Refl), _I, _D, _P, _P, _P, _L, _I, _P, _P, _P], _I),
-    "blrqr_mgs_step": ([C.POINTER(Grid), C.POINTER(Grid), C.POINTER(Grid), _I, _D, _P, _L, _I, _P, _P, _P], _I),
+    "blrqr_blocked_step": ([C.POINTER(Grid), C.POINTER(Refl), _I, _D, _P, _P, _P, _L, _P, _L, _I, _P, _P, _P], _I),
+    "blrqr_mgs_step": ([C.POINTER(Grid), C.POINTER(Grid), C.POINTER(Grid), _I, _D, _P, _L, _P, _L, _I, _P, _P, _P],
+                       _I),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -295,6 +295,78 @@ __global__ void __launch_bounds__(NT) k_lr_product(int op, int m, int k, int n, 
   }
 }
 
+#include "tasks_blocked_mgs.cuh"
+
+// ---- blocked Householder step kernels ------------------------------------
+__global__ void __launch_bounds__(NT, 1) k_blocked_panel(blrqr_grid g, blrqr_refl rf, int k, double* P, double* Yp,
+                                                         double* ws, long long wsp, int* status,
+                                                         unsigned long long* flops) {
+  Ctx cx = make_ctx(ws, wsp, status, flops);
+  blocked_panel(cx, g, rf, k, P, Yp);
+}
+
+__global__ void __launch_bounds__(NT, 1) k_blocked_chain(blrqr_grid g, blrqr_refl rf, int k, double eps, double* zbuf,
+                                                         int* zrank, double* ws, long long wsp, int* status,
+                                                         unsigned long long* flops) {
+  Ctx cx = make_ctx(ws, wsp, status, flops);
+  const long long bb = (long long)g.b * g.b;
+  for (int j = k + 1 + blockIdx.x; j < g.q; j += gridDim.x) {
+    blocked_chain(cx, g, rf, eps, k, j, zbuf + 2 * bb * j, zbuf + 2 * bb * j + bb, zrank + j);
+    cx.top = 0;
+    cx.stop = 0;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(NT, 1) k_blocked_update(blrqr_grid g, blrqr_refl rf, int k, double eps,
+                                                          double* zbuf, const int* zrank, double* ws, long long wsp,
+                                                          int* status, unsigned long long* flops) {
+  Ctx cx = make_ctx(ws, wsp, status, flops);
+  const long long bb = (long long)g.b * g.b;
+  const int ni = g.p - k, nj = g.q - k - 1;
+  for (int t = blockIdx.x; t < ni * nj; t += gridDim.x) {
+    const int i = k + t % ni, j = k + 1 + t / ni;
+    blocked_update(cx, g, rf, eps, k, i, j, zbuf + 2 * bb * j, zbuf + 2 * bb * j + bb, zrank + j);
+    cx.top = 0;
+    cx.stop = 0;
+    __syncthreads();
+  }
+}
+
+// ---- blocked MGS step kernels ---------------------------------------------
+__global__ void __launch_bounds__(NT, 1) k_mgs_panel_task(blrqr_grid a, blrqr_grid qg, blrqr_grid rg, int j,
+                                                          double* P, double* ws, long long wsp, int* status,
+                                                          unsigned long long* flops) {
+  Ctx cx = make_ctx(ws, wsp, status, flops);
+  mgs_panel_task(cx, a, qg, rg, j, P);
+}
+
+__global__ void __launch_bounds__(NT, 1) k_mgs_project(blrqr_grid a, blrqr_grid qg, blrqr_grid rg, int j, double eps,
+                                                       double* ws, long long wsp, int* status,
+                                                       unsigned long long* flops) {
+  Ctx cx = make_ctx(ws, wsp, status, flops);
+  for (int k = j + 1 + blockIdx.x; k < a.q; k += gridDim.x) {
+    mgs_project(cx, a, qg, rg, eps, j, k);
+    cx.top = 0;
+    cx.stop = 0;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(NT, 1) k_mgs_update(blrqr_grid a, blrqr_grid qg, blrqr_grid rg, int j, double eps,
+                                                      double* ws, long long wsp, int* status,
+                                                      unsigned long long* flops) {
+  Ctx cx = make_ctx(ws, wsp, status, flops);
+  const int nk = a.q - j - 1;
+  for (int t = blockIdx.x; t < nk * a.p; t += gridDim.x) {
+    const int i = t % a.p, k = j + 1 + t / a.p;
+    mgs_update(cx, a, qg, rg, eps, j, i, k);
+    cx.top = 0;
+    cx.stop = 0;
+    __syncthreads();
+  }
+}
+
 // one level (or any contiguous range) of tiled tasks, one CTA per task
 __global__ void __launch_bounds__(NT, 1) k_tiled(const blrqr_task* tasks, long long t0, long long t1, blrqr_grid g,
                                                blrqr_refl rf, double eps, double* ws, long long wsp, int* status,
@@ -362,6 +434,12 @@ static void init_kernels() {
     smem_optin(k_mgs_panel);
     smem_optin(k_lr_product);
     smem_optin(k_tiled);
+    smem_optin(k_blocked_panel);
+    smem_optin(k_blocked_chain);
+    smem_optin(k_blocked_update);
+    smem_optin(k_mgs_panel_task);
+    smem_optin(k_mgs_project);
+    smem_optin(k_mgs_update);
   });
 }
 #define INIT_KERNELS() init_kernels()
@@ -599,14 +677,50 @@ int blrqr_grid_pack(const blrqr_grid* g, double* stage, const int64_t* stage_off
   return 0;
 }
 
-int blrqr_blocked_step(const blrqr_grid*, const blrqr_refl*, int, double, double*, int*, double*, int64_t, int,
-                       int*, unsigned long long*, void*) {
-  return -100;  // implemented below in a later revision
+int blrqr_blocked_step(const blrqr_grid* g, const blrqr_refl* rf, int k, double eps, double* zbuf, int* zrank,
+                       double* panel_ws, int64_t panel_doubles, double* ws, int64_t ws_per_cta, int nctas,
+                       int* status, unsigned long long* flops, void* stream) {
+  if (!g || !rf || k < 0 || k >= g->q) return -1;
+  if (!(eps > 0.0 && eps < 1.0)) return -2;
+  if (panel_doubles < 2LL * g->p * g->b * g->b) return -3;
+  INIT_KERNELS();
+  cudaStream_t st = as_stream(stream);
+  double* P = panel_ws;
+  double* Yp = panel_ws + (int64_t)g->p * g->b * g->b;
+  k_blocked_panel<<<1, NT, SMEM_BYTES, st>>>(*g, *rf, k, P, Yp, ws, ws_per_cta, status, flops);
+  CK(cudaGetLastError());
+  const int nj = g->q - k - 1;
+  if (nj > 0) {
+    k_blocked_chain<<<std::min(nj, nctas), NT, SMEM_BYTES, st>>>(*g, *rf, k, eps, zbuf, zrank, ws, ws_per_cta,
+                                                                 status, flops);
+    CK(cudaGetLastError());
+    const int nt = (g->p - k) * nj;
+    k_blocked_update<<<std::min(nt, nctas), NT, SMEM_BYTES, st>>>(*g, *rf, k, eps, zbuf, zrank, ws, ws_per_cta,
+                                                                  status, flops);
+    CK(cudaGetLastError());
+  }
+  return 0;
 }
 
-int blrqr_mgs_step(const blrqr_grid*, const blrqr_grid*, const blrqr_grid*, int, double, double*, int64_t, int,
-                   int*, unsigned long long*, void*) {
-  return -100;
+int blrqr_mgs_step(const blrqr_grid* a, const blrqr_grid* qg, const blrqr_grid* rg, int j, double eps,
+                   double* panel_ws, int64_t panel_doubles, double* ws, int64_t ws_per_cta, int nctas, int* status,
+                   unsigned long long* flops, void* stream) {
+  if (!a || !qg || !rg || j < 0 || j >= a->q) return -1;
+  if (!(eps > 0.0 && eps < 1.0)) return -2;
+  if (panel_doubles < (int64_t)a->p * a->b * a->b) return -3;
+  INIT_KERNELS();
+  cudaStream_t st = as_stream(stream);
+  k_mgs_panel_task<<<1, NT, SMEM_BYTES, st>>>(*a, *qg, *rg, j, panel_ws, ws, ws_per_cta, status, flops);
+  CK(cudaGetLastError());
+  const int nk = a->q - j - 1;
+  if (nk > 0) {
+    k_mgs_project<<<std::min(nk, nctas), NT, SMEM_BYTES, st>>>(*a, *qg, *rg, j, eps, ws, ws_per_cta, status, flops);
+    CK(cudaGetLastError());
+    k_mgs_update<<<std::min(nk * a->p, nctas), NT, SMEM_BYTES, st>>>(*a, *qg, *rg, j, eps, ws, ws_per_cta, status,
+                                                                     flops);
+    CK(cudaGetLastError());
+  }
+  return 0;
 }
 
 }  // extern "C"

@@ -101,9 +101,20 @@ class DeviceFactorization:
             self.tasks = torch.from_numpy(tasks).to(self.rt.dev)
             self.nlevels = len(self.levels) - 1
         elif method == "blocked-hh":
-            raise NotImplementedError("blocked-hh device driver")
+            g = self.g
+            self.rf = DeviceRefl(self.g)
+            dev = self.rt.dev
+            self.zbuf = torch.empty(g.q * 2 * g.b * g.b, dtype=torch.float64, device=dev)
+            self.zrank = torch.zeros(g.q, dtype=torch.int32, device=dev)
+            self.panel = torch.empty(2 * g.p * g.b * g.b, dtype=torch.float64, device=dev)
         else:
-            raise NotImplementedError("mgs device driver")
+            g = self.g
+            self.qg = DeviceGrid(g.m, g.n, g.b, g.kind_host, g.cap)
+            rl = g.kind_host[: g.q, :].copy()
+            d = np.arange(g.q)
+            rl[d, d] = False
+            self.rg = DeviceGrid(g.n, g.n, g.b, rl, g.cap)
+            self.panel = torch.empty(g.p * g.b * g.b, dtype=torch.float64, device=self.rt.dev)
 
     # -- execution ---------------------------------------------------------
     def run(self, nctas: int | None = None) -> "DeviceFactorization":
@@ -118,6 +129,21 @@ class DeviceFactorization:
                                               self.nlevels, self.cfg.epsilon, ws, per, nct,
                                               rt.status.data_ptr(), rt.flops.data_ptr(), _lib.stream_ptr()),
                        "tiled_run")
+        elif self.method == "blocked-hh":
+            gs, rs = g.cstruct(), self.rf.cstruct()
+            for k in range(g.q):
+                _lib.check(rt.lib.blrqr_blocked_step(C.byref(gs), C.byref(rs), k, self.cfg.epsilon,
+                                                     self.zbuf.data_ptr(), self.zrank.data_ptr(),
+                                                     self.panel.data_ptr(), self.panel.numel(), ws, per, nct,
+                                                     rt.status.data_ptr(), rt.flops.data_ptr(), _lib.stream_ptr()),
+                           "blocked_step")
+        else:
+            gs, qs, rs = g.cstruct(), self.qg.cstruct(), self.rg.cstruct()
+            for j in range(g.q):
+                _lib.check(rt.lib.blrqr_mgs_step(C.byref(gs), C.byref(qs), C.byref(rs), j, self.cfg.epsilon,
+                                                 self.panel.data_ptr(), self.panel.numel(), ws, per, nct,
+                                                 rt.status.data_ptr(), rt.flops.data_ptr(), _lib.stream_ptr()),
+                           "mgs_step")
         return self
 
     def finish(self) -> dict:
@@ -127,13 +153,41 @@ class DeviceFactorization:
 
     # -- results -----------------------------------------------------------
     def r_device(self) -> DeviceGrid:
-        return self.g
+        return self.rg if self.method == "mgs" else self.g
 
     def to_host(self) -> FactorizationResult:
+        if self.method == "mgs":
+            return FactorizationResult("mgs", self.rg.to_host(), q_explicit=self.qg.to_host())
         r = self.g.to_host()
         if self.method == "tiled-hh":
             return FactorizationResult("tiled-hh", r, q_tiles=self._tiles_host())
-        raise NotImplementedError
+        return FactorizationResult("blocked-hh", r, q_columns=self._columns_host())
+
+    def _ytilde(self, i: int, k: int, yr: np.ndarray):
+        """Reflector entry (i, k): LowRankBlock(U_ik, Y_i^T) aliasing the cell's
+        slabs, or the dense Y block (factorize.py:214-224, 404-407)."""
+        g, rf = self.g, self.rf
+        b = g.b
+        c = i * g.q + k
+        if yr[c] >= 0:
+            r = int(yr[c])
+            ou, ov = g.off_u_host[c], g.off_v_host[c]
+            u = g.pool[ou:ou + b * r].cpu().numpy().reshape(r, b).T
+            v = g.pool[ov:ov + b * r].cpu().numpy().reshape(r, b).T
+            return LowRankBlock(np.ascontiguousarray(u), np.ascontiguousarray(v))
+        return rf.mat(rf.y_off_host[c], b, b)
+
+    def _columns_host(self) -> list:
+        g, rf = self.g, self.rf
+        b = g.b
+        yr = rf.yrank.cpu().numpy()
+        cols = []
+        for k in range(g.q):
+            c = k * g.q + k
+            entries = [(k, rf.mat(rf.y_off_host[c], b, b))]
+            entries += [(i, self._ytilde(i, k, yr)) for i in range(k + 1, g.p)]
+            cols.append(ReflectorColumn(k, entries, rf.mat(rf.t_off_host[c], b, b)))
+        return cols
 
     def _tiles_host(self) -> TileReflectorStore:
         g, rf = self.g, self.rf

@@ -61,7 +61,7 @@ def test_compression_parity(pk, tag):
 
 
 @pytest.mark.parametrize("tag", ["rand256", "lap512", "exp512", "inv256", "C1"])
-@pytest.mark.parametrize("method", ["tiled-hh"])
+@pytest.mark.parametrize("method", ["tiled-hh", "blocked-hh", "mgs"])
 def test_factorization_parity(pk, tag, method):
     from paper_2208_06194_b200 import flops as pflops
     from paper_2208_06194_b200.scheduler import execute_sequential
@@ -87,13 +87,37 @@ def test_factorization_parity(pk, tag, method):
     assert abs(pflops.total() - mm["flops_total"]) <= 0.01 * mm["flops_total"]
     # Res / Orth with the oracle's apply-Q on the GPU result's reflectors
     if n <= 2048:
-        st = oalg.TiledState(oblr.Grid(n, n, b, g.lowrank, [[oblr.LR(x.u, x.v) if pk.is_lowrank(x) else x
-                                                            for x in row] for row in res.r.blocks]), eps)
-        st.diag = {k: (w.y, w.t) for k, w in res.q_tiles.diag.items()}
-        st.upd = {key: ((oblr.LR(y.u, y.v) if pk.is_lowrank(y) else y), t) for key, (y, t) in res.q_tiles.updates.items()}
+        st = _oracle_state(pk, res, g, eps)
         resid, orth = oalg.res_orth(dense, st)
         assert resid <= max(10 * mm["res"], 10 * eps)
         assert orth <= max(10 * mm["orth"], 10 * eps)
+
+
+def _ogrid(pk, a):
+    s = a.structure
+    return oblr.Grid(s.m, s.n, s.b, s.admissible,
+                     [[oblr.LR(x.u, x.v) if pk.is_lowrank(x) else x for x in row] for row in a.blocks])
+
+
+def _oblk(pk, y):
+    return oblr.LR(y.u, y.v) if pk.is_lowrank(y) else y
+
+
+def _oracle_state(pk, res, g, eps):
+    """Oracle state objects wrapping the GPU result (for apply-Q / metrics)."""
+    if res.algorithm == "tiled-hh":
+        st = oalg.TiledState(_ogrid(pk, res.r), eps)
+        st.diag = {k: (w.y, w.t) for k, w in res.q_tiles.diag.items()}
+        st.upd = {key: (_oblk(pk, y), t) for key, (y, t) in res.q_tiles.updates.items()}
+        return st
+    if res.algorithm == "blocked-hh":
+        cols = [oalg.ColumnReflector(c.col, [(i, _oblk(pk, y)) for i, y in c.entries], c.t) for c in res.q_columns]
+        return oalg.BlockedState(_ogrid(pk, res.r), eps, cols)
+    st = oalg.MgsState.__new__(oalg.MgsState)
+    st.g, st.eps = g, eps
+    st.qg = _ogrid(pk, res.q_explicit)
+    st.rg = _ogrid(pk, res.r)
+    return st
 
 
 def test_smoke_entry():
