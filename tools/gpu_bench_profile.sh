@@ -1,0 +1,16 @@
+#!/bin/bash
+# Round measurement: bench (plain), launch list under ncu, one full ncu capture
+# of the top k_tiled launch.  Outputs under gpurun_out/.
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+TAG=${TAG:-r01}
+timeout 900 python bench.py > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err
+echo "bench rc=$?"
+CMD="python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-cpu"
+timeout 900 $CMD > gpurun_out/plain_${TAG}.log 2>&1 && \
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv $CMD > gpurun_out/ncu_launch_${TAG}.log 2>&1
+echo "launch list rc=$?"
+CMD2="python tools/probe_config.py C3"
+timeout 600 $CMD2 > gpurun_out/plain2_${TAG}.log 2>&1 && \
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:k_tiled -s 70 -c 1 -o gpurun_out/prof_tiled_${TAG} $CMD2 > gpurun_out/ncu_full_${TAG}.log 2>&1
+echo "ncu full rc=$?"
