@@ -37,6 +37,7 @@ extern "C" {
 #define BLRQR_ST_MGS_COLLAPSE 8   /* RankDeficiencyWarning (kernels.py:214-221) */
 #define BLRQR_ST_BAD_KIND 16      /* e.g. low-rank diagonal block */
 #define BLRQR_ST_BAD_ARG 32
+#define BLRQR_ST_SCHED_TIMEOUT 64 /* dynamic scheduler gave up (no progress within the timeout) */
 
 /* flop-model kinds (flops.add sites): compress, rounded_add, expand, lr_mul,
  * gemm, panel_qr, apply_wy, update_qr, apply_tp */
@@ -156,6 +157,23 @@ int blrqr_tiled_schedule(int p, int q, blrqr_task* tasks_host, int64_t* level_st
 int blrqr_tiled_run(const blrqr_grid* g, const blrqr_refl* rf, const blrqr_task* tasks_dev,
                     const int64_t* level_start_host, int l0, int l1, double eps, double* ws, int64_t ws_per_cta,
                     int nctas, int* status, unsigned long long* flops, void* stream);
+
+/* Dynamic tiled scheduler: the same DAG as explicit successor lists.
+ * blrqr_tiled_dag_size returns the task count (and *nedges); blrqr_tiled_dag
+ * fills tasks (canonical sweep order), initial in-degrees, CSR successors and
+ * a priority flag (1 = DiagQR/UpdateQR).  blrqr_tiled_run_dag runs the whole
+ * factorization with one persistent CTA per SM pulling ready tasks; work_dev
+ * is 3*ntasks + 8 ints of scratch. */
+int64_t blrqr_tiled_dag_size(int p, int q, int64_t* nedges);
+/* Debug: record (start ns, end ns, SM id) per task of subsequent dynamic runs
+ * into a device buffer of 3*ntasks int64 (NULL disables). */
+void blrqr_debug_trace(void* dev_buf);
+int blrqr_tiled_dag(int p, int q, blrqr_task* tasks_host, int* indeg_host, int64_t* succ_off_host,
+                    int* succ_host, int* prio_host);
+int blrqr_tiled_run_dag(const blrqr_grid* g, const blrqr_refl* rf, int ntasks, const blrqr_task* tasks_dev,
+                        const int* indeg0_dev, const int64_t* succ_off_dev, const int* succ_dev,
+                        const int* prio_dev, int* work_dev, double eps, double* ws, int64_t ws_per_cta, int nctas,
+                        double timeout_s, int* status, unsigned long long* flops, void* stream);
 
 /* Blocked Householder (factorize.py:187-292), one step k: panel GEQRT of
  * block column k (triangularize_block_column, :187-229; one CTA), then for

@@ -23,6 +23,7 @@ PHASES = ("norm", "qr", "core", "svd", "back", "product", "tpqrt", "geqrt", "app
           "qrcp", "jacobi_sweeps", "jacobi_calls")
 ST_RANK_OVERFLOW, ST_ARENA_OVERFLOW, ST_NONFINITE, ST_MGS_COLLAPSE, ST_BAD_KIND, ST_BAD_ARG = (
     1, 2, 4, 8, 16, 32)
+ST_SCHED_TIMEOUT = 64
 
 _lib = None
 _lock = threading.Lock()
@@ -65,6 +66,11 @@ _SIGS = {
     "blrqr_tiled_task_count": ([_I, _I], _L),
     "blrqr_tiled_schedule": ([_I, _I, _P, _P, _L], _I),
     "blrqr_tiled_run": ([C.POINTER(Grid), C.POINTER(Refl), _P, _P, _I, _I, _D, _P, _L, _I, _P, _P, _P], _I),
+    "blrqr_tiled_dag_size": ([_I, _I, _P], _L),
+    "blrqr_debug_trace": ([_P], None),
+    "blrqr_tiled_dag": ([_I, _I, _P, _P, _P, _P, _P], _I),
+    "blrqr_tiled_run_dag": ([C.POINTER(Grid), C.POINTER(Refl), _I, _P, _P, _P, _P, _P, _P, _D, _P, _L, _I, _D, _P,
+                             _P, _P], _I),
     "blrqr_blocked_step": ([C.POINTER(Grid), C.POINTER(Refl), _I, _D, _P, _P, _P, _L, _P, _L, _I, _P, _P, _P], _I),
     "blrqr_mgs_step": ([C.POINTER(Grid), C.POINTER(Grid), C.POINTER(Grid), _I, _D, _P, _L, _P, _L, _I, _P, _P, _P],
                        _I),
@@ -157,6 +163,8 @@ class Runtime:
             raise RuntimeError("per-CTA workspace overflow (blrqr_workspace_doubles too small)")
         if st & ST_RANK_OVERFLOW:
             raise RuntimeError("a low-rank result exceeded the slab capacity (raise cap)")
+        if st & ST_SCHED_TIMEOUT:
+            raise RuntimeError("dynamic scheduler timed out (no ready task); results are invalid")
         if st & ST_BAD_KIND:
             raise ValueError("diagonal blocks must be dense")
         if st & ST_MGS_COLLAPSE and warn_mgs:

@@ -159,7 +159,10 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
     X[piv[j] + (long long)a * k] = j >= a ? G[a + (long long)j * k] : 0.0;
   }
   __syncthreads();
-  jacobi_cols(k, kp, X, k, J, kp, sig, perm, cx.flops);
+  if (in_smem(cx, X) && in_smem(cx, J))
+    jacobi_smem(cx, k, kp, X, J, sig, perm, cx.flops);  // shared-space loads, 2 pairs per warp
+  else
+    jacobi_cols(k, kp, X, k, J, kp, sig, perm, cx.flops);
   ts.stop(cx, PH_SVD);
   // (4) truncation (lowrank.py:204-213); the dropped QRCP remainder rem2
   // (<= (eps_mach ||core||)^2) is counted in the total and in every tail

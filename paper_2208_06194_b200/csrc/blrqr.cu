@@ -367,6 +367,114 @@ __global__ void __launch_bounds__(NT, 1) k_mgs_update(blrqr_grid a, blrqr_grid q
   }
 }
 
+// ---- dynamic (dependency-counter) tiled scheduler ---------------------------
+// Persistent kernel, one CTA per SM.  Ready tasks sit in two FIFO rings
+// (high priority: DiagQR / UpdateQR, the critical chains; low: the
+// applications), each task enters exactly once.  A finished task releases
+// its successors by decrementing their in-degree (scheduler.py:335-416
+// semantics without level barriers).  Memory ordering follows the grid-sync
+// pattern: producer __threadfence before publishing, consumer thread 0
+// acquires then __threadfence + __syncthreads before the CTA reads.
+struct DagDev {
+  int n;
+  const blrqr_task* tasks;
+  const long long* succ_off;
+  const int* succ;
+  const int* prio;
+  int* indeg;
+  int* q[2];
+  int* ctr;  // [0] head hi, [1] tail hi, [2] head lo, [3] tail lo, [4] done
+  long long* trace;  // optional: per task (start ns, end ns, sm id)
+};
+
+__device__ __forceinline__ long long global_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ int ld_volatile(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+
+__device__ __forceinline__ void dag_push(const DagDev& d, int t) {
+  const int c = d.prio[t] ? 0 : 1;
+  const int slot = atomicAdd(d.ctr + 2 * c + 1, 1);
+  atomicExch(d.q[c] + slot, t);
+}
+
+__global__ void __launch_bounds__(NT, 1) k_tiled_dag(DagDev d, blrqr_grid g, blrqr_refl rf, double eps, double* ws,
+                                                     long long wsp, int* status, unsigned long long* flops,
+                                                     long long timeout_cycles) {
+  Ctx cx = make_ctx(ws, wsp, status, flops);
+  __shared__ int s_task;
+  while (true) {
+    if (threadIdx.x == 0) {
+      int t = -1;
+      const long long t0 = sm_clock();
+      while (true) {
+        bool got = false;
+        for (int c = 0; c < 2 && !got; ++c) {
+          const int h = ld_volatile(d.ctr + 2 * c);
+          const int tl = ld_volatile(d.ctr + 2 * c + 1);
+          if (h < tl && atomicCAS(d.ctr + 2 * c, h, h + 1) == h) {
+            int v;
+            while ((v = ld_volatile(d.q[c] + h)) < 0) __nanosleep(32);
+            t = v;
+            got = true;
+          }
+        }
+        if (got) break;
+        if (ld_volatile(d.ctr + 4) >= d.n) break;
+        if (sm_clock() - t0 > timeout_cycles) {
+          atomicOr(status, ST_SCHED_TIMEOUT);
+          atomicExch(d.ctr + 4, d.n);  // release everyone
+          break;
+        }
+        __nanosleep(64);
+      }
+      __threadfence();
+      s_task = t;
+    }
+    __syncthreads();
+    const int t = s_task;
+    if (t < 0) break;
+    __threadfence();
+    const blrqr_task tk = d.tasks[t];
+    if (d.trace && threadIdx.x == 0) d.trace[3 * (long long)t] = global_ns();
+    PhaseTimer tt;
+    switch (tk.kind) {
+      case 0: tiled_diag(cx, g, rf, tk.k); break;
+      case 1: tiled_block(cx, g, rf, tk.k, tk.j); break;
+      case 2: tiled_update(cx, g, rf, tk.k, tk.i); break;
+      default: tiled_trap(cx, g, rf, eps, tk.k, tk.i, tk.j); break;
+    }
+    tt.stop(cx, PH_TASK);
+    cx.top = 0;
+    cx.stop = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (d.trace) {
+        d.trace[3 * (long long)t + 1] = global_ns();
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        d.trace[3 * (long long)t + 2] = smid;
+      }
+      __threadfence();
+      for (long long e = d.succ_off[t]; e < d.succ_off[t + 1]; ++e) {
+        const int s2 = d.succ[e];
+        if (atomicSub(d.indeg + s2, 1) == 1) dag_push(d, s2);
+      }
+      atomicAdd(d.ctr + 4, 1);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_dag_init(DagDev d) {
+  // tasks with no predecessor start ready (only DiagQR(0) for a tiled DAG)
+  for (int t = threadIdx.x; t < d.n; t += blockDim.x)
+    if (d.indeg[t] == 0) dag_push(d, t);
+}
+
 // one level (or any contiguous range) of tiled tasks, one CTA per task
 __global__ void __launch_bounds__(NT, 1) k_tiled(const blrqr_task* tasks, long long t0, long long t1, blrqr_grid g,
                                                blrqr_refl rf, double eps, double* ws, long long wsp, int* status,
@@ -374,12 +482,14 @@ __global__ void __launch_bounds__(NT, 1) k_tiled(const blrqr_task* tasks, long l
   Ctx cx = make_ctx(ws, wsp, status, flops);
   for (long long t = t0 + blockIdx.x; t < t1; t += gridDim.x) {
     const blrqr_task tk = tasks[t];
+    PhaseTimer tt;
     switch (tk.kind) {
       case 0: tiled_diag(cx, g, rf, tk.k); break;
       case 1: tiled_block(cx, g, rf, tk.k, tk.j); break;
       case 2: tiled_update(cx, g, rf, tk.k, tk.i); break;
       default: tiled_trap(cx, g, rf, eps, tk.k, tk.i, tk.j); break;
     }
+    tt.stop(cx, PH_TASK);
     cx.top = 0;
     cx.stop = 0;
     __syncthreads();
@@ -434,6 +544,7 @@ static void init_kernels() {
     smem_optin(k_mgs_panel);
     smem_optin(k_lr_product);
     smem_optin(k_tiled);
+    smem_optin(k_tiled_dag);
     smem_optin(k_blocked_panel);
     smem_optin(k_blocked_chain);
     smem_optin(k_blocked_update);
@@ -651,6 +762,122 @@ int blrqr_tiled_schedule(int p, int q, blrqr_task* tasks_host, int64_t* level_st
   }
   level_start_host[nlev] = (int64_t)tasks.size();
   return nlev;
+}
+
+// canonical-order task list + successor CSR of the tiled DAG
+// (scheduler.py:173-201 edges: last writer -> any touch, readers -> writer)
+static void tiled_dag_host(int p, int q, std::vector<blrqr_task>& tasks, std::vector<int>& indeg,
+                           std::vector<int64_t>& off, std::vector<int>& succ) {
+  tasks.clear();
+  for (int k = 0; k < q; ++k) {
+    tasks.push_back({0, k, -1, -1});
+    for (int j = k + 1; j < q; ++j) tasks.push_back({1, k, -1, j});
+    for (int i = k + 1; i < p; ++i) {
+      tasks.push_back({2, k, i, -1});
+      for (int j = k + 1; j < q; ++j) tasks.push_back({3, k, i, j});
+    }
+  }
+  const int n = (int)tasks.size();
+  std::vector<std::vector<int>> out(n);
+  std::unordered_map<int64_t, int> writer;
+  std::unordered_map<int64_t, std::vector<int>> readers;
+  std::vector<int64_t> rd, wr;
+  for (int t = 0; t < n; ++t) {
+    tiled_access(tasks[t], rd, wr);
+    std::vector<int> preds;
+    auto touch = [&](int64_t c) {
+      auto it = writer.find(c);
+      if (it != writer.end() && it->second != t) preds.push_back(it->second);
+    };
+    for (auto c : rd) touch(c);
+    for (auto c : wr) {
+      touch(c);
+      auto it = readers.find(c);
+      if (it != readers.end())
+        for (int r : it->second)
+          if (r != t) preds.push_back(r);
+    }
+    std::sort(preds.begin(), preds.end());
+    preds.erase(std::unique(preds.begin(), preds.end()), preds.end());
+    for (int u : preds) out[u].push_back(t);
+    for (auto c : wr) {
+      writer[c] = t;
+      readers[c].clear();
+    }
+    for (auto c : rd)
+      if (std::find(wr.begin(), wr.end(), c) == wr.end()) readers[c].push_back(t);
+  }
+  indeg.assign(n, 0);
+  off.assign(n + 1, 0);
+  succ.clear();
+  for (int t = 0; t < n; ++t) {
+    off[t + 1] = off[t] + (int64_t)out[t].size();
+    for (int v : out[t]) {
+      succ.push_back(v);
+      indeg[v] += 1;
+    }
+  }
+}
+
+static long long* g_dag_trace = nullptr;
+void blrqr_debug_trace(void* dev_buf) { g_dag_trace = reinterpret_cast<long long*>(dev_buf); }
+
+int64_t blrqr_tiled_dag_size(int p, int q, int64_t* nedges) {
+  if (q < 1 || p < q) return -1;
+  std::vector<blrqr_task> tasks;
+  std::vector<int> indeg, succ;
+  std::vector<int64_t> off;
+  tiled_dag_host(p, q, tasks, indeg, off, succ);
+  if (nedges) *nedges = (int64_t)succ.size();
+  return (int64_t)tasks.size();
+}
+
+int blrqr_tiled_dag(int p, int q, blrqr_task* tasks_host, int* indeg_host, int64_t* succ_off_host,
+                    int* succ_host, int* prio_host) {
+  if (q < 1 || p < q) return -1;
+  std::vector<blrqr_task> tasks;
+  std::vector<int> indeg, succ;
+  std::vector<int64_t> off;
+  tiled_dag_host(p, q, tasks, indeg, off, succ);
+  std::copy(tasks.begin(), tasks.end(), tasks_host);
+  std::copy(indeg.begin(), indeg.end(), indeg_host);
+  std::copy(off.begin(), off.end(), succ_off_host);
+  std::copy(succ.begin(), succ.end(), succ_host);
+  for (size_t t = 0; t < tasks.size(); ++t) prio_host[t] = (tasks[t].kind == 0 || tasks[t].kind == 2) ? 1 : 0;
+  return 0;
+}
+
+int blrqr_tiled_run_dag(const blrqr_grid* g, const blrqr_refl* rf, int ntasks, const blrqr_task* tasks_dev,
+                        const int* indeg0_dev, const int64_t* succ_off_dev, const int* succ_dev,
+                        const int* prio_dev, int* work_dev, double eps, double* ws, int64_t ws_per_cta, int nctas,
+                        double timeout_s, int* status, unsigned long long* flops, void* stream) {
+  if (!g || !rf || ntasks <= 0) return -1;
+  if (!(eps > 0.0 && eps < 1.0)) return -2;
+  INIT_KERNELS();
+  cudaStream_t st = as_stream(stream);
+  DagDev d;
+  d.n = ntasks;
+  d.tasks = tasks_dev;
+  d.succ_off = (const long long*)succ_off_dev;
+  d.succ = succ_dev;
+  d.prio = prio_dev;
+  d.indeg = work_dev;
+  d.q[0] = work_dev + ntasks;
+  d.q[1] = work_dev + 2 * (int64_t)ntasks;
+  d.ctr = work_dev + 3 * (int64_t)ntasks;
+  d.trace = g_dag_trace;
+  CK(cudaMemcpyAsync(d.indeg, indeg0_dev, sizeof(int) * ntasks, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemsetAsync(d.q[0], 0xFF, sizeof(int) * 2 * (size_t)ntasks, st));
+  CK(cudaMemsetAsync(d.ctr, 0, sizeof(int) * 8, st));
+  k_dag_init<<<1, 256, 0, st>>>(d);
+  CK(cudaGetLastError());
+  int dev = 0, clk_khz = 1965000;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev);
+  const long long timeout_cycles = (long long)(timeout_s * clk_khz * 1e3);
+  k_tiled_dag<<<nctas, NT, SMEM_BYTES, st>>>(d, *g, *rf, eps, ws, ws_per_cta, status, flops, timeout_cycles);
+  CK(cudaGetLastError());
+  return 0;
 }
 
 int blrqr_tiled_run(const blrqr_grid* g, const blrqr_refl* rf, const blrqr_task* tasks_dev,

@@ -21,6 +21,7 @@ constexpr int ST_NONFINITE = 4;
 constexpr int ST_MGS_COLLAPSE = 8;
 constexpr int ST_BAD_KIND = 16;
 constexpr int ST_BAD_ARG = 32;
+constexpr int ST_SCHED_TIMEOUT = 64;
 
 // model-flop categories (flops.py kinds)
 enum FlopKind : int {
@@ -41,6 +42,10 @@ struct Ctx {
 // dynamic shared-memory arena per CTA (doubles): one 512-thread CTA per SM
 // owns ~180 KB next to the static GEMM scratch (see GEMM_SMEM)
 constexpr int SMEM_ARENA = 23040;  // 180 KB
+
+// the dynamic shared-memory arena (declared once; pointers derived from it
+// compile to LDS/STS instead of generic loads)
+extern __shared__ double dyn_smem[];
 
 struct Mark {
   long long g;
@@ -100,6 +105,11 @@ __device__ __forceinline__ double* salloc(Ctx& c, long long n) {
   c.stop += (int)n;
   return p;
 }
+
+// Re-derive an arena pointer from dyn_smem so the compiler emits shared-space
+// loads/stores (only valid for pointers returned by salloc).
+__device__ __forceinline__ double* as_smem(const Ctx& c, const double* p) { return dyn_smem + (p - c.sbase); }
+__device__ __forceinline__ bool in_smem(const Ctx& c, const double* p) { return p >= c.sbase && p < c.sbase + c.scap; }
 
 // Shared memory when it fits, else the global arena.
 __device__ __forceinline__ double* alloc_fast(Ctx& c, long long n) {

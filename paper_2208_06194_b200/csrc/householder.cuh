@@ -37,7 +37,7 @@ __device__ void house_gen(double alpha, double* X, int n, long long incx, double
 // Unblocked QR of the panel A(r0:m, c0:c0+w) applied also to columns up to
 // c0+w (only panel columns).  Reflectors stored below the diagonal, tau[c].
 // ---------------------------------------------------------------------------
-__device__ __noinline__ void qr_panel_unblocked(int m, int c0, int w, double* A, int lda, double* tau) {
+__device__ __forceinline__ void qr_panel_unblocked(int m, int c0, int w, double* A, int lda, double* tau) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int jj = 0; jj < w; ++jj) {
     const int j = c0 + jj;  // diagonal (j, j)
@@ -154,7 +154,7 @@ __device__ __noinline__ void qr_blocked(Ctx& cx, int m, int n, double* A, int ld
     double* Y;
     if (P) {
       copy_mat(h, w, A + c0 + (long long)c0 * lda, lda, P, h);
-      qr_panel_unblocked(h, 0, w, P, h, tau + c0);
+      qr_panel_unblocked(h, 0, w, as_smem(cx, P), h, tau + c0);  // shared-space loads
       copy_mat(h, w, P, h, A + c0 + (long long)c0 * lda, lda);
       // P becomes the explicit unit-lower-trapezoidal Y in place
       for (int jj = threadIdx.x >> 5; jj < w; jj += NWARP)

@@ -25,6 +25,7 @@ __device__ __noinline__ void jacobi_cols(int rows, int ncols, double* X, int ldx
   }
   __syncthreads();
   const double tol = 2.220446049250313e-16 * (double)max(rows, 1);
+  const double tol2 = tol * tol;
   const int kk = (ncols + 1) & ~1;  // even number of players (one dummy when odd)
   const int npairs = kk / 2;
   for (int sweep = 0; sweep < 40 && ncols > 1; ++sweep) {
@@ -32,8 +33,12 @@ __device__ __noinline__ void jacobi_cols(int rows, int ncols, double* X, int ldx
     __syncthreads();
     for (int rnd = 0; rnd < kk - 1; ++rnd) {
       for (int pi = warp; pi < npairs; pi += NWARP) {
-        int p = pi == 0 ? 0 : 1 + (pi - 1 + rnd) % (kk - 1);
-        int q = 1 + (kk - 2 - pi + rnd) % (kk - 1);
+        int p = pi - 1 + rnd;
+        if (p >= kk - 1) p -= kk - 1;
+        p = pi == 0 ? 0 : 1 + p;
+        int q = kk - 2 - pi + rnd;
+        if (q >= kk - 1) q -= kk - 1;
+        q += 1;
         if (p >= ncols || q >= ncols) continue;
         if (p > q) { const int t = p; p = q; q = t; }
         double* gp = X + (long long)p * ldx;
@@ -49,7 +54,7 @@ __device__ __noinline__ void jacobi_cols(int rows, int ncols, double* X, int ldx
         b = warp_sum(b);
         g = warp_sum(g);
         if (g == 0.0 || a == 0.0 || b == 0.0) continue;
-        if (fabs(g) <= tol * sqrt(a) * sqrt(b)) continue;
+        if (g * g <= tol2 * a * b) continue;
         const double zeta = (b - a) / (2.0 * g);
         const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
         const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
@@ -75,6 +80,279 @@ __device__ __noinline__ void jacobi_cols(int rows, int ncols, double* X, int ldx
     if (!rot) break;
   }
   if (prof && threadIdx.x == 0) atomicAdd(prof + PROF_BASE + PH_JCALLS, 1ull);
+  for (int c = warp; c < ncols; c += NWARP) {
+    const double* gc = X + (long long)c * ldx;
+    double a = 0.0;
+    for (int i = lane; i < rows; i += 32) a = fma(gc[i], gc[i], a);
+    a = warp_sum(a);
+    if (lane == 0) sigma[c] = sqrt(a);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < ncols; i += NT) {
+    const double si = sigma[i];
+    int r = 0;
+    for (int j = 0; j < ncols; ++j) {
+      const double sj = sigma[j];
+      r += (sj > si) || (sj == si && j < i);
+    }
+    perm[r] = i;
+  }
+  __syncthreads();
+}
+
+// Jacobi rotation of one column pair (p, q): returns true if rotated.
+__device__ __forceinline__ void jac_dots(const double* gp, const double* gq, int rows, int lane, double& a, double& b,
+                                         double& g) {
+  a = 0.0; b = 0.0; g = 0.0;
+  for (int i = lane; i < rows; i += 32) {
+    const double x = gp[i], y = gq[i];
+    a = fma(x, x, a);
+    b = fma(y, y, b);
+    g = fma(x, y, g);
+  }
+}
+__device__ __forceinline__ bool jac_angle(double a, double b, double g, double tol2, double& c, double& s) {
+  if (g == 0.0 || a == 0.0 || b == 0.0) return false;
+  if (g * g <= tol2 * a * b) return false;
+  const double zeta = (b - a) / (2.0 * g);
+  const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+  c = 1.0 / sqrt(1.0 + t * t);
+  s = c * t;
+  return true;
+}
+__device__ __forceinline__ void jac_rotate(double* xp, double* xq, int n, int lane, double c, double s) {
+  for (int i = lane; i < n; i += 32) {
+    const double x = xp[i], y = xq[i];
+    xp[i] = c * x - s * y;
+    xq[i] = s * x + c * y;
+  }
+}
+__device__ __forceinline__ void rr_pair(int pi, int rnd, int kk, int& p, int& q) {
+  int a = pi - 1 + rnd;
+  if (a >= kk - 1) a -= kk - 1;
+  p = pi == 0 ? 0 : 1 + a;
+  int b = kk - 2 - pi + rnd;
+  if (b >= kk - 1) b -= kk - 1;
+  q = 1 + b;
+  if (p > q) { const int t = p; p = q; q = t; }
+}
+
+// Shared-memory one-sided Jacobi: X (rows x ncols, ld rows) and J (ncols x
+// ncols) live in the CTA's shared arena (xs, js were returned by salloc).
+// Each warp works on two column pairs at once to overlap the dependent
+// reduction / sqrt / division latency.
+__device__ __noinline__ void jacobi_smem(const Ctx& cx, int rows, int ncols, double* xs_, double* js_, double* sigma,
+                                         int* perm, unsigned long long* prof = nullptr) {
+  __shared__ int s_rot;
+  double* X = as_smem(cx, xs_);
+  double* J = as_smem(cx, js_);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int j = warp; j < ncols; j += NWARP)
+    for (int i = lane; i < ncols; i += 32) J[i + j * ncols] = (i == j) ? 1.0 : 0.0;
+  __syncthreads();
+  const double tol = 2.220446049250313e-16 * (double)max(rows, 1);
+  const double tol2 = tol * tol;
+  const int kk = (ncols + 1) & ~1;
+  const int npairs = kk / 2;
+  for (int sweep = 0; sweep < 40 && ncols > 1; ++sweep) {
+    if (threadIdx.x == 0) s_rot = 0;
+    __syncthreads();
+    for (int rnd = 0; rnd < kk - 1; ++rnd) {
+      for (int pi = warp; pi < npairs; pi += 2 * NWARP) {
+        const int pi2 = pi + NWARP;
+        int p0, q0, p1 = 0, q1 = 0;
+        rr_pair(pi, rnd, kk, p0, q0);
+        const bool v0 = p0 < ncols && q0 < ncols;
+        bool v1 = pi2 < npairs;
+        if (v1) {
+          rr_pair(pi2, rnd, kk, p1, q1);
+          v1 = p1 < ncols && q1 < ncols;
+        }
+        double a0 = 0, b0 = 0, g0 = 0, a1 = 0, b1 = 0, g1 = 0;
+        if (v0) jac_dots(X + p0 * rows, X + q0 * rows, rows, lane, a0, b0, g0);
+        if (v1) jac_dots(X + p1 * rows, X + q1 * rows, rows, lane, a1, b1, g1);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+          b0 += __shfl_xor_sync(0xffffffffu, b0, o);
+          g0 += __shfl_xor_sync(0xffffffffu, g0, o);
+          a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+          b1 += __shfl_xor_sync(0xffffffffu, b1, o);
+          g1 += __shfl_xor_sync(0xffffffffu, g1, o);
+        }
+        double c0, s0, c1, s1;
+        const bool r0 = v0 && jac_angle(a0, b0, g0, tol2, c0, s0);
+        const bool r1 = v1 && jac_angle(a1, b1, g1, tol2, c1, s1);
+        if (r0) {
+          jac_rotate(X + p0 * rows, X + q0 * rows, rows, lane, c0, s0);
+          jac_rotate(J + p0 * ncols, J + q0 * ncols, ncols, lane, c0, s0);
+        }
+        if (r1) {
+          jac_rotate(X + p1 * rows, X + q1 * rows, rows, lane, c1, s1);
+          jac_rotate(J + p1 * ncols, J + q1 * ncols, ncols, lane, c1, s1);
+        }
+        if ((r0 || r1) && lane == 0) s_rot = 1;
+      }
+      __syncthreads();
+    }
+    const int rot = s_rot;
+    __syncthreads();
+    if (prof && threadIdx.x == 0) atomicAdd(prof + PROF_BASE + PH_JSWEEPS, 1ull);
+    if (!rot) break;
+  }
+  if (prof && threadIdx.x == 0) atomicAdd(prof + PROF_BASE + PH_JCALLS, 1ull);
+  for (int c = warp; c < ncols; c += NWARP) {
+    const double* gc = X + c * rows;
+    double a = 0.0;
+    for (int i = lane; i < rows; i += 32) a = fma(gc[i], gc[i], a);
+    a = warp_sum(a);
+    if (lane == 0) sigma[c] = sqrt(a);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < ncols; i += NT) {
+    const double si = sigma[i];
+    int r = 0;
+    for (int j = 0; j < ncols; ++j) {
+      const double sj = sigma[j];
+      r += (sj > si) || (sj == si && j < i);
+    }
+    perm[r] = i;
+  }
+  __syncthreads();
+}
+
+// Blocked one-sided Jacobi for column sets that do not fit in shared memory:
+// columns are grouped in blocks of JB; each outer round pairs blocks
+// (round-robin), two warp groups each stage one block pair (X and J columns)
+// in shared memory and run a full inner sweep over its 2*JB columns there,
+// then write back.  Same rotations and stopping rule as jacobi_cols (every
+// column pair is visited each outer sweep), far less L2 latency per pair.
+constexpr int JB = 8;
+__device__ __noinline__ void jacobi_cols_blocked(Ctx& cx, int rows, int ncols, double* X, int ldx, double* J,
+                                                 int ldj, double* sigma, int* perm,
+                                                 unsigned long long* prof = nullptr) {
+  __shared__ int s_rot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int j = warp; j < ncols; j += NWARP)
+    for (int i = lane; i < ncols; i += 32) J[i + (long long)j * ldj] = (i == j) ? 1.0 : 0.0;
+  __syncthreads();
+  const Mark mk = mark(cx);
+  const int per_group = 2 * JB * (rows + ncols);
+  int groups = 2;
+  double* stage = salloc(cx, (long long)groups * per_group);
+  if (!stage) {
+    groups = 1;
+    stage = salloc(cx, per_group);
+  }
+  if (!stage) stage = alloc(cx, (long long)per_group);  // last resort: L2-resident staging
+  if (!stage) { release(cx, mk); return; }
+  if (in_smem(cx, stage)) stage = as_smem(cx, stage);
+  const int gw = NWARP / groups, gt = gw * 32;
+  const int grp = warp / gw, wg = warp % gw;
+  const int tid_g = threadIdx.x - grp * gt;
+  double* Xs = stage + (long long)grp * per_group;
+  double* Js = Xs + 2 * JB * rows;
+  auto gsync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(gt)); };
+  const double tol = 2.220446049250313e-16 * (double)max(rows, 1);
+  const double tol2 = tol * tol;
+  const int nb = (ncols + JB - 1) / JB;
+  const int nbe = (nb + 1) & ~1;
+  for (int sweep = 0; sweep < 40 && ncols > 1; ++sweep) {
+    if (threadIdx.x == 0) s_rot = 0;
+    __syncthreads();
+    for (int rnd = 0; rnd < max(nbe - 1, 1); ++rnd) {
+      for (int bp = grp; bp < max(nbe / 2, 1); bp += groups) {
+        int bi, bj;
+        if (nbe == 1 || nb == 1) {
+          bi = 0; bj = 0;
+        } else {
+          int p = bp - 1 + rnd;
+          if (p >= nbe - 1) p -= nbe - 1;
+          bi = bp == 0 ? 0 : 1 + p;
+          int q = nbe - 2 - bp + rnd;
+          if (q >= nbe - 1) q -= nbe - 1;
+          bj = 1 + q;
+        }
+        if (bi >= nb || bj >= nb) continue;  // uniform within the group
+        // local columns: block bi (first JB slots) then block bj (unless same)
+        int cols[2 * JB];
+        int nc = 0;
+        for (int c = 0; c < JB; ++c)
+          if (bi * JB + c < ncols) cols[nc++] = bi * JB + c;
+        if (bj != bi)
+          for (int c = 0; c < JB; ++c)
+            if (bj * JB + c < ncols) cols[nc++] = bj * JB + c;
+        // stage in
+        for (int c = tid_g >> 5; c < nc; c += gw) {
+          const double* xs = X + (long long)cols[c] * ldx;
+          const double* js = J + (long long)cols[c] * ldj;
+          for (int i = lane; i < rows; i += 32) Xs[i + c * rows] = xs[i];
+          for (int i = lane; i < ncols; i += 32) Js[i + c * ncols] = js[i];
+        }
+        gsync();
+        // inner round-robin sweep over nc local columns
+        const int kk = (nc + 1) & ~1;
+        for (int r2 = 0; r2 < kk - 1; ++r2) {
+          for (int pi = wg; pi < kk / 2; pi += gw) {
+            int p = pi - 1 + r2;
+            if (p >= kk - 1) p -= kk - 1;
+            p = pi == 0 ? 0 : 1 + p;
+            int q = kk - 2 - pi + r2;
+            if (q >= kk - 1) q -= kk - 1;
+            q += 1;
+            if (p >= nc || q >= nc) continue;
+            if (p > q) { const int t = p; p = q; q = t; }
+            double* gp = Xs + p * rows;
+            double* gq = Xs + q * rows;
+            double a = 0.0, b = 0.0, g = 0.0;
+            for (int i = lane; i < rows; i += 32) {
+              const double x = gp[i], y = gq[i];
+              a = fma(x, x, a);
+              b = fma(y, y, b);
+              g = fma(x, y, g);
+            }
+            a = warp_sum(a);
+            b = warp_sum(b);
+            g = warp_sum(g);
+            if (g == 0.0 || a == 0.0 || b == 0.0) continue;
+            if (g * g <= tol2 * a * b) continue;
+            const double zeta = (b - a) / (2.0 * g);
+            const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+            const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+            for (int i = lane; i < rows; i += 32) {
+              const double x = gp[i], y = gq[i];
+              gp[i] = c * x - s * y;
+              gq[i] = s * x + c * y;
+            }
+            double* jp = Js + p * ncols;
+            double* jq = Js + q * ncols;
+            for (int i = lane; i < ncols; i += 32) {
+              const double x = jp[i], y = jq[i];
+              jp[i] = c * x - s * y;
+              jq[i] = s * x + c * y;
+            }
+            if (lane == 0) s_rot = 1;
+          }
+          gsync();
+        }
+        // stage out
+        for (int c = tid_g >> 5; c < nc; c += gw) {
+          double* xs = X + (long long)cols[c] * ldx;
+          double* js = J + (long long)cols[c] * ldj;
+          for (int i = lane; i < rows; i += 32) xs[i] = Xs[i + c * rows];
+          for (int i = lane; i < ncols; i += 32) js[i] = Js[i + c * ncols];
+        }
+        gsync();
+      }
+      __syncthreads();
+    }
+    const int rot = s_rot;
+    __syncthreads();
+    if (prof && threadIdx.x == 0) atomicAdd(prof + PROF_BASE + PH_JSWEEPS, 1ull);
+    if (!rot) break;
+  }
+  if (prof && threadIdx.x == 0) atomicAdd(prof + PROF_BASE + PH_JCALLS, 1ull);
+  release(cx, mk);
   for (int c = warp; c < ncols; c += NWARP) {
     const double* gc = X + (long long)c * ldx;
     double a = 0.0;

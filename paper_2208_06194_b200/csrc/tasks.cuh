@@ -25,7 +25,6 @@ __device__ __forceinline__ Ctx make_ctx(double* ws, long long ws_per_cta, int* s
   c.base = ws + (long long)blockIdx.x * ws_per_cta;
   c.cap = ws_per_cta;
   c.top = 0;
-  extern __shared__ double dyn_smem[];
   c.sbase = dyn_smem;
   c.scap = SMEM_ARENA;
   c.stop = 0;

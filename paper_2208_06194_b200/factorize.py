@@ -32,6 +32,7 @@ __all__ = ["ReflectorColumn", "TileReflectorStore", "FactorizationResult", "Devi
            "blocked_apply_q", "tiled_apply_q"]
 
 METHODS = ("mgs", "blocked-hh", "tiled-hh")
+DAG_TIMEOUT_S = 120.0  # a persistent CTA waiting this long for a ready task aborts the run
 
 
 @dataclass
@@ -63,6 +64,30 @@ class FactorizationResult:
 
 
 @lru_cache(maxsize=16)
+def tiled_dag_arrays(p: int, q: int):
+    """(tasks[n,4], indeg[n], succ_off[n+1], succ[e], prio[n]) of the tiled DAG
+    (same read/write-set edges as scheduler.py:173-201), from libblrqr."""
+    lib = _lib.load()
+    ne = C.c_int64(0)
+    n = int(lib.blrqr_tiled_dag_size(p, q, C.byref(ne)))
+    if n < 0:
+        raise ValueError("need p >= q >= 1")
+    tasks = np.zeros((n, 4), dtype=np.int32)
+    indeg = np.zeros(n, dtype=np.int32)
+    off = np.zeros(n + 1, dtype=np.int64)
+    succ = np.zeros(max(ne.value, 1), dtype=np.int32)
+    prio = np.zeros(n, dtype=np.int32)
+    rc = lib.blrqr_tiled_dag(p, q, tasks.ctypes.data, indeg.ctypes.data, off.ctypes.data, succ.ctypes.data,
+                             prio.ctypes.data)
+    if rc != 0:
+        raise RuntimeError("tiled DAG build failed")
+    return tasks, indeg, off, succ, prio
+
+
+SCHEDULERS = ("dag", "levels")
+
+
+@lru_cache(maxsize=16)
 def tiled_schedule(p: int, q: int):
     """(tasks ndarray[n, 4] int32, level_start ndarray[int64]) from the C++
     level scheduler over the reference DAG's read/write sets."""
@@ -83,7 +108,8 @@ def tiled_schedule(p: int, q: int):
 class DeviceFactorization:
     """A BLR-QR factorization resident on the GPU (input grid is cloned)."""
 
-    def __init__(self, method: str, a: DeviceGrid, cfg: ToleranceConfig, clone: bool = True):
+    def __init__(self, method: str, a: DeviceGrid, cfg: ToleranceConfig, clone: bool = True,
+                 scheduler: str = "dag"):
         if method not in METHODS:
             raise ValueError(f"unknown algorithm {method!r}")
         if a.p < a.q:
@@ -97,9 +123,19 @@ class DeviceFactorization:
         self.rg = None
         if method == "tiled-hh":
             self.rf = DeviceRefl(self.g)
+            if scheduler not in SCHEDULERS:
+                raise ValueError(f"scheduler must be one of {SCHEDULERS}")
+            self.scheduler = scheduler
             tasks, self.levels = tiled_schedule(self.g.p, self.g.q)
             self.tasks = torch.from_numpy(tasks).to(self.rt.dev)
             self.nlevels = len(self.levels) - 1
+            if scheduler == "dag":
+                dt, ind, off, succ, prio = tiled_dag_arrays(self.g.p, self.g.q)
+                dev = self.rt.dev
+                self.dag = {"n": len(dt), "tasks": torch.from_numpy(dt).to(dev),
+                            "indeg": torch.from_numpy(ind).to(dev), "off": torch.from_numpy(off).to(dev),
+                            "succ": torch.from_numpy(succ).to(dev), "prio": torch.from_numpy(prio).to(dev),
+                            "work": torch.empty(3 * len(dt) + 8, dtype=torch.int32, device=dev)}
         elif method == "blocked-hh":
             g = self.g
             self.rf = DeviceRefl(self.g)
@@ -122,7 +158,14 @@ class DeviceFactorization:
         rt = self.rt
         g = self.g
         ws, per, nct = rt.workspace(g.b, g.cap, 0, nctas)
-        if self.method == "tiled-hh":
+        if self.method == "tiled-hh" and self.scheduler == "dag":
+            gs, rs = g.cstruct(), self.rf.cstruct()
+            d = self.dag
+            _lib.check(rt.lib.blrqr_tiled_run_dag(
+                C.byref(gs), C.byref(rs), d["n"], d["tasks"].data_ptr(), d["indeg"].data_ptr(), d["off"].data_ptr(),
+                d["succ"].data_ptr(), d["prio"].data_ptr(), d["work"].data_ptr(), self.cfg.epsilon, ws, per, nct,
+                DAG_TIMEOUT_S, rt.status.data_ptr(), rt.flops.data_ptr(), _lib.stream_ptr()), "tiled_run_dag")
+        elif self.method == "tiled-hh":
             gs, rs = g.cstruct(), self.rf.cstruct()
             lv = self.levels.ctypes.data_as(C.c_void_p)
             _lib.check(rt.lib.blrqr_tiled_run(C.byref(gs), C.byref(rs), self.tasks.data_ptr(), lv, 0,
@@ -211,8 +254,9 @@ class DeviceFactorization:
         return store
 
 
-def factorize_device(method: str, a: DeviceGrid, cfg: ToleranceConfig, clone: bool = True) -> DeviceFactorization:
-    f = DeviceFactorization(method, a, cfg, clone)
+def factorize_device(method: str, a: DeviceGrid, cfg: ToleranceConfig, clone: bool = True,
+                     scheduler: str = "dag") -> DeviceFactorization:
+    f = DeviceFactorization(method, a, cfg, clone, scheduler)
     f.run()
     f.finish()
     return f

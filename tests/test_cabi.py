@@ -21,7 +21,7 @@ def lib():
 
 def test_exports_match_header(lib):
     hdr = open(os.path.join(REPO, "include", "blrqr.h")).read()
-    declared = set(re.findall(r"^\s*(?:int|int64_t)\s+(blrqr_\w+)\s*\(", hdr, re.M))
+    declared = set(re.findall(r"^\s*(?:int|int64_t|void)\s+(blrqr_\w+)\s*\(", hdr, re.M))
     assert declared, "no declarations parsed"
     so = lib.load()
     for name in declared:

@@ -123,3 +123,21 @@ def _oracle_state(pk, res, g, eps):
 def test_smoke_entry():
     import __graft_entry__ as ge
     ge.smoke()
+
+
+@pytest.mark.parametrize("tag", ["exp512", "C1"])
+def test_dynamic_and_level_schedulers_bitwise_equal(pk, tag):
+    """Acceptance #5 analogue: every schedule respecting the DAG gives
+    bit-identical R and reflectors (scheduler.py:1-11)."""
+    from paper_2208_06194_b200.device import DeviceGrid
+    from paper_2208_06194_b200.factorize import factorize_device
+    z, meta, dense = _input(tag)
+    n, b, eps = meta["n"], meta["b"], meta["eps"]
+    g = schedule.dense_to_blr(dense, b, oblr.weak_map(n // b, n // b), eps)
+    dg = DeviceGrid.from_host(_to_pkg(pk, g))
+    fa = factorize_device("tiled-hh", dg, pk.ToleranceConfig(eps), clone=True, scheduler="dag")
+    fb = factorize_device("tiled-hh", dg, pk.ToleranceConfig(eps), clone=True, scheduler="levels")
+    import torch
+    assert torch.equal(fa.g.rank, fb.g.rank)
+    assert torch.equal(fa.g.pool, fb.g.pool)
+    assert torch.equal(fa.rf.pool, fb.rf.pool)

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--cap", type=int, default=None)
     ap.add_argument("--levels", type=int, default=None, help="only run the first L levels")
     ap.add_argument("--profile-levels", action="store_true")
+    ap.add_argument("--sched", default="dag")
     args = ap.parse_args()
     ge.build()
     from paper_2208_06194_b200 import _lib, configs, flops
@@ -51,12 +52,12 @@ def main():
     print(json.dumps({"gen_s": tg, "compress_s": tc, "in_rank_min": int(lr.min()), "in_rank_med": float(np.median(lr)),
                       "in_rank_max": int(lr.max())}), flush=True)
     flops.reset()
-    f = DeviceFactorization(method, g, ToleranceConfig(cfg.eps))
+    f = DeviceFactorization(method, g, ToleranceConfig(cfg.eps), scheduler=args.sched if method == "tiled-hh" else "dag")
     rt = _lib.runtime()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     e0.record()
-    if method == "tiled-hh" and (args.levels or args.profile_levels):
+    if method == "tiled-hh" and (args.levels or args.profile_levels) and args.sched == "levels":
         import ctypes as C
         ws, per, nct = rt.workspace(g.b, g.cap)
         gs, rs = f.g.cstruct(), f.rf.cstruct()
@@ -89,6 +90,12 @@ def main():
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     rep = f.finish()
+    ph = dict(_lib.runtime().last_phases)
+    clk = 1.965e9
+    print(json.dumps({"phase_seconds_summed_over_ctas": {k: v / clk for k, v in ph.items()
+                                                         if not k.startswith("jacobi")},
+                      "task_seconds_per_sm": ph.get("task", 0) / clk / _lib.runtime().nctas,
+                      "jacobi_sweeps_per_call": ph.get("jacobi_sweeps", 0) / max(1, ph.get("jacobi_calls", 1))}))
     tot = sum(rep.values())
     rr = f.g.rank_map()
     rl = rr[rr >= 0]
