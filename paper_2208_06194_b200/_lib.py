@@ -127,7 +127,7 @@ class Runtime:
         self.lib = load()
         self.status = torch.zeros(1, dtype=torch.int32, device=self.dev)
         # [0:9] model flops per kind, [16:32] per-phase SM cycles (see PHASES)
-        self.flops = torch.zeros(32, dtype=torch.int64, device=self.dev)
+        self.flops = torch.zeros(64, dtype=torch.int64, device=self.dev)
         self.last_phases = {}
         self.nctas = int(self.lib.blrqr_default_ctas())
         self._ws = None
@@ -155,7 +155,8 @@ class Runtime:
         self.status.zero_()
         self.flops.zero_()
         counts = {k: int(v) for k, v in zip(FLOP_KINDS, fl) if v}
-        self.last_phases = {k: int(v) for k, v in zip(PHASES, fl[16:]) if v}
+        self.last_phases = {k: int(v) for k, v in zip(PHASES, fl[16:32]) if v}
+        self.last_stats = fl[48:56].tolist()
         from . import flops as _fl
         for k, v in counts.items():
             _fl.add(k, v)

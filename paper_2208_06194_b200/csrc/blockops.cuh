@@ -90,6 +90,15 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
   PhaseTimer tc;
   const int kU = min(m, c), kV = min(n, c);
   const int k = kU;  // square blocks: kU == kV
+  // small per-core vectors first, so the k x k core is the top of the shared
+  // arena and can be dropped once its reflectors are saved
+  double* col2 = alloc_fast(cx, k);
+  double* col2o = alloc_fast(cx, k);
+  double* taus = alloc_fast(cx, k);
+  int* piv = reinterpret_cast<int*>(alloc_fast(cx, k));
+  double* tau2 = alloc_fast(cx, k);
+  if (!col2 || !col2o || !taus || !piv || !tau2) { release(cx, mk); return 0; }
+  const int smem_before_g = cx.stop;
   double* G = alloc_fast(cx, (long long)k * k);
   const Mark after_g = mark(cx);  // H, RU, RV are released once the core is formed
   double* H = alloc_fast(cx, (long long)k * k);
@@ -97,27 +106,23 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
   double* RV = alloc_fast(cx, (long long)kV * c);
   if (!G || !H || !RU || !RV) { release(cx, mk); return 0; }
   for (int j = threadIdx.x >> 5; j < c; j += NWARP)
-    for (int i = threadIdx.x & 31; i < kU; i += 32) {
-    const long long e = (long long)j * kU + i;
-    RU[e] = i <= j ? Uc[i + (long long)j * m] : 0.0;
-  }
+    for (int i = threadIdx.x & 31; i < kU; i += 32) RU[(long long)j * kU + i] = i <= j ? Uc[i + (long long)j * m] : 0.0;
   for (int j = threadIdx.x >> 5; j < c; j += NWARP)
-    for (int i = threadIdx.x & 31; i < kV; i += 32) {
-    const long long e = (long long)j * kV + i;
-    RV[e] = i <= j ? Vc[i + (long long)j * n] : 0.0;
-  }
+    for (int i = threadIdx.x & 31; i < kV; i += 32) RV[(long long)j * kV + i] = i <= j ? Vc[i + (long long)j * n] : 0.0;
   __syncthreads();
   gemm(false, true, kU, kV, ra, 1.0, RU, kU, RV, kV, 0.0, G, k);
   gemm(false, true, kU, kV, rb, 1.0, RU + (long long)ra * kU, kU, RV + (long long)ra * kV, kV, 0.0, H, k);
   double sa = 0.0, sb = 0.0, sc = 0.0;
-  for (long long e = threadIdx.x; e < (long long)k * k; e += NT) {
-    const double x = G[e], y = H[e];
-    sa = fma(x, x, sa);
-    sb = fma(y, y, sb);
-    const double z = x + y;
-    G[e] = z;
-    sc = fma(z, z, sc);
-  }
+  for (int j = threadIdx.x >> 5; j < k; j += NWARP)
+    for (int i = threadIdx.x & 31; i < k; i += 32) {
+      const long long e = (long long)j * k + i;
+      const double x = G[e], y = H[e];
+      sa = fma(x, x, sa);
+      sb = fma(y, y, sb);
+      const double z = x + y;
+      G[e] = z;
+      sc = fma(z, z, sc);
+    }
   const double nA = sqrt(cta_sum(sa)), nB = sqrt(cta_sum(sb));
   const double core2 = cta_sum(sc);
   release(cx, after_g);
@@ -125,12 +130,7 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
   add_flops(cx, FK_ROUNDED_ADD, qr_cost(m, c) + qr_cost(n, c) + mm_cost(kU, c, kV) + svd_cost(kU));
   if (core2 == 0.0) { release(cx, mk); return 0; }
   PhaseTimer ts;
-  // (3) QRCP of the core, truncated at rounding level
-  double* col2 = alloc_fast(cx, k);
-  double* col2o = alloc_fast(cx, k);
-  double* taus = alloc_fast(cx, k);
-  int* piv = reinterpret_cast<int*>(alloc_fast(cx, k));
-  if (!col2 || !col2o || !taus || !piv) { release(cx, mk); return 0; }
+  // (3a) QRCP of the core, stopped at rounding level: core P = Q1 [R1; R2]
   {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int cc = warp; cc < k; cc += NWARP) {
@@ -147,22 +147,42 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
   PhaseTimer tqp;
   const int kp = pivoted_qr(k, k, G, k, eps_m * eps_m * core2, k, core2, col2, col2o, piv, taus, &rem2);
   tqp.stop(cx, PH_QRCP);
-  // X = P R1^T (k x kp): X[piv[j], a] = R1[a, j] for j >= a
-  double* X = alloc_fast(cx, (long long)k * max(kp, 1));
-  double* J = alloc_fast(cx, (long long)max(kp, 1) * max(kp, 1));
-  double* sig = alloc_fast(cx, max(kp, 1));
-  int* perm = reinterpret_cast<int*>(alloc_fast(cx, max(kp, 1)));
-  if (!X || !J || !sig || !perm) { release(cx, mk); return 0; }
+  if (threadIdx.x == 0 && cx.flops && k >= 64) {  // stats: sum k, sum kp, count, sum k^3, sum kp^3
+    atomicAdd(cx.flops + 48, (unsigned long long)k);
+    atomicAdd(cx.flops + 49, (unsigned long long)kp);
+    atomicAdd(cx.flops + 50, 1ull);
+    atomicAdd(cx.flops + 51, (unsigned long long)k * k * k);
+    atomicAdd(cx.flops + 52, (unsigned long long)kp * kp * kp);
+  }
+  const int kq = max(kp, 1);
+  // (3b) X = P R1^T (k x kp) and the Q1 reflectors move to the global arena;
+  // the core's shared slot is dropped
+  double* X = alloc(cx, (long long)k * kq);
+  double* Gr = alloc(cx, (long long)k * kq);
+  double* Tp2 = alloc(cx, (long long)QR_NB * kq);
+  if (!X || !Gr || !Tp2) { release(cx, mk); return 0; }
   for (int a = threadIdx.x >> 5; a < kp; a += NWARP)
     for (int j = threadIdx.x & 31; j < k; j += 32) {
-    const long long e = (long long)a * k + j;
-    X[piv[j] + (long long)a * k] = j >= a ? G[a + (long long)j * k] : 0.0;
-  }
+      X[piv[j] + (long long)a * k] = j >= a ? G[a + (long long)j * k] : 0.0;
+      Gr[j + (long long)a * k] = G[j + (long long)a * k];
+    }
   __syncthreads();
-  if (in_smem(cx, X) && in_smem(cx, J))
-    jacobi_smem(cx, k, kp, X, J, sig, perm, cx.flops);  // shared-space loads, 2 pairs per warp
-  else
-    jacobi_cols(k, kp, X, k, J, kp, sig, perm, cx.flops);
+  if (in_smem(cx, G)) cx.stop = smem_before_g;
+  // (3c) second (unpivoted) QR, X = Q2 R2 -- Drmac-Veselic QR+LQ
+  // preconditioning: Jacobi then works on the kp x kp triangle R2
+  qr_blocked(cx, k, kp, X, k, tau2, Tp2);
+  double* W2 = alloc_fast(cx, (long long)kq * kq);
+  double* J = alloc_fast(cx, (long long)kq * kq);
+  double* sig = alloc_fast(cx, kq);
+  int* perm = reinterpret_cast<int*>(alloc_fast(cx, kq));
+  if (!W2 || !J || !sig || !perm) { release(cx, mk); return 0; }
+  for (int j = threadIdx.x >> 5; j < kp; j += NWARP)
+    for (int i = threadIdx.x & 31; i < kp; i += 32) W2[i + (long long)j * kp] = i <= j ? X[i + (long long)j * k] : 0.0;
+  __syncthreads();
+  if (in_smem(cx, W2) && in_smem(cx, J))
+    jacobi_smem(cx, kp, kp, W2, J, sig, perm, cx.flops);  // shared-space loads, 2 pairs per warp
+  else if (kp <= 32 || !jacobi_blocked(cx, kp, kp, W2, kp, J, kp, sig, perm, cx.flops))
+    jacobi_cols(kp, kp, W2, kp, J, kp, sig, perm, cx.flops);
   ts.stop(cx, PH_SVD);
   // (4) truncation (lowrank.py:204-213); the dropped QRCP remainder rem2
   // (<= (eps_mach ||core||)^2) is counted in the total and in every tail
@@ -187,7 +207,7 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
         if (acc <= thresh2) first = i;
         else break;
       }
-      if (first < 0) first = kp;  // unreachable: tail2[k] = 0 <= thresh in the reference
+      if (first < 0) first = kp;
       rank = min(first, significant);
     }
     s_rank = rank;
@@ -202,20 +222,20 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
     PhaseTimer tb;
     double* ZU = alloc(cx, (long long)m * rank);
     double* ZV = alloc(cx, (long long)n * rank);
-    if (!ZU || !ZV) { release(cx, mk); return 0; }
-    // ZU(0:k) = [J_r; 0] then Q_core, ZV(0:k) = W_r
+    double* Z2 = alloc(cx, (long long)k * rank);
+    if (!ZU || !ZV || !Z2) { release(cx, mk); return 0; }
+    // core = Q1 [J; 0] Sigma (Q2 W2hat)^T P^T: left vectors Q1 [J_r; 0],
+    // right (scaled by sigma) Q2 [W2_r; 0]
     for (int j = threadIdx.x >> 5; j < rank; j += NWARP)
-      for (int i = threadIdx.x & 31; i < m; i += 32) {
-      const long long e = (long long)j * m + i;
-      ZU[e] = i < kp ? J[i + (long long)perm[j] * kp] : 0.0;
-    }
+      for (int i = threadIdx.x & 31; i < m; i += 32) ZU[(long long)j * m + i] = i < kp ? J[i + (long long)perm[j] * kp] : 0.0;
     for (int j = threadIdx.x >> 5; j < rank; j += NWARP)
-      for (int i = threadIdx.x & 31; i < n; i += 32) {
-      const long long e = (long long)j * n + i;
-      ZV[e] = i < k ? X[i + (long long)perm[j] * k] : 0.0;
-    }
+      for (int i = threadIdx.x & 31; i < k; i += 32) Z2[(long long)j * k + i] = i < kp ? W2[i + (long long)perm[j] * kp] : 0.0;
     __syncthreads();
-    apply_reflectors(k, kp, G, k, taus, ZU, m, rank);
+    apply_reflectors(k, kp, Gr, k, taus, ZU, m, rank);
+    qr_apply(cx, k, kp, X, k, Tp2, Z2, k, rank, false);
+    for (int j = threadIdx.x >> 5; j < rank; j += NWARP)
+      for (int i = threadIdx.x & 31; i < n; i += 32) ZV[(long long)j * n + i] = i < k ? Z2[i + (long long)j * k] : 0.0;
+    __syncthreads();
     qr_apply(cx, m, kU, Uc, m, TpU, ZU, m, rank, false);
     qr_apply(cx, n, kV, Vc, n, TpV, ZV, n, rank, false);
     copy_mat(m, rank, ZU, m, du, lddu);

@@ -221,130 +221,80 @@ __device__ __noinline__ void jacobi_smem(const Ctx& cx, int rows, int ncols, dou
   __syncthreads();
 }
 
-// Blocked one-sided Jacobi for column sets that do not fit in shared memory:
-// columns are grouped in blocks of JB; each outer round pairs blocks
-// (round-robin), two warp groups each stage one block pair (X and J columns)
-// in shared memory and run a full inner sweep over its 2*JB columns there,
-// then write back.  Same rotations and stopping rule as jacobi_cols (every
-// column pair is visited each outer sweep), far less L2 latency per pair.
-constexpr int JB = 8;
-__device__ __noinline__ void jacobi_cols_blocked(Ctx& cx, int rows, int ncols, double* X, int ldx, double* J,
-                                                 int ldj, double* sigma, int* perm,
-                                                 unsigned long long* prof = nullptr) {
+// Blocked one-sided Jacobi for column sets that do not fit in shared memory
+// (X k x kp and J kp x kp in L2).  Columns are grouped in blocks of jb; each
+// outer round pairs blocks round-robin and, per block pair, the CTA stages
+// the 2*jb columns of X and J in shared memory, runs a full inner cyclic
+// sweep over them there (one warp per column pair), and writes them back.
+// Every column pair is met at least once per outer sweep, so the stopping
+// rule is the plain method's; L2 traffic drops by ~jb versus visiting pairs
+// one at a time in global memory.  Returns false (nothing done) when the
+// staging buffer does not fit, so the caller can fall back.
+__device__ __noinline__ bool jacobi_blocked(Ctx& cx, int rows, int ncols, double* X, int ldx, double* J, int ldj,
+                                            double* sigma, int* perm, unsigned long long* prof = nullptr) {
   __shared__ int s_rot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int jb = 16;
+  while (jb > 2 && 2 * jb * (rows + ncols) > cx.scap - cx.stop) jb >>= 1;
+  if (2 * jb * (rows + ncols) > cx.scap - cx.stop) return false;
+  const Mark mk = mark(cx);
+  double* st = salloc(cx, (long long)2 * jb * (rows + ncols));
+  double* Xs = as_smem(cx, st);
+  double* Js = Xs + 2 * jb * rows;
   for (int j = warp; j < ncols; j += NWARP)
     for (int i = lane; i < ncols; i += 32) J[i + (long long)j * ldj] = (i == j) ? 1.0 : 0.0;
   __syncthreads();
-  const Mark mk = mark(cx);
-  const int per_group = 2 * JB * (rows + ncols);
-  int groups = 2;
-  double* stage = salloc(cx, (long long)groups * per_group);
-  if (!stage) {
-    groups = 1;
-    stage = salloc(cx, per_group);
-  }
-  if (!stage) stage = alloc(cx, (long long)per_group);  // last resort: L2-resident staging
-  if (!stage) { release(cx, mk); return; }
-  if (in_smem(cx, stage)) stage = as_smem(cx, stage);
-  const int gw = NWARP / groups, gt = gw * 32;
-  const int grp = warp / gw, wg = warp % gw;
-  const int tid_g = threadIdx.x - grp * gt;
-  double* Xs = stage + (long long)grp * per_group;
-  double* Js = Xs + 2 * JB * rows;
-  auto gsync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(gt)); };
   const double tol = 2.220446049250313e-16 * (double)max(rows, 1);
   const double tol2 = tol * tol;
-  const int nb = (ncols + JB - 1) / JB;
+  const int nb = (ncols + jb - 1) / jb;
   const int nbe = (nb + 1) & ~1;
   for (int sweep = 0; sweep < 40 && ncols > 1; ++sweep) {
     if (threadIdx.x == 0) s_rot = 0;
     __syncthreads();
-    for (int rnd = 0; rnd < max(nbe - 1, 1); ++rnd) {
-      for (int bp = grp; bp < max(nbe / 2, 1); bp += groups) {
+    for (int rnd = 0; rnd < nbe - 1; ++rnd) {
+      for (int bp = 0; bp < nbe / 2; ++bp) {
         int bi, bj;
-        if (nbe == 1 || nb == 1) {
-          bi = 0; bj = 0;
-        } else {
-          int p = bp - 1 + rnd;
-          if (p >= nbe - 1) p -= nbe - 1;
-          bi = bp == 0 ? 0 : 1 + p;
-          int q = nbe - 2 - bp + rnd;
-          if (q >= nbe - 1) q -= nbe - 1;
-          bj = 1 + q;
+        rr_pair(bp, rnd, nbe, bi, bj);
+        if (bj >= nb) continue;  // dummy block (uniform across the CTA)
+        const int ni = min(jb, ncols - bi * jb), nj = min(jb, ncols - bj * jb);
+        const int nc = ni + nj;
+        // stage in: local column c -> global column
+        for (int c = warp; c < nc; c += NWARP) {
+          const int gc = c < ni ? bi * jb + c : bj * jb + (c - ni);
+          const double* xg = X + (long long)gc * ldx;
+          const double* jg = J + (long long)gc * ldj;
+          for (int i = lane; i < rows; i += 32) Xs[i + c * rows] = xg[i];
+          for (int i = lane; i < ncols; i += 32) Js[i + c * ncols] = jg[i];
         }
-        if (bi >= nb || bj >= nb) continue;  // uniform within the group
-        // local columns: block bi (first JB slots) then block bj (unless same)
-        int cols[2 * JB];
-        int nc = 0;
-        for (int c = 0; c < JB; ++c)
-          if (bi * JB + c < ncols) cols[nc++] = bi * JB + c;
-        if (bj != bi)
-          for (int c = 0; c < JB; ++c)
-            if (bj * JB + c < ncols) cols[nc++] = bj * JB + c;
-        // stage in
-        for (int c = tid_g >> 5; c < nc; c += gw) {
-          const double* xs = X + (long long)cols[c] * ldx;
-          const double* js = J + (long long)cols[c] * ldj;
-          for (int i = lane; i < rows; i += 32) Xs[i + c * rows] = xs[i];
-          for (int i = lane; i < ncols; i += 32) Js[i + c * ncols] = js[i];
-        }
-        gsync();
-        // inner round-robin sweep over nc local columns
+        __syncthreads();
         const int kk = (nc + 1) & ~1;
         for (int r2 = 0; r2 < kk - 1; ++r2) {
-          for (int pi = wg; pi < kk / 2; pi += gw) {
-            int p = pi - 1 + r2;
-            if (p >= kk - 1) p -= kk - 1;
-            p = pi == 0 ? 0 : 1 + p;
-            int q = kk - 2 - pi + r2;
-            if (q >= kk - 1) q -= kk - 1;
-            q += 1;
-            if (p >= nc || q >= nc) continue;
-            if (p > q) { const int t = p; p = q; q = t; }
-            double* gp = Xs + p * rows;
-            double* gq = Xs + q * rows;
-            double a = 0.0, b = 0.0, g = 0.0;
-            for (int i = lane; i < rows; i += 32) {
-              const double x = gp[i], y = gq[i];
-              a = fma(x, x, a);
-              b = fma(y, y, b);
-              g = fma(x, y, g);
-            }
+          for (int pi = warp; pi < kk / 2; pi += NWARP) {
+            int p, q;
+            rr_pair(pi, r2, kk, p, q);
+            if (q >= nc) continue;
+            double a, b, g;
+            jac_dots(Xs + p * rows, Xs + q * rows, rows, lane, a, b, g);
             a = warp_sum(a);
             b = warp_sum(b);
             g = warp_sum(g);
-            if (g == 0.0 || a == 0.0 || b == 0.0) continue;
-            if (g * g <= tol2 * a * b) continue;
-            const double zeta = (b - a) / (2.0 * g);
-            const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-            const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-            for (int i = lane; i < rows; i += 32) {
-              const double x = gp[i], y = gq[i];
-              gp[i] = c * x - s * y;
-              gq[i] = s * x + c * y;
-            }
-            double* jp = Js + p * ncols;
-            double* jq = Js + q * ncols;
-            for (int i = lane; i < ncols; i += 32) {
-              const double x = jp[i], y = jq[i];
-              jp[i] = c * x - s * y;
-              jq[i] = s * x + c * y;
-            }
+            double c, s;
+            if (!jac_angle(a, b, g, tol2, c, s)) continue;
+            jac_rotate(Xs + p * rows, Xs + q * rows, rows, lane, c, s);
+            jac_rotate(Js + p * ncols, Js + q * ncols, ncols, lane, c, s);
             if (lane == 0) s_rot = 1;
           }
-          gsync();
+          __syncthreads();
         }
-        // stage out
-        for (int c = tid_g >> 5; c < nc; c += gw) {
-          double* xs = X + (long long)cols[c] * ldx;
-          double* js = J + (long long)cols[c] * ldj;
-          for (int i = lane; i < rows; i += 32) xs[i] = Xs[i + c * rows];
-          for (int i = lane; i < ncols; i += 32) js[i] = Js[i + c * ncols];
+        for (int c = warp; c < nc; c += NWARP) {
+          const int gc = c < ni ? bi * jb + c : bj * jb + (c - ni);
+          double* xg = X + (long long)gc * ldx;
+          double* jg = J + (long long)gc * ldj;
+          for (int i = lane; i < rows; i += 32) xg[i] = Xs[i + c * rows];
+          for (int i = lane; i < ncols; i += 32) jg[i] = Js[i + c * ncols];
         }
-        gsync();
+        __syncthreads();
       }
-      __syncthreads();
     }
     const int rot = s_rot;
     __syncthreads();
@@ -371,6 +321,7 @@ __device__ __noinline__ void jacobi_cols_blocked(Ctx& cx, int rows, int ncols, d
     perm[r] = i;
   }
   __syncthreads();
+  return true;
 }
 
 // Column-pivoted Householder QR steps on A (m x n, lda), in place: pivot on

@@ -95,7 +95,8 @@ def main():
     print(json.dumps({"phase_seconds_summed_over_ctas": {k: v / clk for k, v in ph.items()
                                                          if not k.startswith("jacobi")},
                       "task_seconds_per_sm": ph.get("task", 0) / clk / _lib.runtime().nctas,
-                      "jacobi_sweeps_per_call": ph.get("jacobi_sweeps", 0) / max(1, ph.get("jacobi_calls", 1))}))
+                      "jacobi_sweeps_per_call": ph.get("jacobi_sweeps", 0) / max(1, ph.get("jacobi_calls", 1)),
+                      "big_core_stats(k>=64)": {"count": _lib.runtime().last_stats[2], "mean_k": _lib.runtime().last_stats[0] / max(1, _lib.runtime().last_stats[2]), "mean_kp": _lib.runtime().last_stats[1] / max(1, _lib.runtime().last_stats[2]), "sum_k3_over_sum_kp3": _lib.runtime().last_stats[3] / max(1, _lib.runtime().last_stats[4])}}))
     tot = sum(rep.values())
     rr = f.g.rank_map()
     rl = rr[rr >= 0]
