@@ -141,3 +141,52 @@ def test_dynamic_and_level_schedulers_bitwise_equal(pk, tag):
     assert torch.equal(fa.g.rank, fb.g.rank)
     assert torch.equal(fa.g.pool, fb.g.pool)
     assert torch.equal(fa.rf.pool, fb.rf.pool)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_distributed_gpu_store_emulated_ranks(pk, world):
+    """The GPU store of the block-cyclic driver, with `world` ranks emulated
+    on one GPU level by level (no rank ever waits on another; broadcasts are
+    device copies from the owner's buffers): the assembled R-tilde and every
+    reflector must equal the single-GPU run bit for bit."""
+    import torch
+    from paper_2208_06194_b200 import distributed as D
+    from paper_2208_06194_b200.device import DeviceGrid
+    from paper_2208_06194_b200.factorize import factorize_device
+    z, meta, dense = _input("exp512")
+    n, b, eps = meta["n"], meta["b"], meta["eps"]
+    g = schedule.dense_to_blr(dense, b, oblr.weak_map(n // b, n // b), eps)
+    dg = DeviceGrid.from_host(_to_pkg(pk, g))
+    cfg = pk.ToleranceConfig(eps)
+    ref = factorize_device("tiled-hh", dg, cfg, clone=True, scheduler="levels")
+    stores = [D.GpuStore(dg.clone(), cfg, world, r) for r in range(world)]
+    for lv in range(len(stores[0].plan)):
+        for r, st in enumerate(stores):
+            own = st.plan[lv][0]
+            if len(own):
+                st.run(lv, own)
+        for t in stores[0].plan[lv][1]:
+            src = D.task_owner(t, world)
+            sb = stores[src].reflector_buffers(t)
+            for r in range(world):
+                if r != src:
+                    for dst, s_ in zip(stores[r].reflector_buffers(t), sb):
+                        dst.copy_(s_)
+    torch.cuda.synchronize()
+    q = ref.g.q
+    for j in range(q):
+        st = stores[D.column_owner(j, world)]
+        for i in range(ref.g.p):
+            c = i * q + j
+            assert int(st.g.rank[c]) == int(ref.g.rank[c])
+            o = int(ref.g.off_u_host[c])
+            sz = 2 * b * ref.g.cap if ref.g.kind_host[i, j] else b * b
+            if ref.g.kind_host[i, j]:
+                r_ = int(ref.g.rank[c])
+                assert torch.equal(st.g.pool[o:o + b * r_], ref.g.pool[o:o + b * r_])
+            else:
+                assert torch.equal(st.g.pool[o:o + sz], ref.g.pool[o:o + sz])
+    for st in stores:  # every rank ends with every column's T factors
+        for c in np.nonzero(ref.rf.t_off_host >= 0)[0]:
+            t0 = int(ref.rf.t_off_host[c])
+            assert torch.equal(st.rf.pool[t0:t0 + b * b], ref.rf.pool[t0:t0 + b * b])
