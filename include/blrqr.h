@@ -70,10 +70,18 @@ typedef struct {
   const int64_t* y_off;
   const int64_t* t_off;
   int* yrank;
+  /* dynamic scheduler only: per-cell slot (2*b*b doubles at wpool + c*2*b*b)
+   * holding w = T_ik^T (R_kj + Ytilde^T A_ij) between the two halves of a
+   * split ApplyTrapReflector; wrank[c] its rank (-1 dense).  NULL otherwise. */
+  double* wpool;
+  int* wrank;
 } blrqr_refl;
 
 /* one tiled task: kind 0 DiagQR(k), 1 ApplyBlockReflector(k,j),
- * 2 UpdateQR(k,i), 3 ApplyTrapReflector(k,i,j) (scheduler.py:61-70) */
+ * 2 UpdateQR(k,i), 3 ApplyTrapReflector(k,i,j) (scheduler.py:61-70);
+ * the dynamic scheduler splits kind 3 into 4 (top half: R_kj update, stores
+ * w) and 5 (bottom half: A_ij -= Ytilde w), which may run concurrently with
+ * the next link of the R_kj chain. */
 typedef struct {
   int kind, k, i, j;
 } blrqr_task;

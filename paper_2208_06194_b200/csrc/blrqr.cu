@@ -445,6 +445,8 @@ __global__ void __launch_bounds__(NT, 1) k_tiled_dag(DagDev d, blrqr_grid g, blr
       case 0: tiled_diag(cx, g, rf, tk.k); break;
       case 1: tiled_block(cx, g, rf, tk.k, tk.j); break;
       case 2: tiled_update(cx, g, rf, tk.k, tk.i); break;
+      case 4: tiled_trap_a(cx, g, rf, eps, tk.k, tk.i, tk.j); break;
+      case 5: tiled_trap_b(cx, g, rf, eps, tk.k, tk.i, tk.j); break;
       default: tiled_trap(cx, g, rf, eps, tk.k, tk.i, tk.j); break;
     }
     tt.stop(cx, PH_TASK);
@@ -682,12 +684,15 @@ static void tiled_access(const blrqr_task& t, std::vector<int64_t>& rd, std::vec
   auto A = [](int i, int j) { return ((int64_t)0 << 40) | ((int64_t)i << 20) | j; };
   auto D = [](int k) { return ((int64_t)1 << 40) | ((int64_t)k << 20) | k; };
   auto U = [](int i, int k) { return ((int64_t)2 << 40) | ((int64_t)i << 20) | k; };
+  auto W = [](int i, int j) { return ((int64_t)3 << 40) | ((int64_t)i << 20) | j; };
   rd.clear();
   wr.clear();
   switch (t.kind) {
     case 0: rd = {A(t.k, t.k)}; wr = {A(t.k, t.k), D(t.k)}; break;
     case 1: rd = {D(t.k), A(t.k, t.j)}; wr = {A(t.k, t.j)}; break;
     case 2: rd = {A(t.k, t.k), A(t.i, t.k)}; wr = {A(t.k, t.k), A(t.i, t.k), U(t.i, t.k)}; break;
+    case 4: rd = {U(t.i, t.k), A(t.k, t.j), A(t.i, t.j)}; wr = {A(t.k, t.j), W(t.i, t.j)}; break;
+    case 5: rd = {U(t.i, t.k), W(t.i, t.j), A(t.i, t.j)}; wr = {A(t.i, t.j)}; break;
     default: rd = {U(t.i, t.k), A(t.k, t.j), A(t.i, t.j)}; wr = {A(t.k, t.j), A(t.i, t.j)}; break;
   }
 }
@@ -774,7 +779,10 @@ static void tiled_dag_host(int p, int q, std::vector<blrqr_task>& tasks, std::ve
     for (int j = k + 1; j < q; ++j) tasks.push_back({1, k, -1, j});
     for (int i = k + 1; i < p; ++i) {
       tasks.push_back({2, k, i, -1});
-      for (int j = k + 1; j < q; ++j) tasks.push_back({3, k, i, j});
+      for (int j = k + 1; j < q; ++j) {
+        tasks.push_back({4, k, i, j});  // split ApplyTrap: top half
+        tasks.push_back({5, k, i, j});  //                   bottom half
+      }
     }
   }
   const int n = (int)tasks.size();
@@ -843,7 +851,10 @@ int blrqr_tiled_dag(int p, int q, blrqr_task* tasks_host, int* indeg_host, int64
   std::copy(indeg.begin(), indeg.end(), indeg_host);
   std::copy(off.begin(), off.end(), succ_off_host);
   std::copy(succ.begin(), succ.end(), succ_host);
-  for (size_t t = 0; t < tasks.size(); ++t) prio_host[t] = (tasks[t].kind == 0 || tasks[t].kind == 2) ? 1 : 0;
+  // high priority: DiagQR, UpdateQR and the R_kj chain of the next panel column
+  for (size_t t = 0; t < tasks.size(); ++t)
+    prio_host[t] = (tasks[t].kind == 0 || tasks[t].kind == 2 || (tasks[t].kind == 4 && tasks[t].j == tasks[t].k + 1))
+                       ? 1 : 0;
   return 0;
 }
 

@@ -169,4 +169,54 @@ __device__ void tiled_trap(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, d
   cx.top = mark;
 }
 
+// Split ApplyTrapReflector for the dynamic scheduler: the top half computes
+// w and updates R_kj (the serial chain over i), the bottom half updates A_ij
+// from the stored w and can overlap the next link of the chain.  Same
+// operations as tiled_trap, so results are bitwise identical.
+__device__ void tiled_trap_a(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, double eps, int k, int i, int j) {
+  const long long mark = cx.top;
+  const int b = g.b;
+  const Blk yt = refl_blk(g, rf, i, k);
+  const double* T = rf.pool + rf.t_off[(long long)i * g.q + k];
+  Cell top = grid_cell(g, k, j), bot = grid_cell(g, i, j);
+  const Blk tb = cell_blk(top), bb = cell_blk(bot);
+  PhaseTimer t1;
+  Blk prod = blk_mul_t(cx, yt, bb);
+  t1.stop(cx, PH_PRODUCT);
+  Blk ssum = blk_acc(cx, tb, prod, eps, b);
+  PhaseTimer t2;
+  Blk w = blk_dense_times(cx, T, b, true, ssum);
+  t2.stop(cx, PH_PRODUCT);
+  const long long cw = (long long)i * g.q + j;
+  double* wu = rf.wpool + cw * 2 * b * b;
+  double* wv = wu + (long long)b * b;
+  if (w.lr) {
+    copy_mat(b, w.rank, w.u, w.ldu, wu, b);
+    copy_mat(b, w.rank, w.v, w.ldv, wv, b);
+    if (threadIdx.x == 0) rf.wrank[cw] = w.rank;
+  } else {
+    copy_mat(b, b, w.u, w.ldu, wu, b);
+    if (threadIdx.x == 0) rf.wrank[cw] = -1;
+  }
+  if (w.s != 1.0) set_status(cx, ST_BAD_ARG);  // w inherits ssum's unit scale
+  __syncthreads();
+  sub_into_cell(cx, top, w, eps);
+  cx.top = mark;
+}
+
+__device__ void tiled_trap_b(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, double eps, int k, int i, int j) {
+  const long long mark = cx.top;
+  const int b = g.b;
+  const Blk yt = refl_blk(g, rf, i, k);
+  const long long cw = (long long)i * g.q + j;
+  double* wu = rf.wpool + cw * 2 * b * b;
+  const int wr = rf.wrank[cw];
+  const Blk w = wr >= 0 ? make_lr(b, b, wr, wu, b, wu + (long long)b * b, b, 1.0) : make_dense(b, b, wu, b, 1.0);
+  PhaseTimer t3;
+  Blk yw = blk_mul(cx, yt, w);
+  t3.stop(cx, PH_PRODUCT);
+  sub_into_cell(cx, grid_cell(g, i, j), yw, eps);
+  cx.top = mark;
+}
+
 }  // namespace blr

@@ -192,10 +192,21 @@ class DeviceRefl:
         self.t_off = torch.from_numpy(t_off).to(dev)
         self.yrank = torch.full((p * q,), -1, dtype=torch.int32, device=dev)
         self.pool = torch.zeros(o, dtype=torch.float64, device=dev)
+        self.wpool = None
+        self.wrank = None
+
+    def enable_split_traps(self) -> None:
+        """Allocate the per-cell w slots used by the split ApplyTrap tasks of
+        the dynamic scheduler (2*b*b doubles per cell)."""
+        if self.wpool is None:
+            g = self.grid
+            self.wpool = torch.empty(g.p * g.q * 2 * g.b * g.b, dtype=torch.float64, device=g.pool.device)
+            self.wrank = torch.zeros(g.p * g.q, dtype=torch.int32, device=g.pool.device)
 
     def cstruct(self) -> _lib.Refl:
         return _lib.Refl(self.pool.data_ptr(), self.y_off.data_ptr(), self.t_off.data_ptr(),
-                         self.yrank.data_ptr())
+                         self.yrank.data_ptr(), self.wpool.data_ptr() if self.wpool is not None else None,
+                         self.wrank.data_ptr() if self.wrank is not None else None)
 
     def mat(self, off: int, rows: int, cols: int) -> np.ndarray:
         """Download a column-major rows x cols matrix at pool offset ``off``."""

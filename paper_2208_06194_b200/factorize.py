@@ -130,6 +130,7 @@ class DeviceFactorization:
             self.tasks = torch.from_numpy(tasks).to(self.rt.dev)
             self.nlevels = len(self.levels) - 1
             if scheduler == "dag":
+                self.rf.enable_split_traps()
                 dt, ind, off, succ, prio = tiled_dag_arrays(self.g.p, self.g.q)
                 dev = self.rt.dev
                 self.dag = {"n": len(dt), "tasks": torch.from_numpy(dt).to(dev),

@@ -48,7 +48,7 @@ while t >= 0:
     path.append(t)
     t = pred[t]
 path = path[::-1]
-kinds = ["diag", "block", "update", "trap"]
+kinds = ["diag", "block", "update", "trap", "trapA", "trapB"]
 kind_time = {k: float(dur[tasks[:, 0] == i].sum()) for i, k in enumerate(kinds)}
 path_kinds = {k: 0.0 for k in kinds}
 for t in path:
