@@ -176,6 +176,9 @@ int64_t blrqr_tiled_dag_size(int p, int q, int64_t* nedges);
 /* Debug: record (start ns, end ns, SM id) per task of subsequent dynamic runs
  * into a device buffer of 3*ntasks int64 (NULL disables). */
 void blrqr_debug_trace(void* dev_buf);
+/* Debug: `ctas` CTAs each run `reps` CTA-level GEMMs C = op(A) op(B) (+ C). */
+int blrqr_debug_gemm(int ta, int tb, int M, int N, int K, const double* A, int lda, const double* B, int ldb,
+                     double* C, int ldc, int reps, int ctas, void* stream);
 int blrqr_tiled_dag(int p, int q, blrqr_task* tasks_host, int* indeg_host, int64_t* succ_off_host,
                     int* succ_host, int* prio_host);
 int blrqr_tiled_run_dag(const blrqr_grid* g, const blrqr_refl* rf, int ntasks, const blrqr_task* tasks_dev,

@@ -962,3 +962,18 @@ int blrqr_mgs_step(const blrqr_grid* a, const blrqr_grid* qg, const blrqr_grid* 
 }
 
 }  // extern "C"
+
+// ---- debug: single-CTA GEMM throughput probe -------------------------------
+__global__ void __launch_bounds__(NT, 1) k_gemm_probe(int ta, int tb, int M, int N, int K, const double* A, int lda,
+                                                      const double* B, int ldb, double* C, int ldc, int reps) {
+  for (int r = 0; r < reps; ++r) gemm(ta != 0, tb != 0, M, N, K, 1.0, A, lda, B, ldb, r == 0 ? 0.0 : 1.0, C, ldc);
+}
+
+extern "C" int blrqr_debug_gemm(int ta, int tb, int M, int N, int K, const double* A, int lda, const double* B,
+                                int ldb, double* C, int ldc, int reps, int ctas, void* stream) {
+  INIT_KERNELS();
+  cudaFuncSetAttribute(k_gemm_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  k_gemm_probe<<<ctas, NT, SMEM_BYTES, as_stream(stream)>>>(ta, tb, M, N, K, A, lda, B, ldb, C, ldc, reps);
+  CK(cudaGetLastError());
+  return 0;
+}

@@ -231,7 +231,7 @@ __device__ void transpose_mat(int m, int n, const double* A, int lda, double* B,
 
 constexpr int GEMM_SMEM = 2600;  // doubles of shared scratch shared by all GEMM tile shapes
 __device__ __forceinline__ double* gemm_smem() {
-  __shared__ double buf[GEMM_SMEM];
+  __shared__ __align__(16) double buf[GEMM_SMEM];
   return buf;
 }
 
@@ -353,6 +353,63 @@ __device__ __noinline__ void gemm_tn_dot(int M, int N, int K, double alpha, cons
   __syncthreads();
 }
 
+// Row-streaming GEMM for tall outputs (M >= NT/2): thread t owns rows
+// t, t+NT, ...  K is processed in chunks of 16: the 16 x ncs slab of op(B)
+// is staged in shared memory (read back as warp-uniform broadcasts), the
+// thread's 16 values of op(A) sit in registers, and C is streamed once per
+// chunk with coalesced column accesses.  For the rank-16 panel updates of
+// the Householder kernels (K = QR_NB) C is touched exactly once.
+__device__ __noinline__ void gemm_rows(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, int lda,
+                                       const double* B, int ldb, double beta, double* C, int ldc) {
+  constexpr int KC = 16;
+  constexpr int CS = (GEMM_SMEM / KC) & ~3;  // columns per staged B slab
+  double* Bs = gemm_smem();
+  for (int cs = 0; cs < N; cs += CS) {
+    const int ncs = min(CS, N - cs);
+    for (int k0 = 0; k0 < K; k0 += KC) {
+      const int kc = min(KC, K - k0);
+      __syncthreads();
+      for (int e = threadIdx.x; e < KC * ncs; e += NT) {
+        const int kk = e % KC, jj = e / KC;
+        const int k = k0 + kk, j = cs + jj;
+        Bs[e] = kk < kc ? (tb ? B[j + (long long)k * ldb] : B[k + (long long)j * ldb]) : 0.0;
+      }
+      __syncthreads();
+      const bool first = (k0 == 0);
+      for (int i = threadIdx.x; i < M; i += NT) {
+        double a[KC];
+#pragma unroll
+        for (int kk = 0; kk < KC; ++kk)
+          a[kk] = kk < kc ? (ta ? A[(k0 + kk) + (long long)i * lda] : A[i + (long long)(k0 + kk) * lda]) : 0.0;
+        for (int jj = 0; jj < ncs; jj += 4) {
+          double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const double2* b2 = reinterpret_cast<const double2*>(Bs + KC * (jj + u));
+#pragma unroll
+            for (int kk = 0; kk < KC; kk += 2) {
+              const double2 bv = b2[kk >> 1];
+              acc[u] = fma(a[kk], bv.x, acc[u]);
+              acc[u] = fma(a[kk + 1], bv.y, acc[u]);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (jj + u < ncs) {
+              double* c = C + i + (long long)(cs + jj + u) * ldc;
+              if (first)
+                *c = beta == 0.0 ? alpha * acc[u] : alpha * acc[u] + beta * (*c);
+              else
+                *c += alpha * acc[u];
+            }
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
 __device__ __noinline__ void gemm(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, int lda,
                      const double* B, int ldb, double beta, double* C, int ldc) {
   if (ta && !tb && M > 0 && N > 0 && K >= 64 && (long long)M * N <= 4096) {
@@ -360,6 +417,10 @@ __device__ __noinline__ void gemm(bool ta, bool tb, int M, int N, int K, double 
     return;
   }
   if (M <= 0 || N <= 0) return;
+  if (!ta && K > 0 && K <= 32 && M >= NT / 2) {  // rank-16/32 panel updates
+    gemm_rows(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    return;
+  }
   if (K <= 0) {  // C = beta * C
     const long long tot = (long long)M * N;
     for (long long e = threadIdx.x; e < tot; e += NT) {
