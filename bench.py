@@ -172,7 +172,7 @@ def run_ours(args):
     t_gen = time.perf_counter() - t0
     t0 = time.perf_counter()
     g0 = DeviceGrid.from_dense(dense, cfg.b, weak_admissibility(cfg.n // cfg.b, cfg.n // cfg.b), cfg.eps, 0.5,
-                               colmajor=True)
+                               cap=cfg.cap, colmajor=True)
     torch.cuda.synchronize()
     t_comp = time.perf_counter() - t0
     del dense

@@ -70,11 +70,12 @@ typedef struct {
   const int64_t* y_off;
   const int64_t* t_off;
   int* yrank;
-  /* dynamic scheduler only: per-cell slot (2*b*b doubles at wpool + c*2*b*b)
+  /* dynamic scheduler only: per-cell slot (wslot doubles at wpool + c*wslot)
    * holding w = T_ik^T (R_kj + Ytilde^T A_ij) between the two halves of a
    * split ApplyTrapReflector; wrank[c] its rank (-1 dense).  NULL otherwise. */
   double* wpool;
   int* wrank;
+  int64_t wslot; /* doubles per cell slot (2*b*cap; a dense w needs b*b <= wslot) */
 } blrqr_refl;
 
 /* one tiled task: kind 0 DiagQR(k), 1 ApplyBlockReflector(k,j),

@@ -37,7 +37,7 @@ class Grid(C.Structure):
 
 class Refl(C.Structure):
     _fields_ = [("pool", C.c_void_p), ("y_off", C.c_void_p), ("t_off", C.c_void_p),
-                ("yrank", C.c_void_p), ("wpool", C.c_void_p), ("wrank", C.c_void_p)]
+                ("yrank", C.c_void_p), ("wpool", C.c_void_p), ("wrank", C.c_void_p), ("wslot", C.c_int64)]
 
 
 class Task(C.Structure):

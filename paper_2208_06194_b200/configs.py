@@ -25,6 +25,7 @@ class Config:
     eps: float
     method: str
     seed: int = 0
+    cap: int | None = None  # low-rank slab capacity (None: b)
 
 
 CONFIGS = {
@@ -32,7 +33,7 @@ CONFIGS = {
     "C2": Config("C2", "laplace", 16384, 256, 1e-8, "blocked-hh"),
     "C3": Config("C3", "expcov", 32768, 512, 1e-8, "tiled-hh"),
     "C4": Config("C4", "invpoisson", 16384, 256, 1e-10, "tiled-hh"),
-    "C5": Config("C5", "laplace", 65536, 1024, 1e-8, "tiled-hh"),
+    "C5": Config("C5", "laplace", 65536, 1024, 1e-8, "tiled-hh", cap=256),  # ranks <= ~15
 }
 
 

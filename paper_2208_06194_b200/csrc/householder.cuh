@@ -301,4 +301,127 @@ __device__ __noinline__ void tpqrt(Ctx& cx, int n, int k, double* R, int ldr, do
   cx.top = mark;
 }
 
+
+// ---------------------------------------------------------------------------
+// Triangular-pentagonal QR for a SHORT bottom block (k <= KM rows, n <= 2*NT
+// columns): the UpdateQR of a low-rank tile (B = V_ik^T, k = rank).
+// Column l is owned by one thread, which keeps B(:, l) in registers; the
+// reflector of column j is formed by its owner and broadcast through shared
+// memory (one barrier per column, double-buffered).  The full T then follows
+// from the low-rank Gram structure V^T V = I + Y^T Y of V = [I; Y]: with
+// Z_j = T(0:j,0:j) Y(:,0:j)^T, T(0:j, j) = -tau_j Z_j y_j and
+// Z_{j+1} = Z_j + T(:, j) y_j^T, so every row i of T is produced by one thread
+// with a k-vector of state -- O(n^2 k) work, no barriers -- instead of the
+// O(n^3) forward recurrence.  Same reflectors as LAPACK dtpqrt (l = 0).
+// B is read / written transposed: element (a, l) at Bt[l + a*ldbt].
+// ---------------------------------------------------------------------------
+template <int KM>
+__device__ __noinline__ void tpqrt_small(Ctx& cx, int n, int k, double* R, int ldr, double* Bt, int ldbt, double* T,
+                                         int ldt) {
+  __shared__ double s_v[2][KM];
+  __shared__ double s_tau[2];
+  const Mark mk = mark(cx);
+  double* taus = alloc_fast(cx, n);
+  if (!taus) return;
+  const int l0 = threadIdx.x, l1 = threadIdx.x + NT;
+  double b0[KM], b1[KM];
+#pragma unroll
+  for (int a = 0; a < KM; ++a) {
+    b0[a] = (a < k && l0 < n) ? Bt[l0 + (long long)a * ldbt] : 0.0;
+    b1[a] = (a < k && l1 < n) ? Bt[l1 + (long long)a * ldbt] : 0.0;
+  }
+  for (int j = 0; j < n; ++j) {
+    const int buf = j & 1;
+    if (threadIdx.x == (j % NT)) {
+      const bool hi = j >= NT;
+      double xn2 = 0.0;
+#pragma unroll
+      for (int a = 0; a < KM; ++a) {
+        const double x = hi ? b1[a] : b0[a];
+        xn2 = fma(x, x, xn2);
+      }
+      double* rjj = R + j + (long long)j * ldr;
+      const double alpha = *rjj;
+      double tau = 0.0, beta = alpha;
+      if (xn2 != 0.0) {
+        const double mu = sqrt(alpha * alpha + xn2);
+        beta = alpha >= 0.0 ? -mu : mu;
+        tau = (beta - alpha) / beta;
+        const double scal = 1.0 / (alpha - beta);
+#pragma unroll
+        for (int a = 0; a < KM; ++a) {
+          if (hi) b1[a] *= scal;
+          else b0[a] *= scal;
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < KM; ++a) s_v[buf][a] = hi ? b1[a] : b0[a];
+      s_tau[buf] = tau;
+      taus[j] = tau;
+      *rjj = beta;
+    }
+    __syncthreads();
+    const double tau = s_tau[buf];
+    if (tau != 0.0) {
+      if (l0 < n && l0 > j) {
+        double* r = R + j + (long long)l0 * ldr;
+        double d = *r;
+#pragma unroll
+        for (int a = 0; a < KM; ++a) d = fma(s_v[buf][a], b0[a], d);
+        d *= tau;
+        *r -= d;
+#pragma unroll
+        for (int a = 0; a < KM; ++a) b0[a] = fma(-d, s_v[buf][a], b0[a]);
+      }
+      if (l1 < n && l1 > j) {
+        double* r = R + j + (long long)l1 * ldr;
+        double d = *r;
+#pragma unroll
+        for (int a = 0; a < KM; ++a) d = fma(s_v[buf][a], b1[a], d);
+        d *= tau;
+        *r -= d;
+#pragma unroll
+        for (int a = 0; a < KM; ++a) b1[a] = fma(-d, s_v[buf][a], b1[a]);
+      }
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < KM; ++a) {
+    if (a < k && l0 < n) Bt[l0 + (long long)a * ldbt] = b0[a];
+    if (a < k && l1 < n) Bt[l1 + (long long)a * ldbt] = b1[a];
+  }
+  __syncthreads();
+  // Y (k x n) for the T build: shared memory when it fits
+  double* Ys = salloc(cx, (long long)KM * n);
+  if (Ys) {
+    for (int l = threadIdx.x; l < n; l += NT)
+#pragma unroll
+      for (int a = 0; a < KM; ++a) Ys[a + KM * l] = a < k ? Bt[l + (long long)a * ldbt] : 0.0;
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < n; i += NT) {
+    double z[KM];
+    const double ti = taus[i];
+    for (int j = 0; j < i; ++j) T[i + (long long)j * ldt] = 0.0;
+    T[i + (long long)i * ldt] = ti;
+#pragma unroll
+    for (int a = 0; a < KM; ++a)
+      z[a] = ti * (Ys ? Ys[a + KM * i] : (a < k ? Bt[i + (long long)a * ldbt] : 0.0));
+    for (int j = i + 1; j < n; ++j) {
+      double y[KM];
+#pragma unroll
+      for (int a = 0; a < KM; ++a) y[a] = Ys ? Ys[a + KM * j] : (a < k ? Bt[j + (long long)a * ldbt] : 0.0);
+      double dot = 0.0;
+#pragma unroll
+      for (int a = 0; a < KM; ++a) dot = fma(z[a], y[a], dot);
+      const double t = -taus[j] * dot;
+      T[i + (long long)j * ldt] = t;
+#pragma unroll
+      for (int a = 0; a < KM; ++a) z[a] = fma(t, y[a], z[a]);
+    }
+  }
+  __syncthreads();
+  release(cx, mk);
+}
+
 }  // namespace blr

@@ -127,11 +127,17 @@ __device__ void tiled_update(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf,
     if (r == 0) {  // tp_qr with an empty bottom: identity reflector (kernels.py:146-147)
       zero_mat(b, b, T, b);
     } else {
-      double* B = alloc(cx, (long long)r * b);
-      if (!B) return;
-      transpose_mat(b, r, x.v, x.ld, B, r);          // B = V_ik^T (r x b)
-      tpqrt(cx, b, r, rk.u, rk.ld, B, r, T, b);
-      transpose_mat(r, b, B, r, x.v, x.ld);          // Ytilde.v = Y^T stored in the V slab
+      if (r <= 16 && b <= 2 * NT) {
+        tpqrt_small<16>(cx, b, r, rk.u, rk.ld, x.v, x.ld, T, b);  // B^T = V in place -> Y^T
+      } else if (r <= 32 && b <= 2 * NT) {
+        tpqrt_small<32>(cx, b, r, rk.u, rk.ld, x.v, x.ld, T, b);
+      } else {
+        double* B = alloc(cx, (long long)r * b);
+        if (!B) return;
+        transpose_mat(b, r, x.v, x.ld, B, r);          // B = V_ik^T (r x b)
+        tpqrt(cx, b, r, rk.u, rk.ld, B, r, T, b);
+        transpose_mat(r, b, B, r, x.v, x.ld);          // Ytilde.v = Y^T stored in the V slab
+      }
       add_flops(cx, FK_UPDATE_QR, qr_cost(b + r, b) + tgen_cost(b + r, b));
     }
     if (threadIdx.x == 0) { rf.yrank[c] = r; *x.rank = 0; }
@@ -188,13 +194,15 @@ __device__ void tiled_trap_a(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf,
   Blk w = blk_dense_times(cx, T, b, true, ssum);
   t2.stop(cx, PH_PRODUCT);
   const long long cw = (long long)i * g.q + j;
-  double* wu = rf.wpool + cw * 2 * b * b;
-  double* wv = wu + (long long)b * b;
+  double* wu = rf.wpool + cw * rf.wslot;
+  double* wv = wu + rf.wslot / 2;
   if (w.lr) {
+    if ((long long)b * w.rank > rf.wslot / 2) set_status(cx, ST_RANK_OVERFLOW);
     copy_mat(b, w.rank, w.u, w.ldu, wu, b);
     copy_mat(b, w.rank, w.v, w.ldv, wv, b);
     if (threadIdx.x == 0) rf.wrank[cw] = w.rank;
   } else {
+    if ((long long)b * b > rf.wslot) set_status(cx, ST_RANK_OVERFLOW);
     copy_mat(b, b, w.u, w.ldu, wu, b);
     if (threadIdx.x == 0) rf.wrank[cw] = -1;
   }
@@ -209,9 +217,9 @@ __device__ void tiled_trap_b(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf,
   const int b = g.b;
   const Blk yt = refl_blk(g, rf, i, k);
   const long long cw = (long long)i * g.q + j;
-  double* wu = rf.wpool + cw * 2 * b * b;
+  double* wu = rf.wpool + cw * rf.wslot;
   const int wr = rf.wrank[cw];
-  const Blk w = wr >= 0 ? make_lr(b, b, wr, wu, b, wu + (long long)b * b, b, 1.0) : make_dense(b, b, wu, b, 1.0);
+  const Blk w = wr >= 0 ? make_lr(b, b, wr, wu, b, wu + rf.wslot / 2, b, 1.0) : make_dense(b, b, wu, b, 1.0);
   PhaseTimer t3;
   Blk yw = blk_mul(cx, yt, w);
   t3.stop(cx, PH_PRODUCT);

@@ -153,8 +153,8 @@ class DeviceGrid:
             dt = dense
         adm = np.asarray(admissible, dtype=bool)
         g = cls(m, n, b, adm, cap, min_lr_slab=b * b)
-        if g.cap < int(fallback * b):
-            raise ValueError("cap must be at least dense_fallback_fraction * b")
+        # cap < fallback*b is allowed: a tile whose rank lands in (cap, fallback*b]
+        # raises (rank-overflow status) instead of silently changing kind
         cm = dt if colmajor else dt.t().contiguous()  # column-major m x n, lda = m
         ws, per, nct = rt.workspace(b, g.cap)
         st = g.cstruct()
@@ -197,16 +197,18 @@ class DeviceRefl:
 
     def enable_split_traps(self) -> None:
         """Allocate the per-cell w slots used by the split ApplyTrap tasks of
-        the dynamic scheduler (2*b*b doubles per cell)."""
+        the dynamic scheduler (2*b*cap doubles per cell)."""
         if self.wpool is None:
             g = self.grid
-            self.wpool = torch.empty(g.p * g.q * 2 * g.b * g.b, dtype=torch.float64, device=g.pool.device)
+            self.wslot = 2 * g.b * g.cap
+            self.wpool = torch.empty(g.p * g.q * self.wslot, dtype=torch.float64, device=g.pool.device)
             self.wrank = torch.zeros(g.p * g.q, dtype=torch.int32, device=g.pool.device)
 
     def cstruct(self) -> _lib.Refl:
         return _lib.Refl(self.pool.data_ptr(), self.y_off.data_ptr(), self.t_off.data_ptr(),
                          self.yrank.data_ptr(), self.wpool.data_ptr() if self.wpool is not None else None,
-                         self.wrank.data_ptr() if self.wrank is not None else None)
+                         self.wrank.data_ptr() if self.wrank is not None else None,
+                         getattr(self, "wslot", 0))
 
     def mat(self, off: int, rows: int, cols: int) -> np.ndarray:
         """Download a column-major rows x cols matrix at pool offset ``off``."""

@@ -43,7 +43,7 @@ def main():
     tg = time.perf_counter() - t0
     t0 = time.perf_counter()
     g = DeviceGrid.from_dense(dense, cfg.b, weak_admissibility(n // cfg.b, n // cfg.b), cfg.eps, 0.5,
-                              cap=args.cap, colmajor=True)
+                              cap=args.cap or cfg.cap, colmajor=True)
     torch.cuda.synchronize()
     tc = time.perf_counter() - t0
     del dense
