@@ -50,23 +50,37 @@ __device__ void geqrt_inplace(Ctx& cx, int m, int n, double* A, int lda, double*
   const long long mark = cx.top;
   double* tau = alloc(cx, n);
   double* Tp = alloc(cx, (long long)QR_NB * n);
-  double* S = alloc(cx, (long long)n * n);
-  if (!tau || !Tp || !S) { cx.top = mark; return; }
+  double* X = alloc(cx, (long long)n * QR_NB);
+  double* X2 = alloc(cx, (long long)n * QR_NB);
+  if (!tau || !Tp || !X || !X2) { cx.top = mark; return; }
   qr_blocked(cx, m, n, A, lda, tau, Tp);
   // Y explicit unit-lower-trapezoidal; zero A below the diagonal
   for (int j = threadIdx.x >> 5; j < n; j += NWARP)
     for (int i = threadIdx.x & 31; i < m; i += 32) {
-    const long long e = (long long)j * m + i;
-    double* a = A + i + (long long)j * lda;
-    double y;
-    if (i < j) y = 0.0;
-    else if (i == j) y = 1.0;
-    else { y = *a; *a = 0.0; }
-    Y[i + (long long)j * ldy] = y;
-  }
+      double* a = A + i + (long long)j * lda;
+      double y;
+      if (i < j) y = 0.0;
+      else if (i == j) y = 1.0;
+      else { y = *a; *a = 0.0; }
+      Y[i + (long long)j * ldy] = y;
+    }
   __syncthreads();
-  gemm(true, false, n, n, m, 1.0, Y, ldy, Y, ldy, 0.0, S, n);
-  build_t_full(cx, n, S, n, tau, T, ldt);
+  // full forward-columnwise T from the panel T's: T(0:J0, J) = -T(0:J0,0:J0)
+  // (Y(:,0:J0)^T Y(:,J)) T_JJ, where Y(:,J) vanishes above row J0, so the
+  // inner products only run over rows J0..m
+  for (int j0 = 0; j0 < n; j0 += QR_NB) {
+    const int w = min(QR_NB, n - j0);
+    const double* TJ = Tp + (long long)j0 * QR_NB;
+    for (int c = threadIdx.x >> 5; c < w; c += NWARP)
+      for (int i = threadIdx.x & 31; i < n; i += 32)
+        T[i + (long long)(j0 + c) * ldt] = (i >= j0 && i < j0 + w) ? TJ[(i - j0) + c * QR_NB] : 0.0;
+    __syncthreads();
+    if (j0 > 0) {
+      gemm(true, false, j0, w, m - j0, 1.0, Y + j0, ldy, Y + j0 + (long long)j0 * ldy, ldy, 0.0, X, j0);
+      gemm(false, false, j0, w, w, 1.0, X, j0, TJ, QR_NB, 0.0, X2, j0);
+      gemm(false, false, j0, w, j0, -1.0, T, ldt, X2, j0, 0.0, T + (long long)j0 * ldt, ldt);
+    }
+  }
   add_flops(cx, FK_PANEL_QR, qr_cost(m, n) + tgen_cost(m, n));
   cx.top = mark;
 }

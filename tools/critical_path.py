@@ -14,7 +14,7 @@ from paper_2208_06194_b200.lowrank import ToleranceConfig
 name = sys.argv[1] if len(sys.argv) > 1 else "C3"
 cfg = configs.CONFIGS[name]
 dense = configs.dense_device(cfg)
-g = DeviceGrid.from_dense(dense, cfg.b, weak_admissibility(cfg.n // cfg.b, cfg.n // cfg.b), cfg.eps, 0.5, colmajor=True)
+g = DeviceGrid.from_dense(dense, cfg.b, weak_admissibility(cfg.n // cfg.b, cfg.n // cfg.b), cfg.eps, 0.5, cap=cfg.cap, colmajor=True)
 del dense
 tasks, indeg, off, succ, prio = tiled_dag_arrays(g.p, g.q)
 n = len(tasks)
