@@ -206,6 +206,16 @@ int blrqr_mgs_step(const blrqr_grid* a, const blrqr_grid* qg, const blrqr_grid* 
                    double* panel_ws, int64_t panel_doubles, double* ws, int64_t ws_per_cta, int nctas, int* status,
                    unsigned long long* flops, void* stream);
 
+/* ---- Q application and expansion (metrics; factorize.py:295-352, 461-524) */
+/* C (m x nc, column-major, ldc >= m) <- Q C (transpose = 0) or Q^T C, Q the
+ * orthogonal factor stored by a tiled (method 0) or blocked (method 1)
+ * factorization in (g, rf).  Column chunks of 64 are independent CTAs. */
+int blrqr_apply_q(const blrqr_grid* g, const blrqr_refl* rf, int method, double* C, int64_t ldc, int nc,
+                  int transpose, double* ws, int64_t ws_per_cta, int nctas, int* status, unsigned long long* flops,
+                  void* stream);
+/* D (m x n, column-major, ldd >= m) = the grid expanded (blr_to_dense, core.py:192-201). */
+int blrqr_blr_to_dense(const blrqr_grid* g, double* D, int64_t ldd, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

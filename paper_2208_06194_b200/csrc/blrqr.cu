@@ -977,3 +977,154 @@ extern "C" int blrqr_debug_gemm(int ta, int tb, int M, int N, int K, const doubl
   CK(cudaGetLastError());
   return 0;
 }
+
+// ===========================================================================
+// Q application to dense operands + BLR expansion (metrics; factorize.py
+// blocked_apply_q :295-352 / tiled_apply_q :461-524 on ndarray operands).
+// Each CTA owns a 64-column chunk of C and applies every reflector to it in
+// the reference's order; chunks are independent.
+// ===========================================================================
+constexpr int QCW = 64;
+
+// w = op(T)(c_top + Y^T c_bot); c_top -= w; c_bot -= Y w  (_trap_apply_dense)
+__device__ void trap_apply_dense_dev(Ctx& cx, const Blk& yt, const double* T, int b, double* ct, double* cb,
+                                     int ldc, int nc, bool transpose) {
+  const Mark mk = mark(cx);
+  double* S = alloc(cx, (long long)b * nc);
+  double* W = alloc(cx, (long long)b * nc);
+  if (!S || !W) { release(cx, mk); return; }
+  copy_mat(b, nc, ct, ldc, S, b);
+  if (yt.lr) {
+    if (yt.rank > 0) {
+      double* t1 = alloc(cx, (long long)yt.rank * nc);
+      gemm(true, false, yt.rank, nc, b, 1.0, yt.u, yt.ldu, cb, ldc, 0.0, t1, yt.rank);
+      gemm(false, false, b, nc, yt.rank, 1.0, yt.v, yt.ldv, t1, yt.rank, 1.0, S, b);
+    }
+  } else {
+    gemm(true, false, b, nc, b, 1.0, yt.u, yt.ldu, cb, ldc, 1.0, S, b);
+  }
+  gemm(transpose, false, b, nc, b, 1.0, T, b, S, b, 0.0, W, b);
+  for (int j = threadIdx.x >> 5; j < nc; j += NWARP)
+    for (int i = threadIdx.x & 31; i < b; i += 32) ct[i + (long long)j * ldc] -= W[i + (long long)j * b];
+  __syncthreads();
+  if (yt.lr) {
+    if (yt.rank > 0) {
+      double* t2 = alloc(cx, (long long)yt.rank * nc);
+      gemm(true, false, yt.rank, nc, b, 1.0, yt.v, yt.ldv, W, b, 0.0, t2, yt.rank);
+      gemm(false, false, b, nc, yt.rank, -1.0, yt.u, yt.ldu, t2, yt.rank, 1.0, cb, ldc);
+    }
+  } else {
+    gemm(false, false, b, nc, b, -1.0, yt.u, yt.ldu, W, b, 1.0, cb, ldc);
+  }
+  release(cx, mk);
+}
+
+__global__ void __launch_bounds__(NT, 1) k_apply_q(blrqr_grid g, blrqr_refl rf, int method, double* C, long long ldc,
+                                                   int nc, int transpose, double* ws, long long wsp, int* status,
+                                                   unsigned long long* flops) {
+  Ctx cx = make_ctx(ws, wsp, status, flops);
+  const int b = g.b, p = g.p, q = g.q;
+  for (int c0 = blockIdx.x * QCW; c0 < nc; c0 += gridDim.x * QCW) {
+    const int w = min(QCW, nc - c0);
+    double* Cc = C + (long long)c0 * ldc;
+    auto rows = [&](int i) { return Cc + (long long)i * b; };
+    if (method == 0) {  // tiled (factorize.py:508-523)
+      auto diag = [&](int k) {
+        const long long c = (long long)k * q + k;
+        apply_wy_dev(cx, b, b, w, rf.pool + rf.y_off[c], b, rf.pool + rf.t_off[c], b, rows(k), (int)ldc,
+                     transpose != 0);
+      };
+      if (transpose) {
+        for (int k = 0; k < q; ++k) {
+          diag(k);
+          for (int i = k + 1; i < p; ++i)
+            trap_apply_dense_dev(cx, refl_blk(g, rf, i, k), rf.pool + rf.t_off[(long long)i * q + k], b, rows(k),
+                                 rows(i), (int)ldc, w, true);
+        }
+      } else {
+        for (int k = q - 1; k >= 0; --k) {
+          for (int i = p - 1; i > k; --i)
+            trap_apply_dense_dev(cx, refl_blk(g, rf, i, k), rf.pool + rf.t_off[(long long)i * q + k], b, rows(k),
+                                 rows(i), (int)ldc, w, false);
+          diag(k);
+        }
+      }
+    } else {  // blocked (factorize.py:295-323, 343-350)
+      for (int kk = 0; kk < q; ++kk) {
+        const int k = transpose ? kk : q - 1 - kk;
+        const Mark mk = mark(cx);
+        double* acc = alloc(cx, (long long)b * w);
+        double* z = alloc(cx, (long long)b * w);
+        if (!acc || !z) return;
+        zero_mat(b, w, acc, b);
+        for (int i = k; i < p; ++i) {
+          const Blk y = (i == k) ? make_dense(b, b, rf.pool + rf.y_off[(long long)k * q + k], b) : refl_blk(g, rf, i, k);
+          if (y.lr) {
+            if (y.rank == 0) continue;
+            double* t1 = alloc(cx, (long long)y.rank * w);
+            gemm(true, false, y.rank, w, b, 1.0, y.u, y.ldu, rows(i), (int)ldc, 0.0, t1, y.rank);
+            gemm(false, false, b, w, y.rank, 1.0, y.v, y.ldv, t1, y.rank, 1.0, acc, b);
+          } else {
+            gemm(true, false, b, w, b, 1.0, y.u, y.ldu, rows(i), (int)ldc, 1.0, acc, b);
+          }
+        }
+        gemm(transpose != 0, false, b, w, b, 1.0, rf.pool + rf.t_off[(long long)k * q + k], b, acc, b, 0.0, z, b);
+        for (int i = k; i < p; ++i) {
+          const Blk y = (i == k) ? make_dense(b, b, rf.pool + rf.y_off[(long long)k * q + k], b) : refl_blk(g, rf, i, k);
+          if (y.lr) {
+            if (y.rank == 0) continue;
+            double* t2 = alloc(cx, (long long)y.rank * w);
+            gemm(true, false, y.rank, w, b, 1.0, y.v, y.ldv, z, b, 0.0, t2, y.rank);
+            gemm(false, false, b, w, y.rank, -1.0, y.u, y.ldu, t2, y.rank, 1.0, rows(i), (int)ldc);
+          } else {
+            gemm(false, false, b, w, b, -1.0, y.u, y.ldu, z, b, 1.0, rows(i), (int)ldc);
+          }
+        }
+        release(cx, mk);
+      }
+    }
+    cx.top = 0;
+    cx.stop = 0;
+    __syncthreads();
+  }
+}
+
+// dense D (m x n, column-major, ldd) = expanded grid
+__global__ void __launch_bounds__(NT, 1) k_blr_to_dense(blrqr_grid g, double* D, long long ldd) {
+  const int b = g.b;
+  for (int c = blockIdx.x; c < g.p * g.q; c += gridDim.x) {
+    const int i = c / g.q, j = c % g.q;
+    double* d = D + (long long)i * b + (long long)j * b * ldd;
+    if (g.lowrank[c]) {
+      const int r = g.rank[c];
+      if (r > 0)
+        gemm(false, true, b, b, r, 1.0, g.pool + g.off_u[c], b, g.pool + g.off_v[c], b, 0.0, d, (int)ldd);
+      else
+        zero_mat(b, b, d, (int)ldd);
+    } else {
+      copy_mat(b, b, g.pool + g.off_u[c], b, d, (int)ldd);
+    }
+  }
+}
+
+extern "C" int blrqr_apply_q(const blrqr_grid* g, const blrqr_refl* rf, int method, double* C, int64_t ldc, int nc,
+                             int transpose, double* ws, int64_t ws_per_cta, int nctas, int* status,
+                             unsigned long long* flops, void* stream) {
+  if (!g || !rf || method < 0 || method > 1 || nc < 0 || ldc < (int64_t)g->p * g->b) return -1;
+  if (nc == 0) return 0;
+  INIT_KERNELS();
+  cudaFuncSetAttribute(k_apply_q, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  const int chunks = (nc + QCW - 1) / QCW;
+  k_apply_q<<<std::min(chunks, nctas), NT, SMEM_BYTES, as_stream(stream)>>>(*g, *rf, method, C, ldc, nc, transpose,
+                                                                            ws, ws_per_cta, status, flops);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+extern "C" int blrqr_blr_to_dense(const blrqr_grid* g, double* D, int64_t ldd, void* stream) {
+  if (!g || ldd < (int64_t)g->p * g->b) return -1;
+  cudaFuncSetAttribute(k_blr_to_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  k_blr_to_dense<<<std::min(g->p * g->q, 4096), NT, SMEM_BYTES, as_stream(stream)>>>(*g, D, ldd);
+  CK(cudaGetLastError());
+  return 0;
+}

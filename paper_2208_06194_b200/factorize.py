@@ -285,9 +285,49 @@ def blocked_mgs_qr(a: BlrMatrix, cfg: ToleranceConfig) -> FactorizationResult:
     return _host_entry("mgs", a, cfg)
 
 
-def blocked_apply_q(result, c, transpose, cfg=None):  # pragma: no cover - next round
-    raise NotImplementedError("GPU apply-Q (SURVEY §8f row 1) is not built yet")
+def _apply_q_dense(result, c: np.ndarray, transpose: bool, method: str) -> np.ndarray:
+    """Q (or Q^T) times a dense host operand, on the GPU."""
+    from .metrics import _upload_reflectors
+
+    rt = _lib.runtime()
+    m = result.r.structure.m
+    if c.ndim != 2 or c.shape[0] != m:
+        raise ValueError(f"operand has {c.shape[0]} rows, expected {m}")
+    f = DeviceFactorization.__new__(DeviceFactorization)
+    f.method, f.rt = method, rt
+    f.g = DeviceGrid.from_host(result.r)
+    f.rf = DeviceRefl(f.g)
+    _upload_reflectors(f, result)
+    nc = c.shape[1]
+    ct = torch.from_numpy(np.ascontiguousarray(np.asarray(c, dtype=np.float64).T)).to(rt.dev)
+    ws, per, nct = rt.workspace(f.g.b, f.g.cap)
+    gs, rs = f.g.cstruct(), f.rf.cstruct()
+    _lib.check(rt.lib.blrqr_apply_q(C.byref(gs), C.byref(rs), 0 if method == "tiled-hh" else 1, ct.data_ptr(), m,
+                                    nc, int(transpose), ws, per, nct, rt.status.data_ptr(), rt.flops.data_ptr(),
+                                    _lib.stream_ptr()), "apply_q")
+    rt.harvest()
+    return np.ascontiguousarray(ct.cpu().numpy().T)
 
 
-def tiled_apply_q(result, c, transpose, cfg=None):  # pragma: no cover - next round
-    raise NotImplementedError("GPU apply-Q (SURVEY §8f row 1) is not built yet")
+def blocked_apply_q(result, c, transpose, cfg=None):
+    """factorize.py:326-361 for dense operands (GPU).  Block low-rank operands
+    are not supported on the device path (they are not on the factorization
+    path)."""
+    if result.q_columns is None:
+        raise ValueError("result does not carry blocked reflector columns")
+    if not isinstance(c, np.ndarray):
+        if cfg is None:
+            raise ValueError("block low-rank operands need a tolerance config")
+        raise NotImplementedError("BLR operands for apply-Q are not built on the GPU path")
+    return _apply_q_dense(result, c, transpose, "blocked-hh")
+
+
+def tiled_apply_q(result, c, transpose, cfg=None):
+    """factorize.py:495-568 for dense operands (GPU)."""
+    if result.q_tiles is None:
+        raise ValueError("result does not carry tiled reflectors")
+    if not isinstance(c, np.ndarray):
+        if cfg is None:
+            raise ValueError("block low-rank operands need a tolerance config")
+        raise NotImplementedError("BLR operands for apply-Q are not built on the GPU path")
+    return _apply_q_dense(result, c, transpose, "tiled-hh")

@@ -190,3 +190,27 @@ def test_distributed_gpu_store_emulated_ranks(pk, world):
         for c in np.nonzero(ref.rf.t_off_host >= 0)[0]:
             t0 = int(ref.rf.t_off_host[c])
             assert torch.equal(st.rf.pool[t0:t0 + b * b], ref.rf.pool[t0:t0 + b * b])
+
+
+@pytest.mark.parametrize("tag", ["rand256", "lap512", "C1"])
+@pytest.mark.parametrize("method", ["tiled-hh", "blocked-hh", "mgs"])
+def test_gpu_metrics_match_oracle(pk, tag, method):
+    """GPU apply-Q + Res/Orth (no n <= 8192 guard) against the oracle's
+    materialize_q / metrics on the same factorization result."""
+    from paper_2208_06194_b200 import metrics as pm
+    from paper_2208_06194_b200.scheduler import execute_sequential
+    z, meta, dense = _input(tag)
+    n, b, eps = meta["n"], meta["b"], meta["eps"]
+    g = schedule.dense_to_blr(dense, b, oblr.weak_map(n // b, n // b), eps)
+    res = execute_sequential(method, _to_pkg(pk, g), pk.ToleranceConfig(eps))
+    rep = pm.compute_metrics(dense, res, eps)
+    ores, oorth = oalg.res_orth(dense, _oracle_state(pk, res, g, eps))
+    assert abs(rep.res - ores) <= 1e-3 * ores + 1e-15, (rep.res, ores)
+    assert abs(rep.orth - oorth) <= 1e-3 * oorth + 1e-15, (rep.orth, oorth)
+    mm = meta["methods"][method]
+    assert rep.res <= max(10 * mm["res"], 10 * eps) and rep.orth <= max(10 * mm["orth"], 10 * eps)
+    if method != "mgs":  # Q^T (Q c) == c through the drop-in apply-Q API
+        cmat = np.random.default_rng(1).standard_normal((n, 5))
+        fn = pk.factorize.tiled_apply_q if method == "tiled-hh" else pk.factorize.blocked_apply_q
+        back = fn(res, fn(res, cmat, False), True)
+        assert np.linalg.norm(back - cmat) <= 1e-12 * np.linalg.norm(cmat)
