@@ -114,9 +114,12 @@ __device__ __forceinline__ void jac_dots(const double* gp, const double* gq, int
 __device__ __forceinline__ bool jac_angle(double a, double b, double g, double tol2, double& c, double& s) {
   if (g == 0.0 || a == 0.0 || b == 0.0) return false;
   if (g * g <= tol2 * a * b) return false;
-  const double zeta = (b - a) / (2.0 * g);
-  const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-  c = 1.0 / sqrt(1.0 + t * t);
+  // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (b - a) / (2g), written
+  // with one sqrt and one division: t = 2g / (d + sign(d) sqrt(d^2 + 4g^2))
+  const double d = b - a;
+  const double h = sqrt(fma(d, d, 4.0 * g * g));
+  const double t = (2.0 * g) / (d + copysign(h, d));
+  c = rsqrt(fma(t, t, 1.0));
   s = c * t;
   return true;
 }
