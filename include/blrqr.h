@@ -177,6 +177,10 @@ int64_t blrqr_tiled_dag_size(int p, int q, int64_t* nedges);
 /* Debug: record (start ns, end ns, SM id) per task of subsequent dynamic runs
  * into a device buffer of 3*ntasks int64 (NULL disables). */
 void blrqr_debug_trace(void* dev_buf);
+/* CTA teams in the dynamic scheduler (default on): idle CTAs join the
+ * one-sided Jacobi of large rounded-addition cores.  The rotation sequence
+ * is the single-CTA one, so results do not depend on this switch. */
+void blrqr_set_teams(int enable);
 /* Debug: `ctas` CTAs each run `reps` CTA-level GEMMs C = op(A) op(B) (+ C). */
 int blrqr_debug_gemm(int ta, int tb, int M, int N, int K, const double* A, int lda, const double* B, int ldb,
                      double* C, int ldc, int reps, int ctas, void* stream);

@@ -4,7 +4,7 @@
 // addition (Alg. 6); writes are coerced to the structural kind of the target
 // cell.  All routines are CTA-cooperative.
 #pragma once
-#include "svd_rrqr.cuh"
+#include "team.cuh"
 
 namespace blr {
 
@@ -181,7 +181,8 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
   __syncthreads();
   if (in_smem(cx, W2) && in_smem(cx, J))
     jacobi_smem(cx, kp, kp, W2, J, sig, perm, cx.flops);  // shared-space loads, 2 pairs per warp
-  else if (kp <= 32 || !jacobi_blocked(cx, kp, kp, W2, kp, J, kp, sig, perm, cx.flops))
+  else if (kp <= 32 || (!team_jacobi_lead(cx, kp, kp, W2, kp, J, kp, sig, perm) &&
+                        !jacobi_blocked(cx, kp, kp, W2, kp, J, kp, sig, perm, cx.flops)))
     jacobi_cols(kp, kp, W2, kp, J, kp, sig, perm, cx.flops);
   ts.stop(cx, PH_SVD);
   // (4) truncation (lowrank.py:204-213); the dropped QRCP remainder rem2

@@ -385,6 +385,7 @@ struct DagDev {
   int* q[2];
   int* ctr;  // [0] head hi, [1] tail hi, [2] head lo, [3] tail lo, [4] done
   long long* trace;  // optional: per task (start ns, end ns, sm id)
+  TeamCtx* team;     // optional: CTA teams for large Jacobi cores (team.cuh)
 };
 
 __device__ __forceinline__ long long global_ns() {
@@ -405,13 +406,23 @@ __global__ void __launch_bounds__(NT, 1) k_tiled_dag(DagDev d, blrqr_grid g, blr
                                                      long long wsp, int* status, unsigned long long* flops,
                                                      long long timeout_cycles) {
   Ctx cx = make_ctx(ws, wsp, status, flops);
-  __shared__ int s_task;
+  cx.team = d.team;
+  __shared__ int s_task, s_member;
   while (true) {
     if (threadIdx.x == 0) {
       int t = -1;
       const long long t0 = sm_clock();
       while (true) {
         bool got = false;
+        if (d.team) {  // help a running team job first: it is on the critical path
+          int member;
+          const int slot = team_try_join(d.team, &member);
+          if (slot >= 0) {
+            t = -2 - slot;
+            s_member = member;
+            break;
+          }
+        }
         for (int c = 0; c < 2 && !got; ++c) {
           const int h = ld_volatile(d.ctr + 2 * c);
           const int tl = ld_volatile(d.ctr + 2 * c + 1);
@@ -436,8 +447,15 @@ __global__ void __launch_bounds__(NT, 1) k_tiled_dag(DagDev d, blrqr_grid g, blr
     }
     __syncthreads();
     const int t = s_task;
-    if (t < 0) break;
+    if (t == -1) break;
     __threadfence();
+    if (t < -1) {
+      team_help(cx, d.team, -2 - t, s_member);
+      cx.top = 0;
+      cx.stop = 0;
+      __syncthreads();
+      continue;
+    }
     const blrqr_task tk = d.tasks[t];
     if (d.trace && threadIdx.x == 0) d.trace[3 * (long long)t] = global_ns();
     PhaseTimer tt;
@@ -830,6 +848,9 @@ static void tiled_dag_host(int p, int q, std::vector<blrqr_task>& tasks, std::ve
 static long long* g_dag_trace = nullptr;
 void blrqr_debug_trace(void* dev_buf) { g_dag_trace = reinterpret_cast<long long*>(dev_buf); }
 
+static int g_teams_enabled = 1;
+void blrqr_set_teams(int enable) { g_teams_enabled = enable ? 1 : 0; }
+
 int64_t blrqr_tiled_dag_size(int p, int q, int64_t* nedges) {
   if (q < 1 || p < q) return -1;
   std::vector<blrqr_task> tasks;
@@ -877,13 +898,36 @@ int blrqr_tiled_run_dag(const blrqr_grid* g, const blrqr_refl* rf, int ntasks, c
   d.q[1] = work_dev + 2 * (int64_t)ntasks;
   d.ctr = work_dev + 3 * (int64_t)ntasks;
   d.trace = g_dag_trace;
+  int dev = 0, clk_khz = 1965000;
+  cudaGetDevice(&dev);
+  d.team = nullptr;
+  if (g_teams_enabled && dev >= 0 && dev < 16) {
+    // one team-job table + ticket ring per device, allocated once, reset per run
+    static TeamCtx* team_buf[16] = {};
+    static TeamCtx team_host[16];
+    const size_t jobs_b = sizeof(TeamJob) * TEAM_JOBS, tick_b = sizeof(int) * (size_t)TEAM_TICKETS;
+    if (!team_buf[dev]) {
+      char* p = nullptr;
+      CK(cudaMalloc(&p, sizeof(TeamCtx) + 256 + jobs_b + tick_b + 256));
+      TeamCtx& h = team_host[dev];
+      h.jobs = reinterpret_cast<TeamJob*>(p + 256);
+      h.tickets = reinterpret_cast<int*>(p + 256 + jobs_b);
+      h.tk = reinterpret_cast<int*>(p + 256 + jobs_b + tick_b);
+      h.tk_cap = TEAM_TICKETS;
+      CK(cudaMemcpy(p, &h, sizeof(TeamCtx), cudaMemcpyHostToDevice));
+      team_buf[dev] = reinterpret_cast<TeamCtx*>(p);
+    }
+    const TeamCtx& h = team_host[dev];
+    CK(cudaMemsetAsync(h.jobs, 0, jobs_b, st));
+    CK(cudaMemsetAsync(h.tickets, 0xFF, tick_b, st));
+    CK(cudaMemsetAsync(h.tk, 0, 256, st));
+    d.team = team_buf[dev];
+  }
   CK(cudaMemcpyAsync(d.indeg, indeg0_dev, sizeof(int) * ntasks, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemsetAsync(d.q[0], 0xFF, sizeof(int) * 2 * (size_t)ntasks, st));
   CK(cudaMemsetAsync(d.ctr, 0, sizeof(int) * 8, st));
   k_dag_init<<<1, 256, 0, st>>>(d);
   CK(cudaGetLastError());
-  int dev = 0, clk_khz = 1965000;
-  cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev);
   const long long timeout_cycles = (long long)(timeout_s * clk_khz * 1e3);
   k_tiled_dag<<<nctas, NT, SMEM_BYTES, st>>>(d, *g, *rf, eps, ws, ws_per_cta, status, flops, timeout_cycles);

@@ -29,6 +29,8 @@ enum FlopKind : int {
   FK_APPLY_WY, FK_UPDATE_QR, FK_APPLY_TP, FK_COUNT
 };
 
+struct TeamCtx;
+
 struct Ctx {
   double* base;            // this CTA's global (L2/HBM) arena
   long long cap;           // doubles
@@ -37,6 +39,7 @@ struct Ctx {
   int scap, stop;          // doubles
   int* status;             // global status word
   unsigned long long* flops;  // FK_COUNT counters (global)
+  TeamCtx* team;           // CTA teams (dynamic scheduler only), else nullptr
 };
 
 // dynamic shared-memory arena per CTA (doubles): one 512-thread CTA per SM

@@ -30,6 +30,7 @@ __device__ __forceinline__ Ctx make_ctx(double* ws, long long ws_per_cta, int* s
   c.stop = 0;
   c.status = status;
   c.flops = flops;
+  c.team = nullptr;
   return c;
 }
 

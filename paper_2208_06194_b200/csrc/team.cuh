@@ -1,0 +1,301 @@
+// CTA teams inside the persistent dynamic scheduler.
+//
+// The tiled DAG's makespan is its critical path (tools/critical_path.py):
+// chains of large-rank rounded additions, each dominated by the one-sided
+// Jacobi SVD of its core, while most SMs sit idle.  A CTA that meets a core
+// too large for its shared memory posts a *team job*; idle CTAs of the
+// persistent kernel (which poll a ticket ring before the task queues) join
+// it, and the team runs jacobi_blocked's block Jacobi in parallel: the block
+// pairs of one round-robin round touch disjoint columns, so member t takes
+// pairs t, t+T, ... of each round and a team barrier separates rounds.  The
+// rotation sequence is therefore exactly the single-CTA jacobi_blocked one
+// (same block size, same rounds, same inner sweeps): results are bitwise
+// independent of how many helpers turned up, and equal to the level
+// scheduler's.
+//
+// Safety: the leader waits a bounded time for helpers and then closes the
+// job (the join word carries a generation tag and a closed bit, so stale or
+// late helpers leave without being counted); only counted members take part
+// in barriers, and every spin has a timeout that raises ST_SCHED_TIMEOUT.
+// Cross-CTA data is read with ld.global.cg (L2) after a fence.
+#pragma once
+#include "svd_rrqr.cuh"
+
+namespace blr {
+
+constexpr int TEAM_MAX = 16;  // members including the leader
+constexpr int TEAM_JOBS = 128;
+constexpr int TEAM_TICKETS = 1 << 20;
+constexpr int TEAM_CLOSED = 0x8000;
+constexpr long long TEAM_WAIT_CYCLES = 40000;           // leader's wait for helpers (~20 us)
+constexpr long long TEAM_SPIN_TIMEOUT = 20000000000LL;  // ~10 s of spinning -> abort
+
+struct __align__(128) TeamJob {
+  int state;  // 0 free, 9 being set up, 2 running (team size published)
+  int gen;
+  int join;   // (gen & 0x7fff) << 16 | closed bit | count
+  int team;
+  int bar_count;
+  int bar_gen;
+  int rot[3];
+  int done;
+  int rows, ncols, ldx, ldj, jb;
+  double* X;
+  double* J;
+};
+
+struct TeamCtx {
+  TeamJob* jobs;  // TEAM_JOBS
+  int* tickets;   // ring of slot << 16 | (gen & 0x7fff), -1 = not yet written
+  int* tk;        // [0] head, [1] tail
+  int tk_cap;
+};
+
+__device__ __forceinline__ int vload(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+
+__device__ __forceinline__ bool team_spin_ok(Ctx& cx, long long t0) {
+  if (sm_clock() - t0 > TEAM_SPIN_TIMEOUT) {
+    atomicOr(cx.status, ST_SCHED_TIMEOUT);
+    return false;
+  }
+  return true;
+}
+
+// barrier across the counted members (all threads of each member call it)
+__device__ void team_barrier(Ctx& cx, TeamJob* job, int team) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int g = vload(&job->bar_gen);
+    if (atomicAdd(&job->bar_count, 1) == team - 1) {
+      job->bar_count = 0;
+      __threadfence();
+      atomicAdd(&job->bar_gen, 1);
+    } else {
+      const long long t0 = sm_clock();
+      while (vload(&job->bar_gen) == g && team_spin_ok(cx, t0)) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Member t's share of the team Jacobi (jacobi_blocked's rotation sequence).
+__device__ void team_jacobi_member(Ctx& cx, TeamJob* job, int t, int team) {
+  __shared__ int s_rot, s_conv;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rows = job->rows, ncols = job->ncols, ldx = job->ldx, ldj = job->ldj, jb = job->jb;
+  double* X = job->X;
+  double* J = job->J;
+  const Mark mk = mark(cx);
+  double* st = salloc(cx, (long long)2 * jb * (rows + ncols));
+  if (!st) {  // the leader sized jb for its own (fuller) arena; cannot happen
+    if (threadIdx.x == 0) atomicOr(cx.status, ST_ARENA_OVERFLOW);
+    st = cx.sbase;
+  }
+  double* Xs = as_smem(cx, st);
+  double* Js = Xs + 2 * jb * rows;
+  const double tol = 2.220446049250313e-16 * (double)max(rows, 1);
+  const double tol2 = tol * tol;
+  const int nb = (ncols + jb - 1) / jb;
+  const int nbe = (nb + 1) & ~1;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    if (threadIdx.x == 0) s_rot = 0;
+    for (int rnd = 0; rnd < nbe - 1; ++rnd) {
+      for (int bp = t; bp < nbe / 2; bp += team) {
+        int bi, bj;
+        rr_pair(bp, rnd, nbe, bi, bj);
+        if (bj >= nb) continue;
+        const int ni = min(jb, ncols - bi * jb), nj = min(jb, ncols - bj * jb);
+        const int nc = ni + nj;
+        for (int c = warp; c < nc; c += NWARP) {
+          const int gc = c < ni ? bi * jb + c : bj * jb + (c - ni);
+          const double* xg = X + (long long)gc * ldx;
+          const double* jg = J + (long long)gc * ldj;
+          for (int i = lane; i < rows; i += 32) Xs[i + c * rows] = __ldcg(xg + i);
+          for (int i = lane; i < ncols; i += 32) Js[i + c * ncols] = __ldcg(jg + i);
+        }
+        __syncthreads();
+        const int kk = (nc + 1) & ~1;
+        for (int r2 = 0; r2 < kk - 1; ++r2) {
+          for (int pi = warp; pi < kk / 2; pi += NWARP) {
+            int p, q;
+            rr_pair(pi, r2, kk, p, q);
+            if (q >= nc) continue;
+            double a, b, g;
+            jac_dots(Xs + p * rows, Xs + q * rows, rows, lane, a, b, g);
+            a = warp_sum(a);
+            b = warp_sum(b);
+            g = warp_sum(g);
+            double cs, sn;
+            if (!jac_angle(a, b, g, tol2, cs, sn)) continue;
+            jac_rotate(Xs + p * rows, Xs + q * rows, rows, lane, cs, sn);
+            jac_rotate(Js + p * ncols, Js + q * ncols, ncols, lane, cs, sn);
+            if (lane == 0) s_rot = 1;
+          }
+          __syncthreads();
+        }
+        for (int c = warp; c < nc; c += NWARP) {
+          const int gc = c < ni ? bi * jb + c : bj * jb + (c - ni);
+          double* xg = X + (long long)gc * ldx;
+          double* jg = J + (long long)gc * ldj;
+          for (int i = lane; i < rows; i += 32) __stcg(xg + i, Xs[i + c * rows]);
+          for (int i = lane; i < ncols; i += 32) __stcg(jg + i, Js[i + c * ncols]);
+        }
+        __syncthreads();
+      }
+      if (rnd == 0 && t == 0 && threadIdx.x == 0) job->rot[(sweep + 2) % 3] = 0;  // all read it last sweep
+      team_barrier(cx, job, team);
+    }
+    // publish this member's rotations, then agree on convergence
+    if (threadIdx.x == 0 && s_rot) atomicOr(&job->rot[sweep % 3], 1);
+    team_barrier(cx, job, team);
+    if (threadIdx.x == 0) s_conv = (vload(&job->rot[sweep % 3]) == 0);
+    __syncthreads();
+    if (t == 0 && threadIdx.x == 0 && cx.flops) atomicAdd(cx.flops + PROF_BASE + PH_JSWEEPS, 1ull);
+    if (s_conv) break;
+  }
+  release(cx, mk);
+}
+
+// Leader side (called from rounded_add inside the dynamic scheduler): X
+// (rows x ncols) and J (ncols x ncols) in the leader's global arena.
+// Returns false when it should run single-CTA instead (jacobi_blocked,
+// bitwise the same result).
+__device__ bool team_jacobi_lead(Ctx& cx, int rows, int ncols, double* X, int ldx, double* J, int ldj, double* sigma,
+                                 int* perm) {
+  __shared__ int s_slot, s_team;
+  TeamCtx* tc = cx.team;
+  if (!tc || in_smem(cx, X) || in_smem(cx, J)) return false;  // other CTAs need global addresses
+  // jacobi_blocked's block size for this arena state
+  int jb = 16;
+  while (jb > 2 && 2 * jb * (rows + ncols) > cx.scap - cx.stop) jb >>= 1;
+  if (2 * jb * (rows + ncols) > cx.scap - cx.stop) return false;
+  const int nb = (ncols + jb - 1) / jb;
+  const int want = min(TEAM_MAX, ((nb + 1) & ~1) / 2);
+  if (want < 2) return false;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    s_slot = -1;
+    for (int s = 0; s < TEAM_JOBS; ++s)
+      if (vload(&tc->jobs[s].state) == 0 && atomicCAS(&tc->jobs[s].state, 0, 9) == 0) {
+        s_slot = s;
+        break;
+      }
+  }
+  __syncthreads();
+  const int slot = s_slot;
+  if (slot < 0) return false;
+  TeamJob* job = tc->jobs + slot;
+  for (int j = warp; j < ncols; j += NWARP)
+    for (int i = lane; i < ncols; i += 32) J[i + (long long)j * ldj] = (i == j) ? 1.0 : 0.0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int gen = (job->gen + 1) & 0x7fff;
+    job->gen = gen;
+    job->team = 0;
+    job->bar_count = 0;
+    job->rot[0] = job->rot[1] = job->rot[2] = 0;
+    job->done = 0;
+    job->rows = rows;
+    job->ncols = ncols;
+    job->ldx = ldx;
+    job->ldj = ldj;
+    job->jb = jb;
+    job->X = X;
+    job->J = J;
+    __threadfence();
+    atomicExch(&job->join, gen << 16);  // open
+    const int ticket = (slot << 16) | gen;
+    for (int h = 1; h < want; ++h) {
+      const int idx = atomicAdd(tc->tk + 1, 1);
+      if (idx < tc->tk_cap) atomicExch(tc->tickets + idx, ticket);
+    }
+    const long long t0 = sm_clock();
+    while ((vload(&job->join) & 0x7fff) < want - 1 && sm_clock() - t0 < TEAM_WAIT_CYCLES) __nanosleep(64);
+    const int got = atomicOr(&job->join, TEAM_CLOSED) & 0x7fff;
+    const int team = 1 + min(got, want - 1);
+    job->team = team;
+    __threadfence();
+    atomicExch(&job->state, 2);
+    s_team = team;
+  }
+  __syncthreads();
+  const int team = s_team;
+  if (team > 1) {
+    if (cx.flops && threadIdx.x == 0) {
+      atomicAdd(cx.flops + 53, 1ull);                      // stats: team jobs
+      atomicAdd(cx.flops + 54, (unsigned long long)team);  //        members
+    }
+    team_jacobi_member(cx, job, 0, team);
+    if (threadIdx.x == 0) {
+      const long long t0 = sm_clock();
+      while (vload(&job->done) < team - 1 && team_spin_ok(cx, t0)) __nanosleep(64);
+      __threadfence();
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) atomicExch(&job->state, 0);
+  if (team == 1) return false;  // nobody came: single-CTA jacobi_blocked
+  if (cx.flops && threadIdx.x == 0) atomicAdd(cx.flops + PROF_BASE + PH_JCALLS, 1ull);
+  for (int c = warp; c < ncols; c += NWARP) {
+    const double* gc = X + (long long)c * ldx;
+    double a = 0.0;
+    for (int i = lane; i < rows; i += 32) {
+      const double x = __ldcg(gc + i);
+      a = fma(x, x, a);
+    }
+    a = warp_sum(a);
+    if (lane == 0) sigma[c] = sqrt(a);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < ncols; i += NT) {
+    const double si = sigma[i];
+    int r = 0;
+    for (int j = 0; j < ncols; ++j) {
+      const double sj = sigma[j];
+      r += (sj > si) || (sj == si && j < i);
+    }
+    perm[r] = i;
+  }
+  __syncthreads();
+  return true;
+}
+
+// Helper side, thread 0 of an idle CTA: claim a ticket and join its job.
+// Returns the job slot (>= 0) with *member set, or -1.
+__device__ int team_try_join(TeamCtx* tc, int* member) {
+  const int h = vload(tc->tk);
+  const int tl = vload(tc->tk + 1);
+  if (h >= tl || h >= tc->tk_cap) return -1;
+  if (atomicCAS(tc->tk, h, h + 1) != h) return -1;
+  int tk;
+  while ((tk = vload(tc->tickets + h)) < 0) __nanosleep(32);
+  const int slot = tk >> 16, gen = tk & 0x7fff;
+  TeamJob* job = tc->jobs + slot;
+  int w = vload(&job->join);
+  while (true) {
+    if ((w >> 16) != gen || (w & TEAM_CLOSED)) return -1;  // stale ticket or closed
+    const int o = atomicCAS(&job->join, w, w + 1);
+    if (o == w) break;
+    w = o;
+  }
+  const int m = w & 0x7fff;  // counted: the leader's team includes this member
+  while (vload(&job->state) != 2) __nanosleep(32);
+  __threadfence();
+  *member = m + 1;
+  return slot;
+}
+
+__device__ void team_help(Ctx& cx, TeamCtx* tc, int slot, int member) {
+  TeamJob* job = tc->jobs + slot;
+  const int team = vload(&job->team);
+  team_jacobi_member(cx, job, member, team);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(&job->done, 1);
+  }
+}
+
+}  // namespace blr

@@ -143,6 +143,39 @@ def test_dynamic_and_level_schedulers_bitwise_equal(pk, tag):
     assert torch.equal(fa.rf.pool, fb.rf.pool)
 
 
+def test_cta_teams_bitwise_equal_to_single_cta(pk):
+    """CTA teams (team.cuh) replay jacobi_blocked's rotation sequence: an
+    expcov problem whose rounded additions have large cores gives the same
+    bits with teams (dynamic scheduler), without teams, and under the level
+    scheduler (no teams)."""
+    import torch
+    from paper_2208_06194_b200 import _lib, configs
+    from paper_2208_06194_b200.core import weak_admissibility
+    from paper_2208_06194_b200.device import DeviceGrid
+    from paper_2208_06194_b200.factorize import factorize_device
+    cfg = configs.CONFIGS["C3"]
+    n = 8192
+    dense = configs.dense_device(cfg, n)
+    dg = DeviceGrid.from_dense(dense, cfg.b, weak_admissibility(n // cfg.b, n // cfg.b), cfg.eps, colmajor=True)
+    del dense
+    tol = pk.ToleranceConfig(cfg.eps)
+    rt = _lib.runtime()
+    fa = factorize_device("tiled-hh", dg, tol, clone=True, scheduler="dag")
+    jobs = rt.last_stats[5]
+    try:
+        rt.lib.blrqr_set_teams(0)
+        fb = factorize_device("tiled-hh", dg, tol, clone=True, scheduler="dag")
+        assert rt.last_stats[5] == 0
+    finally:
+        rt.lib.blrqr_set_teams(1)
+    fc = factorize_device("tiled-hh", dg, tol, clone=True, scheduler="levels")
+    assert jobs > 0, "no team job formed: the test no longer exercises teams"
+    for f in (fb, fc):
+        assert torch.equal(fa.g.rank, f.g.rank)
+        assert torch.equal(fa.g.pool, f.g.pool)
+        assert torch.equal(fa.rf.pool, f.rf.pool)
+
+
 @pytest.mark.parametrize("world", [1, 2, 3])
 def test_distributed_gpu_store_emulated_ranks(pk, world):
     """The GPU store of the block-cyclic driver, with `world` ranks emulated

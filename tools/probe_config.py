@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--levels", type=int, default=None, help="only run the first L levels")
     ap.add_argument("--profile-levels", action="store_true")
     ap.add_argument("--sched", default="dag")
+    ap.add_argument("--no-teams", action="store_true")
     args = ap.parse_args()
     ge.build()
     from paper_2208_06194_b200 import _lib, configs, flops
@@ -34,6 +35,8 @@ def main():
     from paper_2208_06194_b200.factorize import DeviceFactorization
     from paper_2208_06194_b200.lowrank import ToleranceConfig
 
+    if args.no_teams:
+        _lib.runtime().lib.blrqr_set_teams(0)
     cfg = configs.CONFIGS[args.config]
     n = args.n or cfg.n
     method = args.method or cfg.method
@@ -96,7 +99,8 @@ def main():
                                                          if not k.startswith("jacobi")},
                       "task_seconds_per_sm": ph.get("task", 0) / clk / _lib.runtime().nctas,
                       "jacobi_sweeps_per_call": ph.get("jacobi_sweeps", 0) / max(1, ph.get("jacobi_calls", 1)),
-                      "big_core_stats(k>=64)": {"count": _lib.runtime().last_stats[2], "mean_k": _lib.runtime().last_stats[0] / max(1, _lib.runtime().last_stats[2]), "mean_kp": _lib.runtime().last_stats[1] / max(1, _lib.runtime().last_stats[2]), "sum_k3_over_sum_kp3": _lib.runtime().last_stats[3] / max(1, _lib.runtime().last_stats[4])}}))
+                      "big_core_stats(k>=64)": {"count": _lib.runtime().last_stats[2], "mean_k": _lib.runtime().last_stats[0] / max(1, _lib.runtime().last_stats[2]), "mean_kp": _lib.runtime().last_stats[1] / max(1, _lib.runtime().last_stats[2]), "sum_k3_over_sum_kp3": _lib.runtime().last_stats[3] / max(1, _lib.runtime().last_stats[4])},
+                      "team_jobs": _lib.runtime().last_stats[5], "team_members": _lib.runtime().last_stats[6]}))
     tot = sum(rep.values())
     rr = f.g.rank_map()
     rl = rr[rr >= 0]
