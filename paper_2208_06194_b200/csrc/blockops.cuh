@@ -171,8 +171,16 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
   // (3c) second (unpivoted) QR, X = Q2 R2 -- Drmac-Veselic QR+LQ
   // preconditioning: Jacobi then works on the kp x kp triangle R2
   qr_blocked(cx, k, kp, X, k, tau2, Tp2);
-  double* W2 = alloc_fast(cx, (long long)kq * kq);
-  double* J = alloc_fast(cx, (long long)kq * kq);
+  // W2 and J both in shared memory (jacobi_smem) or both in the global arena,
+  // leaving the shared arena to the block Jacobi's staging (jb = 16 columns)
+  const Mark before_w = mark(cx);
+  double* W2 = salloc(cx, (long long)kq * kq);
+  double* J = W2 ? salloc(cx, (long long)kq * kq) : nullptr;
+  if (!J) {
+    release(cx, before_w);
+    W2 = alloc(cx, (long long)kq * kq);
+    J = alloc(cx, (long long)kq * kq);
+  }
   double* sig = alloc_fast(cx, kq);
   int* perm = reinterpret_cast<int*>(alloc_fast(cx, kq));
   if (!W2 || !J || !sig || !perm) { release(cx, mk); return 0; }

@@ -144,8 +144,10 @@ __device__ void team_jacobi_member(Ctx& cx, TeamJob* job, int t, int team) {
         }
         __syncthreads();
       }
-      if (rnd == 0 && t == 0 && threadIdx.x == 0) job->rot[(sweep + 2) % 3] = 0;  // all read it last sweep
       team_barrier(cx, job, team);
+      // every member has passed this sweep's first barrier, so all have read
+      // the flag of the previous sweep: recycle the one of the sweep after next
+      if (rnd == 0 && t == 0 && threadIdx.x == 0) job->rot[(sweep + 2) % 3] = 0;
     }
     // publish this member's rotations, then agree on convergence
     if (threadIdx.x == 0 && s_rot) atomicOr(&job->rot[sweep % 3], 1);
