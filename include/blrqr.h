@@ -177,6 +177,9 @@ int64_t blrqr_tiled_dag_size(int p, int q, int64_t* nedges);
 /* Debug: record (start ns, end ns, SM id) per task of subsequent dynamic runs
  * into a device buffer of 3*ntasks int64 (NULL disables). */
 void blrqr_debug_trace(void* dev_buf);
+/* Debug: per task of subsequent dynamic runs, 16 uint64 SM-cycle counters
+ * per phase (PHASES in _lib.py) into a zeroed device buffer (NULL disables). */
+void blrqr_debug_phase_trace(void* dev_buf);
 /* CTA teams in the dynamic scheduler (default on): idle CTAs join the
  * one-sided Jacobi of large rounded-addition cores.  The rotation sequence
  * is the single-CTA one, so results do not depend on this switch. */

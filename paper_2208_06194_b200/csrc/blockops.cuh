@@ -75,8 +75,8 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
   PhaseTimer tq;
   double* Uc = alloc(cx, (long long)m * c);
   double* Vc = alloc(cx, (long long)n * c);
-  double* tauU = alloc_fast(cx, c);
-  double* tauV = alloc_fast(cx, c);
+  double* tauU = alloc(cx, c);  // global: a team helper may factor either side
+  double* tauV = alloc(cx, c);
   double* TpU = alloc(cx, (long long)QR_NB * c);
   double* TpV = alloc(cx, (long long)QR_NB * c);
   if (!Uc || !Vc || !tauU || !tauV || !TpU || !TpV) { release(cx, mk); return 0; }
@@ -84,8 +84,26 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
   copy_mat(m, rb, B.u, B.ldu, Uc + (long long)ra * m, m);
   copy_mat(n, ra, A.v, A.ldv, Vc, n, A.s);
   copy_mat(n, rb, B.v, B.ldv, Vc + (long long)ra * n, n, B.s);
-  qr_blocked(cx, m, c, Uc, m, tauU, TpU);
-  qr_blocked(cx, n, c, Vc, n, tauV, TpV);
+  {
+    TeamJob* job = (c >= TEAM_QR2_MIN) ? team_reserve(cx) : nullptr;
+    int team = 1;
+    if (job) {
+      if (threadIdx.x == 0) {
+        job->kind = TK_QR2;
+        job->iv[0] = m; job->iv[1] = n; job->iv[2] = c;
+        job->pv[0] = Uc; job->pv[1] = tauU; job->pv[2] = TpU;
+        job->pv[3] = Vc; job->pv[4] = tauV; job->pv[5] = TpV;
+      }
+      team = team_launch(cx, job, 2);
+    }
+    if (team > 1) {  // helper factors [V_A V_B]
+      team_qr2_member(cx, job, 0);
+      team_finish(cx, job, team);
+    } else {
+      qr_blocked(cx, m, c, Uc, m, tauU, TpU);
+      qr_blocked(cx, n, c, Vc, n, tauV, TpV);
+    }
+  }
   tq.stop(cx, PH_QR);
   PhaseTimer tc;
   const int kU = min(m, c), kV = min(n, c);
@@ -94,7 +112,7 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
   // arena and can be dropped once its reflectors are saved
   double* col2 = alloc_fast(cx, k);
   double* col2o = alloc_fast(cx, k);
-  double* taus = alloc_fast(cx, k);
+  double* taus = alloc(cx, k);  // global: read by back-transform helpers
   int* piv = reinterpret_cast<int*>(alloc_fast(cx, k));
   double* tau2 = alloc_fast(cx, k);
   if (!col2 || !col2o || !taus || !piv || !tau2) { release(cx, mk); return 0; }
@@ -240,15 +258,31 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
     for (int j = threadIdx.x >> 5; j < rank; j += NWARP)
       for (int i = threadIdx.x & 31; i < k; i += 32) Z2[(long long)j * k + i] = i < kp ? W2[i + (long long)perm[j] * kp] : 0.0;
     __syncthreads();
-    apply_reflectors(k, kp, Gr, k, taus, ZU, m, rank);
-    qr_apply(cx, k, kp, X, k, Tp2, Z2, k, rank, false);
-    for (int j = threadIdx.x >> 5; j < rank; j += NWARP)
-      for (int i = threadIdx.x & 31; i < n; i += 32) ZV[(long long)j * n + i] = i < k ? Z2[i + (long long)j * k] : 0.0;
+    // fixed 32-column chunks (team.cuh back_chunk), so a team computes the
+    // same bits as a lone CTA
+    __shared__ int s_iv[9];
+    __shared__ double* s_pv[13];
+    if (threadIdx.x == 0) {
+      const int iv[9] = {m, n, k, kp, kU, kV, lddu, lddv, rank};
+      double* const pv[13] = {Gr, taus, X, Tp2, Uc, TpU, Vc, TpV, ZU, ZV, Z2, du, dv};
+      for (int i = 0; i < 9; ++i) s_iv[i] = iv[i];
+      for (int i = 0; i < 13; ++i) s_pv[i] = pv[i];
+    }
     __syncthreads();
-    qr_apply(cx, m, kU, Uc, m, TpU, ZU, m, rank, false);
-    qr_apply(cx, n, kV, Vc, n, TpV, ZV, n, rank, false);
-    copy_mat(m, rank, ZU, m, du, lddu);
-    copy_mat(n, rank, ZV, n, dv, lddv);
+    const int nch = (rank + BACK_CW - 1) / BACK_CW;
+    TeamJob* job = (nch > 1 && kU >= TEAM_BACK_MIN && !in_smem(cx, du) && !in_smem(cx, dv)) ? team_reserve(cx)
+                                                                                              : nullptr;
+    int team = 1;
+    if (job) {
+      if (threadIdx.x == 0) {
+        job->kind = TK_BACK;
+        for (int i = 0; i < 9; ++i) job->iv[i] = s_iv[i];
+        for (int i = 0; i < 13; ++i) job->pv[i] = s_pv[i];
+      }
+      team = team_launch(cx, job, min(nch, TEAM_MAX));
+    }
+    for (int ch = 0; ch < nch; ch += team) back_chunk(cx, s_iv, s_pv, ch * BACK_CW);
+    if (team > 1) team_finish(cx, job, team);
     add_flops(cx, FK_ROUNDED_ADD, mm_cost(m, kU, rank) + mm_cost(n, kV, rank));
     tb.stop(cx, PH_BACK);
   }

@@ -386,6 +386,7 @@ struct DagDev {
   int* ctr;  // [0] head hi, [1] tail hi, [2] head lo, [3] tail lo, [4] done
   long long* trace;  // optional: per task (start ns, end ns, sm id)
   TeamCtx* team;     // optional: CTA teams for large Jacobi cores (team.cuh)
+  unsigned long long* ptrace;  // optional: per task PH_COUNT phase cycle counters
 };
 
 __device__ __forceinline__ long long global_ns() {
@@ -458,6 +459,7 @@ __global__ void __launch_bounds__(NT, 1) k_tiled_dag(DagDev d, blrqr_grid g, blr
     }
     const blrqr_task tk = d.tasks[t];
     if (d.trace && threadIdx.x == 0) d.trace[3 * (long long)t] = global_ns();
+    cx.tph = d.ptrace ? d.ptrace + 16LL * t : nullptr;
     PhaseTimer tt;
     switch (tk.kind) {
       case 0: tiled_diag(cx, g, rf, tk.k); break;
@@ -847,6 +849,8 @@ static void tiled_dag_host(int p, int q, std::vector<blrqr_task>& tasks, std::ve
 
 static long long* g_dag_trace = nullptr;
 void blrqr_debug_trace(void* dev_buf) { g_dag_trace = reinterpret_cast<long long*>(dev_buf); }
+static unsigned long long* g_phase_trace = nullptr;
+void blrqr_debug_phase_trace(void* dev_buf) { g_phase_trace = reinterpret_cast<unsigned long long*>(dev_buf); }
 
 static int g_teams_enabled = 1;
 void blrqr_set_teams(int enable) { g_teams_enabled = enable ? 1 : 0; }
@@ -898,6 +902,7 @@ int blrqr_tiled_run_dag(const blrqr_grid* g, const blrqr_refl* rf, int ntasks, c
   d.q[1] = work_dev + 2 * (int64_t)ntasks;
   d.ctr = work_dev + 3 * (int64_t)ntasks;
   d.trace = g_dag_trace;
+  d.ptrace = g_phase_trace;
   int dev = 0, clk_khz = 1965000;
   cudaGetDevice(&dev);
   d.team = nullptr;

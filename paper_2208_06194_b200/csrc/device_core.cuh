@@ -40,6 +40,7 @@ struct Ctx {
   int* status;             // global status word
   unsigned long long* flops;  // FK_COUNT counters (global)
   TeamCtx* team;           // CTA teams (dynamic scheduler only), else nullptr
+  unsigned long long* tph;  // debug: this task's PH_COUNT phase cycle row, else nullptr
 };
 
 // dynamic shared-memory arena per CTA (doubles): one 512-thread CTA per SM
@@ -83,7 +84,11 @@ struct PhaseTimer {
   long long t0;
   __device__ __forceinline__ PhaseTimer() : t0(sm_clock()) {}
   __device__ __forceinline__ void stop(Ctx& c, int ph) {
-    if (threadIdx.x == 0 && c.flops) atomicAdd(c.flops + PROF_BASE + ph, (unsigned long long)(sm_clock() - t0));
+    if (threadIdx.x == 0 && c.flops) {
+      const unsigned long long d = (unsigned long long)(sm_clock() - t0);
+      atomicAdd(c.flops + PROF_BASE + ph, d);
+      if (c.tph) c.tph[ph] += d;
+    }
   }
 };
 

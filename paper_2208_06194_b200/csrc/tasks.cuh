@@ -31,6 +31,7 @@ __device__ __forceinline__ Ctx make_ctx(double* ws, long long ws_per_cta, int* s
   c.status = status;
   c.flops = flops;
   c.team = nullptr;
+  c.tph = nullptr;
   return c;
 }
 

@@ -1,23 +1,27 @@
 // CTA teams inside the persistent dynamic scheduler.
 //
 // The tiled DAG's makespan is its critical path (tools/critical_path.py):
-// chains of large-rank rounded additions, each dominated by the one-sided
-// Jacobi SVD of its core, while most SMs sit idle.  A CTA that meets a core
-// too large for its shared memory posts a *team job*; idle CTAs of the
-// persistent kernel (which poll a ticket ring before the task queues) join
-// it, and the team runs jacobi_blocked's block Jacobi in parallel: the block
-// pairs of one round-robin round touch disjoint columns, so member t takes
-// pairs t, t+T, ... of each round and a team barrier separates rounds.  The
-// rotation sequence is therefore exactly the single-CTA jacobi_blocked one
-// (same block size, same rounds, same inner sweeps): results are bitwise
-// independent of how many helpers turned up, and equal to the level
-// scheduler's.
+// chains of large-rank rounded additions while most SMs sit idle.  A CTA
+// running a large rounded addition posts *team jobs* for its parallel
+// stages; idle CTAs of the persistent kernel (which poll a ticket ring before
+// the task queues) join them:
+//   TK_QR2    the two independent QRs of [U_A U_B] and [V_A V_B];
+//   TK_JACOBI jacobi_blocked's block Jacobi of the core: the block pairs of
+//             one round-robin round touch disjoint columns, so member t takes
+//             pairs t, t+T, ... and a team barrier separates rounds;
+//   TK_BACK   the back-transform U_C = Q_U [Q1 J_r; 0], V_C = Q_V [Q2 W_r; 0]
+//             in fixed 32-column chunks, chunk c on member c mod T.
+// Every kind performs exactly the single-CTA operation sequence on the same
+// data partition (jacobi_blocked's rounds, the same column chunks), so the
+// results are bitwise independent of how many helpers turned up, and equal
+// to the level scheduler's (which never forms teams).
 //
 // Safety: the leader waits a bounded time for helpers and then closes the
 // job (the join word carries a generation tag and a closed bit, so stale or
-// late helpers leave without being counted); only counted members take part
-// in barriers, and every spin has a timeout that raises ST_SCHED_TIMEOUT.
-// Cross-CTA data is read with ld.global.cg (L2) after a fence.
+// late helpers leave without being counted); only counted members take part,
+// and every spin has a timeout that raises ST_SCHED_TIMEOUT.  Memory ordering
+// is the scheduler's: release fence before publishing, acquire fence (all
+// threads) before reading another CTA's data.
 #pragma once
 #include "svd_rrqr.cuh"
 
@@ -29,6 +33,11 @@ constexpr int TEAM_TICKETS = 1 << 20;
 constexpr int TEAM_CLOSED = 0x8000;
 constexpr long long TEAM_WAIT_CYCLES = 40000;           // leader's wait for helpers (~20 us)
 constexpr long long TEAM_SPIN_TIMEOUT = 20000000000LL;  // ~10 s of spinning -> abort
+constexpr int BACK_CW = 32;                              // back-transform column chunk
+constexpr int TEAM_QR2_MIN = 64;   // [U_A U_B] width from which the two QRs split
+constexpr int TEAM_BACK_MIN = 64;  // Q_U width from which the back-transform splits
+
+enum TeamKind : int { TK_JACOBI = 1, TK_BACK = 2, TK_QR2 = 3 };
 
 struct __align__(128) TeamJob {
   int state;  // 0 free, 9 being set up, 2 running (team size published)
@@ -39,9 +48,9 @@ struct __align__(128) TeamJob {
   int bar_gen;
   int rot[3];
   int done;
-  int rows, ncols, ldx, ldj, jb;
-  double* X;
-  double* J;
+  int kind;
+  int iv[12];
+  double* pv[16];
 };
 
 struct TeamCtx {
@@ -59,6 +68,84 @@ __device__ __forceinline__ bool team_spin_ok(Ctx& cx, long long t0) {
     return false;
   }
   return true;
+}
+
+// acquire for the whole CTA after thread 0 observed another CTA's release
+__device__ __forceinline__ void cta_acquire() {
+  __syncthreads();
+  __threadfence();
+}
+
+// ---- leader side -----------------------------------------------------------
+// team_reserve -> (thread 0 fills kind/iv/pv) -> team_launch -> work as
+// member 0 -> team_finish.
+__device__ TeamJob* team_reserve(Ctx& cx) {
+  __shared__ int s_slot;
+  TeamCtx* tc = cx.team;
+  if (!tc) return nullptr;
+  if (threadIdx.x == 0) {
+    s_slot = -1;
+    for (int s = 0; s < TEAM_JOBS; ++s)
+      if (vload(&tc->jobs[s].state) == 0 && atomicCAS(&tc->jobs[s].state, 0, 9) == 0) {
+        s_slot = s;
+        break;
+      }
+  }
+  __syncthreads();
+  const int slot = s_slot;
+  __syncthreads();
+  return slot < 0 ? nullptr : tc->jobs + slot;
+}
+
+// Opens the job, posts want-1 tickets, waits (bounded) for helpers, closes.
+// Returns the team size (1 = nobody came; the slot is then already free).
+__device__ int team_launch(Ctx& cx, TeamJob* job, int want) {
+  __shared__ int s_team;
+  TeamCtx* tc = cx.team;
+  __syncthreads();  // the whole CTA's writes of the job's inputs precede the release below
+  if (threadIdx.x == 0) {
+    const int slot = (int)(job - tc->jobs);
+    const int gen = (job->gen + 1) & 0x7fff;
+    job->gen = gen;
+    job->team = 0;
+    job->bar_count = 0;
+    job->rot[0] = job->rot[1] = job->rot[2] = 0;
+    job->done = 0;
+    __threadfence();
+    atomicExch(&job->join, gen << 16);  // open
+    const int ticket = (slot << 16) | gen;
+    for (int h = 1; h < want; ++h) {
+      const int idx = atomicAdd(tc->tk + 1, 1);
+      if (idx < tc->tk_cap) atomicExch(tc->tickets + idx, ticket);
+    }
+    const long long t0 = sm_clock();
+    while ((vload(&job->join) & 0x7fff) < want - 1 && sm_clock() - t0 < TEAM_WAIT_CYCLES) __nanosleep(64);
+    const int got = atomicOr(&job->join, TEAM_CLOSED) & 0x7fff;
+    const int team = 1 + min(got, want - 1);
+    job->team = team;
+    __threadfence();
+    atomicExch(&job->state, team > 1 ? 2 : 0);
+    s_team = team;
+    if (team > 1 && cx.flops) {
+      atomicAdd(cx.flops + 53, 1ull);                      // stats: team jobs
+      atomicAdd(cx.flops + 54, (unsigned long long)team);  //        members
+    }
+  }
+  __syncthreads();
+  const int team = s_team;
+  __syncthreads();
+  return team;
+}
+
+// waits for the helpers' results and frees the slot (team > 1 only)
+__device__ void team_finish(Ctx& cx, TeamJob* job, int team) {
+  if (threadIdx.x == 0) {
+    const long long t0 = sm_clock();
+    while (vload(&job->done) < team - 1 && team_spin_ok(cx, t0)) __nanosleep(64);
+    __threadfence();
+    atomicExch(&job->state, 0);
+  }
+  cta_acquire();
 }
 
 // barrier across the counted members (all threads of each member call it)
@@ -80,13 +167,14 @@ __device__ void team_barrier(Ctx& cx, TeamJob* job, int team) {
   __syncthreads();
 }
 
-// Member t's share of the team Jacobi (jacobi_blocked's rotation sequence).
+// ---- TK_JACOBI ---------------------------------------------------------------
+// iv: rows, ncols, ldx, ldj, jb; pv: X, J
 __device__ void team_jacobi_member(Ctx& cx, TeamJob* job, int t, int team) {
   __shared__ int s_rot, s_conv;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rows = job->rows, ncols = job->ncols, ldx = job->ldx, ldj = job->ldj, jb = job->jb;
-  double* X = job->X;
-  double* J = job->J;
+  const int rows = job->iv[0], ncols = job->iv[1], ldx = job->iv[2], ldj = job->iv[3], jb = job->iv[4];
+  double* X = job->pv[0];
+  double* J = job->pv[1];
   const Mark mk = mark(cx);
   double* st = salloc(cx, (long long)2 * jb * (rows + ncols));
   if (!st) {  // the leader sized jb for its own (fuller) arena; cannot happen
@@ -160,15 +248,12 @@ __device__ void team_jacobi_member(Ctx& cx, TeamJob* job, int t, int team) {
   release(cx, mk);
 }
 
-// Leader side (called from rounded_add inside the dynamic scheduler): X
-// (rows x ncols) and J (ncols x ncols) in the leader's global arena.
-// Returns false when it should run single-CTA instead (jacobi_blocked,
-// bitwise the same result).
+// Team version of jacobi_blocked for X (rows x ncols) / J (ncols x ncols) in
+// the leader's global arena.  Returns false when it should run single-CTA
+// instead (jacobi_blocked: bitwise the same result).
 __device__ bool team_jacobi_lead(Ctx& cx, int rows, int ncols, double* X, int ldx, double* J, int ldj, double* sigma,
                                  int* perm) {
-  __shared__ int s_slot, s_team;
-  TeamCtx* tc = cx.team;
-  if (!tc || in_smem(cx, X) || in_smem(cx, J)) return false;  // other CTAs need global addresses
+  if (!cx.team || in_smem(cx, X) || in_smem(cx, J)) return false;  // other CTAs need global addresses
   // jacobi_blocked's block size for this arena state
   int jb = 16;
   while (jb > 2 && 2 * jb * (rows + ncols) > cx.scap - cx.stop) jb >>= 1;
@@ -176,69 +261,21 @@ __device__ bool team_jacobi_lead(Ctx& cx, int rows, int ncols, double* X, int ld
   const int nb = (ncols + jb - 1) / jb;
   const int want = min(TEAM_MAX, ((nb + 1) & ~1) / 2);
   if (want < 2) return false;
+  TeamJob* job = team_reserve(cx);
+  if (!job) return false;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    s_slot = -1;
-    for (int s = 0; s < TEAM_JOBS; ++s)
-      if (vload(&tc->jobs[s].state) == 0 && atomicCAS(&tc->jobs[s].state, 0, 9) == 0) {
-        s_slot = s;
-        break;
-      }
-  }
-  __syncthreads();
-  const int slot = s_slot;
-  if (slot < 0) return false;
-  TeamJob* job = tc->jobs + slot;
   for (int j = warp; j < ncols; j += NWARP)
     for (int i = lane; i < ncols; i += 32) J[i + (long long)j * ldj] = (i == j) ? 1.0 : 0.0;
   __syncthreads();
   if (threadIdx.x == 0) {
-    const int gen = (job->gen + 1) & 0x7fff;
-    job->gen = gen;
-    job->team = 0;
-    job->bar_count = 0;
-    job->rot[0] = job->rot[1] = job->rot[2] = 0;
-    job->done = 0;
-    job->rows = rows;
-    job->ncols = ncols;
-    job->ldx = ldx;
-    job->ldj = ldj;
-    job->jb = jb;
-    job->X = X;
-    job->J = J;
-    __threadfence();
-    atomicExch(&job->join, gen << 16);  // open
-    const int ticket = (slot << 16) | gen;
-    for (int h = 1; h < want; ++h) {
-      const int idx = atomicAdd(tc->tk + 1, 1);
-      if (idx < tc->tk_cap) atomicExch(tc->tickets + idx, ticket);
-    }
-    const long long t0 = sm_clock();
-    while ((vload(&job->join) & 0x7fff) < want - 1 && sm_clock() - t0 < TEAM_WAIT_CYCLES) __nanosleep(64);
-    const int got = atomicOr(&job->join, TEAM_CLOSED) & 0x7fff;
-    const int team = 1 + min(got, want - 1);
-    job->team = team;
-    __threadfence();
-    atomicExch(&job->state, 2);
-    s_team = team;
+    job->kind = TK_JACOBI;
+    job->iv[0] = rows; job->iv[1] = ncols; job->iv[2] = ldx; job->iv[3] = ldj; job->iv[4] = jb;
+    job->pv[0] = X; job->pv[1] = J;
   }
-  __syncthreads();
-  const int team = s_team;
-  if (team > 1) {
-    if (cx.flops && threadIdx.x == 0) {
-      atomicAdd(cx.flops + 53, 1ull);                      // stats: team jobs
-      atomicAdd(cx.flops + 54, (unsigned long long)team);  //        members
-    }
-    team_jacobi_member(cx, job, 0, team);
-    if (threadIdx.x == 0) {
-      const long long t0 = sm_clock();
-      while (vload(&job->done) < team - 1 && team_spin_ok(cx, t0)) __nanosleep(64);
-      __threadfence();
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) atomicExch(&job->state, 0);
+  const int team = team_launch(cx, job, want);
   if (team == 1) return false;  // nobody came: single-CTA jacobi_blocked
+  team_jacobi_member(cx, job, 0, team);
+  team_finish(cx, job, team);
   if (cx.flops && threadIdx.x == 0) atomicAdd(cx.flops + PROF_BASE + PH_JCALLS, 1ull);
   for (int c = warp; c < ncols; c += NWARP) {
     const double* gc = X + (long long)c * ldx;
@@ -264,7 +301,42 @@ __device__ bool team_jacobi_lead(Ctx& cx, int rows, int ncols, double* X, int ld
   return true;
 }
 
-// Helper side, thread 0 of an idle CTA: claim a ticket and join its job.
+// ---- TK_BACK -----------------------------------------------------------------
+// One 32-column chunk of the rounded addition's back-transform.
+// iv: m, n, k, kp, kU, kV, lddu, lddv, rank
+// pv: Gr, taus, X, Tp2, Uc, TpU, Vc, TpV, ZU, ZV, Z2, du, dv
+__device__ void back_chunk(Ctx& cx, const int* iv, double* const* pv, int c0) {
+  const int m = iv[0], n = iv[1], k = iv[2], kp = iv[3], kU = iv[4], kV = iv[5], lddu = iv[6], lddv = iv[7];
+  const int nc = min(BACK_CW, iv[8] - c0);
+  double* ZU = pv[8] + (long long)c0 * m;
+  double* ZV = pv[9] + (long long)c0 * n;
+  double* Z2 = pv[10] + (long long)c0 * k;
+  apply_reflectors(k, kp, pv[0], k, pv[1], ZU, m, nc);
+  qr_apply(cx, k, kp, pv[2], k, pv[3], Z2, k, nc, false);
+  for (int j = threadIdx.x >> 5; j < nc; j += NWARP)
+    for (int i = threadIdx.x & 31; i < n; i += 32) ZV[(long long)j * n + i] = i < k ? Z2[i + (long long)j * k] : 0.0;
+  __syncthreads();
+  qr_apply(cx, m, kU, pv[4], m, pv[5], ZU, m, nc, false);
+  qr_apply(cx, n, kV, pv[6], n, pv[7], ZV, n, nc, false);
+  copy_mat(m, nc, ZU, m, pv[11] + (long long)c0 * lddu, lddu);
+  copy_mat(n, nc, ZV, n, pv[12] + (long long)c0 * lddv, lddv);
+}
+
+__device__ void team_back_member(Ctx& cx, TeamJob* job, int t, int team) {
+  const int nch = (job->iv[8] + BACK_CW - 1) / BACK_CW;
+  for (int ch = t; ch < nch; ch += team) back_chunk(cx, job->iv, job->pv, ch * BACK_CW);
+}
+
+// ---- TK_QR2 ------------------------------------------------------------------
+// iv: m, n, c; pv: Uc, tauU, TpU, Vc, tauV, TpV
+__device__ void team_qr2_member(Ctx& cx, TeamJob* job, int t) {
+  const int m = job->iv[0], n = job->iv[1], c = job->iv[2];
+  if (t == 0) qr_blocked(cx, m, c, job->pv[0], m, job->pv[1], job->pv[2]);
+  else qr_blocked(cx, n, c, job->pv[3], n, job->pv[4], job->pv[5]);
+}
+
+// ---- helper side -------------------------------------------------------------
+// thread 0 of an idle CTA: claim a ticket and join its job.
 // Returns the job slot (>= 0) with *member set, or -1.
 __device__ int team_try_join(TeamCtx* tc, int* member) {
   const int h = vload(tc->tk);
@@ -291,8 +363,14 @@ __device__ int team_try_join(TeamCtx* tc, int* member) {
 
 __device__ void team_help(Ctx& cx, TeamCtx* tc, int slot, int member) {
   TeamJob* job = tc->jobs + slot;
+  cta_acquire();
   const int team = vload(&job->team);
-  team_jacobi_member(cx, job, member, team);
+  switch (job->kind) {
+    case TK_JACOBI: team_jacobi_member(cx, job, member, team); break;
+    case TK_BACK: team_back_member(cx, job, member, team); break;
+    case TK_QR2: team_qr2_member(cx, job, member); break;
+    default: break;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();

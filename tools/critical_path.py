@@ -21,11 +21,15 @@ n = len(tasks)
 rt = _lib.runtime()
 trace = torch.zeros(3 * n, dtype=torch.int64, device=rt.dev)
 rt.lib.blrqr_debug_trace(trace.data_ptr())
+ptrace = torch.zeros(16 * n, dtype=torch.int64, device=rt.dev)
+rt.lib.blrqr_debug_phase_trace(ptrace.data_ptr())
 f = DeviceFactorization("tiled-hh", g, ToleranceConfig(cfg.eps))
 torch.cuda.synchronize(); t0 = time.perf_counter()
 f.run(); f.finish()
 torch.cuda.synchronize(); wall = time.perf_counter() - t0
 rt.lib.blrqr_debug_trace(None)
+rt.lib.blrqr_debug_phase_trace(None)
+ph = ptrace.cpu().numpy().reshape(n, 16).astype(np.float64) / 1.965e9
 tr = trace.cpu().numpy().reshape(n, 3)
 st, en = tr[:, 0].astype(np.float64), tr[:, 1].astype(np.float64)
 dur = (en - st) / 1e9
@@ -53,9 +57,11 @@ kind_time = {k: float(dur[tasks[:, 0] == i].sum()) for i, k in enumerate(kinds)}
 path_kinds = {k: 0.0 for k in kinds}
 for t in path:
     path_kinds[kinds[tasks[t, 0]]] += dur[t]
+path_phases = {nm: round(float(ph[path, i].sum()), 4) for i, nm in enumerate(_lib.PHASES[:13]) if ph[path, i].sum() > 0}
 print(json.dumps({"wall_s": wall, "makespan_s": (en.max() - t0g) / 1e9, "sum_task_s": float(dur.sum()),
                   "sum_task_per_sm_s": float(dur.sum()) / rt.nctas, "critical_path_s": float(finish.max()),
                   "critical_path_tasks": len(path), "time_by_kind_s": kind_time, "critical_path_by_kind_s": path_kinds,
+                  "critical_path_by_phase_s": path_phases,
                   "top_tasks": [[kinds[tasks[t, 0]], int(tasks[t, 1]), int(tasks[t, 2]), int(tasks[t, 3]), round(float(dur[t]), 4)]
                                 for t in np.argsort(-dur)[:15]],
                   "path_sample": [[kinds[tasks[t, 0]], int(tasks[t, 1]), int(tasks[t, 2]), int(tasks[t, 3]), round(float(dur[t]), 4)]
