@@ -196,11 +196,20 @@ def run_ours(args):
         def finish(self):
             return rt.harvest()[1]
 
-    def step():
+    kev = []  # (start, end) CUDA events around the factorization kernels only (no clone)
+
+    def step(record=False):
         if distributed:
             return _DistStep()
         f = DeviceFactorization(method, g0, tol, clone=True)
-        f.run()
+        if record:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            f.run()
+            b.record()
+            kev.append((a, b))
+        else:
+            f.run()
         return f
 
     # warm-up (also builds the schedule and grows the workspace)
@@ -217,12 +226,13 @@ def run_ours(args):
     with ClockSampler(local) as clk:
         for s in range(args.steps):
             ev[s][0].record()
-            f = step()
+            f = step(record=True)
             ev[s][1].record()
         torch.cuda.synchronize()
     barrier()
     counts = f.finish()
     step_ms = [a.elapsed_time(b) for a, b in ev]
+    kern_ms = [a.elapsed_time(b) for a, b in kev]
     # harvest() is called once after K steps: counters summed all K steps;
     # with block-cyclic ranks each rank counts its own tasks -> sum over ranks
     F_step = sum(counts.values()) / args.steps
@@ -236,6 +246,15 @@ def run_ours(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     gflops = F_step / (ms * 1e-3) / 1e9
+    k_ms = (sum(kern_ms) / len(kern_ms)) if kern_ms else ms
+    if distributed:
+        launches, kernel_name = nlev, "k_tiled (per-level task batches, block-cyclic)"
+    elif method == "tiled-hh" and getattr(f, "scheduler", "") == "dag":
+        launches, kernel_name = 2, "k_tiled_dag (persistent dynamic-DAG task kernel, one CTA per SM)"
+    elif method == "tiled-hh":
+        launches, kernel_name = nlev, "k_tiled (level-batched task kernel)"
+    else:
+        launches, kernel_name = None, f"{method} step kernels"
     if distributed:
         gflops /= ws_  # value below multiplies by ws_ for replicas; F_step is already the whole job
 
@@ -291,12 +310,14 @@ def run_ours(args):
                         "max": int(in_ranks.max())},
         "r_ranks": {"median": float(np.median(out_ranks[out_ranks >= 0])), "max": int(out_ranks.max())},
         "setup_s": {"generate": t_gen, "compress": t_comp},
-        "gpu_launches": nlev * args.steps,
-        "roofline": {"bound": "tensor", "achieved": F_step / (ms * 1e-3) / 1e12, "peak": FP64_PEAK_TFLOPS,
-                     "unit": "TFLOP/s", "frac": F_step / (ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
-                     "traffic": None, "kernel": "k_tiled (level-batched task kernel)",
+        "gpu_launches": launches * args.steps,
+        "roofline": {"bound": "tensor", "achieved": F_step / (k_ms * 1e-3) / 1e12, "peak": FP64_PEAK_TFLOPS,
+                     "unit": "TFLOP/s", "frac": F_step / (k_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+                     "traffic": _traffic(args, kernel_name), "kernel": kernel_name, "kernel_ms": k_ms,
                      "peak_source": FP64_PEAK_SRC,
-                     "note": "achieved = reference flop model per factorization / device time of the step"},
+                     "note": "achieved = reference flop model per factorization / CUDA-event time of the "
+                             "factorization launches on their stream (clone excluded); FP64 has no tcgen05 "
+                             "path, the bound is the FP64 DMMA/DFMA pipe"},
         "clocks": clk.summary(),
         "e2e": e2e,
         "impl": "ours",
@@ -310,6 +331,22 @@ def run_ours(args):
         print(json.dumps(res), flush=True)
     if ws_ > 1:
         torch.distributed.destroy_process_group()
+
+
+def _traffic(args, kernel_name):
+    """DRAM bytes (read + write) per launch of the dominant kernel, from the
+    committed ncu --set full capture summary (profiles/ncu_traffic.json)."""
+    if args.traffic is not None:
+        return args.traffic
+    try:
+        with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as fh:
+            d = json.load(fh)
+        e = d.get(args.config, {})
+        if e.get("kernel") and kernel_name.startswith(e["kernel"]):
+            return e.get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        pass
+    return None
 
 
 def _host_cells(f0, rows):
@@ -361,6 +398,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--cpu-rows", type=int, default=12)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="DRAM bytes per launch of the dominant kernel from an ncu --set full capture")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -1,6 +1,8 @@
 #!/bin/bash
 # Round measurement: bench (plain), launch list under ncu, one full ncu capture
-# of the top k_tiled launch.  Outputs under gpurun_out/.
+# of the dominant kernel (k_tiled_dag, C3 full size, application replay so the
+# persistent kernel's 60 GB working set needs no save/restore).  Outputs under
+# gpurun_out/.
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 TAG=${TAG:-r01}
@@ -10,7 +12,9 @@ CMD="python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-cpu"
 timeout 900 $CMD > gpurun_out/plain_${TAG}.log 2>&1 && \
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv $CMD > gpurun_out/ncu_launch_${TAG}.log 2>&1
 echo "launch list rc=$?"
+if [ -z "$SKIP_FULL" ]; then
 CMD2="python tools/probe_config.py C3"
 timeout 600 $CMD2 > gpurun_out/plain2_${TAG}.log 2>&1 && \
-timeout 1500 ncu --set full --clock-control none --import-source on -k regex:k_tiled -s 70 -c 1 -o gpurun_out/prof_tiled_${TAG} $CMD2 > gpurun_out/ncu_full_${TAG}.log 2>&1
+timeout 2700 ncu --set full --clock-control none --import-source on --replay-mode application -k regex:k_tiled_dag -c 1 -o gpurun_out/prof_dag_${TAG} $CMD2 > gpurun_out/ncu_full_${TAG}.log 2>&1
 echo "ncu full rc=$?"
+fi
