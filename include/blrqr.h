@@ -184,6 +184,11 @@ void blrqr_debug_phase_trace(void* dev_buf);
  * one-sided Jacobi of large rounded-addition cores.  The rotation sequence
  * is the single-CTA one, so results do not depend on this switch. */
 void blrqr_set_teams(int enable);
+/* Debug: one-sided Jacobi of X (rows x ncols, column-major, ld rows) with J
+ * (ncols x ncols) -- mode 0 single-CTA blocked, 1 single-CTA column pairs,
+ * 2 CTA team over nctas CTAs.  sigma (ncols), perm (ncols) outputs. */
+int blrqr_debug_jacobi(int rows, int ncols, double* X, double* J, double* sigma, int* perm, int mode, double* ws,
+                       int64_t ws_per_cta, int nctas, int* status, unsigned long long* flops, void* stream);
 /* Debug: `ctas` CTAs each run `reps` CTA-level GEMMs C = op(A) op(B) (+ C). */
 int blrqr_debug_gemm(int ta, int tb, int M, int N, int K, const double* A, int lda, const double* B, int ldb,
                      double* C, int ldc, int reps, int ctas, void* stream);

@@ -72,6 +72,7 @@ _SIGS = {
     "blrqr_debug_phase_trace": ([_P], None),
     "blrqr_apply_q": ([C.POINTER(Grid), C.POINTER(Refl), _I, _P, _L, _I, _I, _P, _L, _I, _P, _P, _P], _I),
     "blrqr_blr_to_dense": ([C.POINTER(Grid), _P, _L, _P], _I),
+    "blrqr_debug_jacobi": ([_I, _I, _P, _P, _P, _P, _I, _P, _L, _I, _P, _P, _P], _I),
     "blrqr_debug_gemm": ([_I, _I, _I, _I, _I, _P, _I, _P, _I, _P, _I, _I, _I, _P], _I),
     "blrqr_tiled_dag": ([_I, _I, _P, _P, _P, _P, _P], _I),
     "blrqr_tiled_run_dag": ([C.POINTER(Grid), C.POINTER(Refl), _I, _P, _P, _P, _P, _P, _P, _D, _P, _L, _I, _D, _P,

@@ -85,24 +85,8 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
   copy_mat(n, ra, A.v, A.ldv, Vc, n, A.s);
   copy_mat(n, rb, B.v, B.ldv, Vc + (long long)ra * n, n, B.s);
   {
-    TeamJob* job = (c >= TEAM_QR2_MIN) ? team_reserve(cx) : nullptr;
-    int team = 1;
-    if (job) {
-      if (threadIdx.x == 0) {
-        job->kind = TK_QR2;
-        job->iv[0] = m; job->iv[1] = n; job->iv[2] = c;
-        job->pv[0] = Uc; job->pv[1] = tauU; job->pv[2] = TpU;
-        job->pv[3] = Vc; job->pv[4] = tauV; job->pv[5] = TpV;
-      }
-      team = team_launch(cx, job, 2);
-    }
-    if (team > 1) {  // helper factors [V_A V_B]
-      team_qr2_member(cx, job, 0);
-      team_finish(cx, job, team);
-    } else {
-      qr_blocked(cx, m, c, Uc, m, tauU, TpU);
-      qr_blocked(cx, n, c, Vc, n, tauV, TpV);
-    }
+    const QrMat mats[2] = {QrMat{Uc, tauU, TpU, m, c, m}, QrMat{Vc, tauV, TpV, n, c, n}};
+    qr_blocked_team(cx, mats, 2);
   }
   tq.stop(cx, PH_QR);
   PhaseTimer tc;
@@ -114,7 +98,7 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
   double* col2o = alloc_fast(cx, k);
   double* taus = alloc(cx, k);  // global: read by back-transform helpers
   int* piv = reinterpret_cast<int*>(alloc_fast(cx, k));
-  double* tau2 = alloc_fast(cx, k);
+  double* tau2 = alloc(cx, k);  // global: the second QR may run as a team
   if (!col2 || !col2o || !taus || !piv || !tau2) { release(cx, mk); return 0; }
   const int smem_before_g = cx.stop;
   double* G = alloc_fast(cx, (long long)k * k);
@@ -188,7 +172,10 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
   if (in_smem(cx, G)) cx.stop = smem_before_g;
   // (3c) second (unpivoted) QR, X = Q2 R2 -- Drmac-Veselic QR+LQ
   // preconditioning: Jacobi then works on the kp x kp triangle R2
-  qr_blocked(cx, k, kp, X, k, tau2, Tp2);
+  {
+    const QrMat mx{X, tau2, Tp2, k, kp, k};
+    qr_blocked_team(cx, &mx, 1);
+  }
   // W2 and J both in shared memory (jacobi_smem) or both in the global arena,
   // leaving the shared arena to the block Jacobi's staging (jb = 16 columns)
   const Mark before_w = mark(cx);

@@ -39,17 +39,15 @@ __global__ void __launch_bounds__(NT) k_rounded_add(int nb, int m, int n, const 
                                                      const double* const* ub, const double* const* vb,
                                                      const int* rb, double* const* uo, double* const* vo, int* ro,
                                                      int cap, double eps, double* ws, long long wsp, int* status,
-                                                     unsigned long long* flops) {
+                                                     unsigned long long* flops, TeamCtx* team, int* ctr) {
   Ctx cx = make_ctx(ws, wsp, status, flops);
-  for (int t = blockIdx.x; t < nb; t += gridDim.x) {
+  cx.team = team;
+  team_task_loop(cx, nb, ctr, [&](long long t) {
     Blk A = make_lr(m, n, ra[t], const_cast<double*>(ua[t]), m, const_cast<double*>(va[t]), n);
     Blk B = make_lr(m, n, rb[t], const_cast<double*>(ub[t]), m, const_cast<double*>(vb[t]), n);
     const int r = rounded_add(cx, A, B, eps, uo[t], m, vo[t], n, cap);
     if (threadIdx.x == 0) ro[t] = r;
-    cx.top = 0;
-    cx.stop = 0;
-    __syncthreads();
-  }
+  });
 }
 
 __global__ void __launch_bounds__(NT) k_compress(int nb, int m, int n, const double* const* a, double* const* uo,
@@ -413,6 +411,7 @@ __global__ void __launch_bounds__(NT, 1) k_tiled_dag(DagDev d, blrqr_grid g, blr
     if (threadIdx.x == 0) {
       int t = -1;
       const long long t0 = sm_clock();
+      if (d.team) atomicAdd(d.team->tk + 2, 1);  // polling
       while (true) {
         bool got = false;
         if (d.team) {  // help a running team job first: it is on the critical path
@@ -443,6 +442,7 @@ __global__ void __launch_bounds__(NT, 1) k_tiled_dag(DagDev d, blrqr_grid g, blr
         }
         __nanosleep(64);
       }
+      if (d.team) atomicSub(d.team->tk + 2, 1);
       __threadfence();
       s_task = t;
     }
@@ -500,10 +500,11 @@ __global__ void k_dag_init(DagDev d) {
 // one level (or any contiguous range) of tiled tasks, one CTA per task
 __global__ void __launch_bounds__(NT, 1) k_tiled(const blrqr_task* tasks, long long t0, long long t1, blrqr_grid g,
                                                blrqr_refl rf, double eps, double* ws, long long wsp, int* status,
-                                               unsigned long long* flops) {
+                                               unsigned long long* flops, TeamCtx* team, int* ctr) {
   Ctx cx = make_ctx(ws, wsp, status, flops);
-  for (long long t = t0 + blockIdx.x; t < t1; t += gridDim.x) {
-    const blrqr_task tk = tasks[t];
+  cx.team = team;
+  team_task_loop(cx, t1 - t0, ctr, [&](long long t) {
+    const blrqr_task tk = tasks[t0 + t];
     PhaseTimer tt;
     switch (tk.kind) {
       case 0: tiled_diag(cx, g, rf, tk.k); break;
@@ -512,10 +513,7 @@ __global__ void __launch_bounds__(NT, 1) k_tiled(const blrqr_task* tasks, long l
       default: tiled_trap(cx, g, rf, eps, tk.k, tk.i, tk.j); break;
     }
     tt.stop(cx, PH_TASK);
-    cx.top = 0;
-    cx.stop = 0;
-    __syncthreads();
-  }
+  });
 }
 
 
@@ -577,6 +575,45 @@ static void init_kernels() {
 }
 #define INIT_KERNELS() init_kernels()
 
+static int g_teams_enabled = 1;
+
+// Team-job table + ticket ring + two task counters, one per (device, stream)
+// so concurrent launches on different streams never share them; allocated
+// once, reset (stream-ordered) before every launch that uses them.  Returns
+// the TeamCtx (nullptr when teams are disabled) and the counter pair.
+static int team_for_launch(cudaStream_t st, TeamCtx** team, int** ctr) {
+  struct Buf {
+    char* p = nullptr;
+    TeamCtx h;
+  };
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, Buf> bufs;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const size_t jobs_b = sizeof(TeamJob) * TEAM_JOBS, tick_b = sizeof(int) * (size_t)TEAM_TICKETS;
+  Buf* b;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    b = &bufs[{dev, st}];
+    if (!b->p) {
+      CK(cudaMalloc(&b->p, 256 + jobs_b + tick_b + 256));
+      b->h.jobs = reinterpret_cast<TeamJob*>(b->p + 256);
+      b->h.tickets = reinterpret_cast<int*>(b->p + 256 + jobs_b);
+      b->h.tk = reinterpret_cast<int*>(b->p + 256 + jobs_b + tick_b);
+      b->h.tk_cap = TEAM_TICKETS;
+      CK(cudaMemcpy(b->p, &b->h, sizeof(TeamCtx), cudaMemcpyHostToDevice));
+    }
+  }
+  if (g_teams_enabled) {
+    CK(cudaMemsetAsync(b->h.jobs, 0, jobs_b, st));
+    CK(cudaMemsetAsync(b->h.tickets, 0xFF, tick_b, st));
+  }
+  CK(cudaMemsetAsync(b->h.tk, 0, 256, st));  // ring head/tail + task counters
+  if (ctr) *ctr = b->h.tk + 16;
+  *team = g_teams_enabled ? reinterpret_cast<TeamCtx*>(b->p) : nullptr;
+  return 0;
+}
+
 extern "C" {
 
 int blrqr_version(void) { return 1; }
@@ -600,10 +637,14 @@ int blrqr_rounded_add_batched(int nbatch, int m, int n, const double* const* ua,
   if (nbatch < 0 || m <= 0 || n <= 0 || cap < 0) return -1;
   if (!(eps > 0.0 && eps < 1.0)) return -2;
   if (nbatch == 0) return 0;
-  const int grid = std::max(1, std::min(nbatch, nctas));
   INIT_KERNELS();
+  int* ctr = nullptr;
+  TeamCtx* team = nullptr;
+  if (int e = team_for_launch(as_stream(stream), &team, &ctr)) return e;
+  // with teams, CTAs without a task of their own help the others
+  const int grid = std::max(1, team ? nctas : std::min(nbatch, nctas));
   k_rounded_add<<<grid, NT, SMEM_BYTES, as_stream(stream)>>>(nbatch, m, n, ua, va, ra, ub, vb, rb, uo, vo, ro, cap, eps, ws,
-                                                   ws_per_cta, status, flops);
+                                                   ws_per_cta, status, flops, team, ctr);
   CK(cudaGetLastError());
   return 0;
 }
@@ -851,9 +892,9 @@ static long long* g_dag_trace = nullptr;
 void blrqr_debug_trace(void* dev_buf) { g_dag_trace = reinterpret_cast<long long*>(dev_buf); }
 static unsigned long long* g_phase_trace = nullptr;
 void blrqr_debug_phase_trace(void* dev_buf) { g_phase_trace = reinterpret_cast<unsigned long long*>(dev_buf); }
-
-static int g_teams_enabled = 1;
 void blrqr_set_teams(int enable) { g_teams_enabled = enable ? 1 : 0; }
+
+
 
 int64_t blrqr_tiled_dag_size(int p, int q, int64_t* nedges) {
   if (q < 1 || p < q) return -1;
@@ -905,29 +946,7 @@ int blrqr_tiled_run_dag(const blrqr_grid* g, const blrqr_refl* rf, int ntasks, c
   d.ptrace = g_phase_trace;
   int dev = 0, clk_khz = 1965000;
   cudaGetDevice(&dev);
-  d.team = nullptr;
-  if (g_teams_enabled && dev >= 0 && dev < 16) {
-    // one team-job table + ticket ring per device, allocated once, reset per run
-    static TeamCtx* team_buf[16] = {};
-    static TeamCtx team_host[16];
-    const size_t jobs_b = sizeof(TeamJob) * TEAM_JOBS, tick_b = sizeof(int) * (size_t)TEAM_TICKETS;
-    if (!team_buf[dev]) {
-      char* p = nullptr;
-      CK(cudaMalloc(&p, sizeof(TeamCtx) + 256 + jobs_b + tick_b + 256));
-      TeamCtx& h = team_host[dev];
-      h.jobs = reinterpret_cast<TeamJob*>(p + 256);
-      h.tickets = reinterpret_cast<int*>(p + 256 + jobs_b);
-      h.tk = reinterpret_cast<int*>(p + 256 + jobs_b + tick_b);
-      h.tk_cap = TEAM_TICKETS;
-      CK(cudaMemcpy(p, &h, sizeof(TeamCtx), cudaMemcpyHostToDevice));
-      team_buf[dev] = reinterpret_cast<TeamCtx*>(p);
-    }
-    const TeamCtx& h = team_host[dev];
-    CK(cudaMemsetAsync(h.jobs, 0, jobs_b, st));
-    CK(cudaMemsetAsync(h.tickets, 0xFF, tick_b, st));
-    CK(cudaMemsetAsync(h.tk, 0, 256, st));
-    d.team = team_buf[dev];
-  }
+  if (int e = team_for_launch(st, &d.team, nullptr)) return e;
   CK(cudaMemcpyAsync(d.indeg, indeg0_dev, sizeof(int) * ntasks, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemsetAsync(d.q[0], 0xFF, sizeof(int) * 2 * (size_t)ntasks, st));
   CK(cudaMemsetAsync(d.ctr, 0, sizeof(int) * 8, st));
@@ -948,9 +967,13 @@ int blrqr_tiled_run(const blrqr_grid* g, const blrqr_refl* rf, const blrqr_task*
   for (int l = l0; l < l1; ++l) {
     const int64_t t0 = level_start_host[l], t1 = level_start_host[l + 1];
     if (t1 <= t0) continue;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(t1 - t0, nctas));
     INIT_KERNELS();
-    k_tiled<<<grid, NT, SMEM_BYTES, as_stream(stream)>>>(tasks_dev, t0, t1, *g, *rf, eps, ws, ws_per_cta, status, flops);
+    int* ctr = nullptr;
+    TeamCtx* team = nullptr;
+    if (int e = team_for_launch(as_stream(stream), &team, &ctr)) return e;
+    const int grid = (int)std::max<int64_t>(1, team ? nctas : std::min<int64_t>(t1 - t0, nctas));
+    k_tiled<<<grid, NT, SMEM_BYTES, as_stream(stream)>>>(tasks_dev, t0, t1, *g, *rf, eps, ws, ws_per_cta, status, flops,
+                                                         team, ctr);
     CK(cudaGetLastError());
   }
   return 0;
@@ -1016,6 +1039,37 @@ int blrqr_mgs_step(const blrqr_grid* a, const blrqr_grid* qg, const blrqr_grid* 
 __global__ void __launch_bounds__(NT, 1) k_gemm_probe(int ta, int tb, int M, int N, int K, const double* A, int lda,
                                                       const double* B, int ldb, double* C, int ldc, int reps) {
   for (int r = 0; r < reps; ++r) gemm(ta != 0, tb != 0, M, N, K, 1.0, A, lda, B, ldb, r == 0 ? 0.0 : 1.0, C, ldc);
+}
+
+// Jacobi probe: one task = the one-sided Jacobi of X (rows x ncols, global)
+// with J (ncols x ncols); mode 0 jacobi_blocked, 1 jacobi_cols, 2 team (idle
+// CTAs of the launch help).  Used by tools/bench_jacobi.py.
+__global__ void __launch_bounds__(NT, 1) k_jacobi_probe(int rows, int ncols, double* X, double* J, double* sigma,
+                                                        int* perm, int mode, double* ws, long long wsp, int* status,
+                                                        unsigned long long* flops, TeamCtx* team, int* ctr) {
+  Ctx cx = make_ctx(ws, wsp, status, flops);
+  cx.team = mode == 2 ? team : nullptr;
+  team_task_loop(cx, 1, ctr, [&](long long) {
+    PhaseTimer t;
+    if (mode == 1 || !((mode == 2 && team_jacobi_lead(cx, rows, ncols, X, rows, J, ncols, sigma, perm)) ||
+                       jacobi_blocked(cx, rows, ncols, X, rows, J, ncols, sigma, perm, flops)))
+      jacobi_cols(rows, ncols, X, rows, J, ncols, sigma, perm, flops);
+    t.stop(cx, PH_SVD);
+  });
+}
+
+extern "C" int blrqr_debug_jacobi(int rows, int ncols, double* X, double* J, double* sigma, int* perm, int mode,
+                                  double* ws, int64_t ws_per_cta, int nctas, int* status, unsigned long long* flops,
+                                  void* stream) {
+  INIT_KERNELS();
+  cudaFuncSetAttribute(k_jacobi_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  int* ctr = nullptr;
+  TeamCtx* team = nullptr;
+  if (int e = team_for_launch(as_stream(stream), &team, &ctr)) return e;
+  k_jacobi_probe<<<mode == 2 ? nctas : 1, NT, SMEM_BYTES, as_stream(stream)>>>(rows, ncols, X, J, sigma, perm, mode, ws,
+                                                                            ws_per_cta, status, flops, team, ctr);
+  CK(cudaGetLastError());
+  return 0;
 }
 
 extern "C" int blrqr_debug_gemm(int ta, int tb, int M, int N, int K, const double* A, int lda, const double* B,

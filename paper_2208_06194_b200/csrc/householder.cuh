@@ -138,68 +138,127 @@ __device__ __noinline__ void build_t_full(Ctx& cx, int n, const double* S, int l
 // On exit: R in the upper triangle, reflectors below, tau[0:k] (tau[j] = 0 for
 // j >= m), and per-panel T factors: Tp (QR_NB x k, panel p at column p*QR_NB,
 // ld QR_NB) holding the panel's own compact-WY T (for fast applications).
+//
+// The trailing update is done in fixed QR_CW-column chunks, each chunk owned
+// by one member of a CTA team (chunk g -> member g mod T; a lone CTA owns
+// all).  Every chunk sees the same operation sequence whatever the team size,
+// so results are bitwise independent of T.  One barrier per panel, with
+// look-ahead: the owner of the next panel updates that chunk first and
+// factors the next panel before finishing its other chunks.
 // ---------------------------------------------------------------------------
-__device__ __noinline__ void qr_blocked(Ctx& cx, int m, int n, double* A, int lda, double* tau, double* Tp) {
-  const int k = min(m, n);
-  const Mark mk = mark(cx);
+constexpr int QR_CW = 64;
+
+struct QrMat {
+  double* A;
+  double* tau;
+  double* Tp;
+  int m, n, lda;
+};
+
+// factor panel [c0, c0 + w) of M: R and reflectors into A, tau, panel T into Tp
+__device__ void qr_factor_panel(Ctx& cx, const QrMat& M, int c0, int w) {
+  const int h = M.m - c0;
+  const Mark pm = mark(cx);
   double* S = alloc_fast(cx, (long long)QR_NB * QR_NB);
-  double* W = alloc(cx, (long long)QR_NB * max(n, 1));
-  if (!S || !W) { release(cx, mk); return; }
-  for (int c0 = 0; c0 < k; c0 += QR_NB) {
-    const int w = min(QR_NB, k - c0);
-    const int h = m - c0;
-    // stage the h x w panel in shared memory when it fits; factor it there
-    const Mark pm = mark(cx);
-    double* P = salloc(cx, (long long)h * w);
-    double* Y;
-    if (P) {
-      copy_mat(h, w, A + c0 + (long long)c0 * lda, lda, P, h);
-      qr_panel_unblocked(h, 0, w, as_smem(cx, P), h, tau + c0);  // shared-space loads
-      copy_mat(h, w, P, h, A + c0 + (long long)c0 * lda, lda);
-      // P becomes the explicit unit-lower-trapezoidal Y in place
-      for (int jj = threadIdx.x >> 5; jj < w; jj += NWARP)
-        for (int i = threadIdx.x & 31; i < h; i += 32) {
+  double* P = salloc(cx, (long long)h * w);
+  double* Y;
+  double* Ap = M.A + c0 + (long long)c0 * M.lda;
+  if (P) {  // stage the h x w panel in shared memory and factor it there
+    copy_mat(h, w, Ap, M.lda, P, h);
+    qr_panel_unblocked(h, 0, w, as_smem(cx, P), h, M.tau + c0);
+    copy_mat(h, w, P, h, Ap, M.lda);
+    for (int jj = threadIdx.x >> 5; jj < w; jj += NWARP)  // P -> explicit unit-lower Y
+      for (int i = threadIdx.x & 31; i < h; i += 32) {
         const long long e = (long long)jj * h + i;
         if (i < jj) P[e] = 0.0;
         else if (i == jj) P[e] = 1.0;
       }
-      __syncthreads();
-      Y = P;
-    } else {
-      qr_panel_unblocked(m, c0, w, A, lda, tau);
-      Y = alloc(cx, (long long)h * QR_NB);
-      if (!Y) { release(cx, mk); return; }
-      extract_y(m, c0, w, A, lda, Y, h);
+    __syncthreads();
+    Y = P;
+  } else {
+    qr_panel_unblocked(M.m, c0, w, M.A, M.lda, M.tau);
+    Y = alloc(cx, (long long)h * QR_NB);
+    if (!Y) { release(cx, pm); return; }
+    extract_y(M.m, c0, w, M.A, M.lda, Y, h);
+  }
+  gemm(true, false, w, w, h, 1.0, Y, h, Y, h, 0.0, S, QR_NB);
+  t_block_recurrence(0, w, S, QR_NB, M.tau + c0, M.Tp + (long long)c0 * QR_NB, QR_NB);
+  release(cx, pm);
+}
+
+// A(c0:m, col0:col1) <- (I - Y T Y^T)^T A(c0:m, col0:col1) for panel c0 (Y h x w)
+__device__ void qr_panel_apply(const QrMat& M, int c0, int w, const double* Y, int col0, int col1, double* W) {
+  const int h = M.m - c0, n2 = col1 - col0;
+  if (n2 <= 0) return;
+  double* A2 = M.A + c0 + (long long)col0 * M.lda;
+  const double* T = M.Tp + (long long)c0 * QR_NB;
+  gemm(true, false, w, n2, h, 1.0, Y, h, A2, M.lda, 0.0, W, QR_NB);
+  // W <- T^T W in place per column (T upper => T^T lower)
+  for (int e = threadIdx.x; e < n2; e += NT) {
+    double* wc = W + (long long)e * QR_NB;
+    double tmp[QR_NB];
+#pragma unroll
+    for (int a = 0; a < QR_NB; ++a) tmp[a] = a < w ? wc[a] : 0.0;
+#pragma unroll
+    for (int a = QR_NB - 1; a >= 0; --a) {
+      double s = 0.0;
+#pragma unroll
+      for (int b2 = 0; b2 <= a; ++b2) s = fma(T[b2 + a * QR_NB], tmp[b2], s);
+      if (a < w) wc[a] = s;
     }
-    // panel T: S = Y^T Y, recurrence
-    gemm(true, false, w, w, h, 1.0, Y, h, Y, h, 0.0, S, QR_NB);
-    double* T = Tp + (long long)c0 * QR_NB;
-    t_block_recurrence(0, w, S, QR_NB, tau + c0, T, QR_NB);
-    const int n2 = n - (c0 + w);
-    if (n2 > 0) {
-      double* A2 = A + c0 + (long long)(c0 + w) * lda;
-      // A2 = (I - Y T Y^T)^T A2 = A2 - Y T^T (Y^T A2)
-      gemm(true, false, w, n2, h, 1.0, Y, h, A2, lda, 0.0, W, QR_NB);
-      // W <- T^T W in place per column (T upper => T^T lower)
-      for (long long e = threadIdx.x; e < (long long)n2; e += NT) {
-        double* wc = W + e * QR_NB;
-        double tmp[QR_NB];
-#pragma unroll
-        for (int a = 0; a < QR_NB; ++a) tmp[a] = a < w ? wc[a] : 0.0;
-#pragma unroll
-        for (int a = QR_NB - 1; a >= 0; --a) {
-          double s = 0.0;
-#pragma unroll
-          for (int b2 = 0; b2 <= a; ++b2) s = fma(T[b2 + a * QR_NB], tmp[b2], s);
-          if (a < w) wc[a] = s;
-        }
+  }
+  __syncthreads();
+  gemm(false, false, h, n2, w, -1.0, Y, h, W, QR_NB, 1.0, A2, M.lda);
+}
+
+// QR of nm (<= 2) matrices at once by member t of a team of `team` CTAs;
+// barrier() synchronises the team (a __syncthreads for a lone CTA).
+template <class Bar>
+__device__ void qr_blocked_multi(Ctx& cx, const QrMat* mats, int nm, int t, int team, Bar&& barrier) {
+  const Mark mk = mark(cx);
+  int mh = 1, np = 0, cbase[3] = {0, 0, 0};
+  for (int i = 0; i < nm; ++i) {
+    mh = max(mh, mats[i].m);
+    np = max(np, (min(mats[i].m, mats[i].n) + QR_NB - 1) / QR_NB);
+    cbase[i + 1] = cbase[i] + (mats[i].n + QR_CW - 1) / QR_CW;
+  }
+  double* W = alloc_fast(cx, (long long)QR_NB * QR_CW);
+  double* Yb = alloc_fast(cx, (long long)mh * QR_NB);
+  if (!W || !Yb) { release(cx, mk); return; }
+  auto owns = [&](int i, int c) { return (cbase[i] + c) % team == t; };
+  for (int i = 0; i < nm; ++i) {  // prologue: panel 0
+    const int k = min(mats[i].m, mats[i].n);
+    if (k > 0 && owns(i, 0)) qr_factor_panel(cx, mats[i], 0, min(QR_NB, k));
+  }
+  barrier();
+  for (int p = 0; p < np; ++p) {
+    for (int i = 0; i < nm; ++i) {
+      const QrMat& M = mats[i];
+      const int k = min(M.m, M.n), c0 = p * QR_NB;
+      if (c0 >= k) continue;
+      const int w = min(QR_NB, k - c0), nxt = c0 + w;
+      const int cfirst = nxt / QR_CW, clast = (M.n - 1) / QR_CW;
+      bool any = false;
+      for (int c = cfirst; c <= clast; ++c) any |= (nxt < M.n) && owns(i, c);
+      if (!any) continue;
+      extract_y(M.m, c0, w, M.A, M.lda, Yb, M.m - c0);
+      int done = -1;
+      if (nxt < k && owns(i, nxt / QR_CW)) {  // look-ahead: next panel's chunk first
+        done = nxt / QR_CW;
+        qr_panel_apply(M, c0, w, Yb, nxt, min((done + 1) * QR_CW, M.n), W);
+        qr_factor_panel(cx, M, nxt, min(QR_NB, k - nxt));
       }
-      __syncthreads();
-      gemm(false, false, h, n2, w, -1.0, Y, h, W, QR_NB, 1.0, A2, lda);
+      for (int c = cfirst; c <= clast; ++c)
+        if (c != done && owns(i, c)) qr_panel_apply(M, c0, w, Yb, max(c * QR_CW, nxt), min((c + 1) * QR_CW, M.n), W);
     }
-    release(cx, pm);
+    barrier();
   }
   release(cx, mk);
+}
+
+__device__ __noinline__ void qr_blocked(Ctx& cx, int m, int n, double* A, int lda, double* tau, double* Tp) {
+  const QrMat M{A, tau, Tp, m, n, lda};
+  qr_blocked_multi(cx, &M, 1, 0, 1, [] { __syncthreads(); });
 }
 
 // Apply Q = H_0 H_1 ... H_{k-1} (from qr_blocked of an m-row matrix) to Z

@@ -55,7 +55,10 @@ __device__ void geqrt_inplace(Ctx& cx, int m, int n, double* A, int lda, double*
   double* X = alloc(cx, (long long)n * QR_NB);
   double* X2 = alloc(cx, (long long)n * QR_NB);
   if (!tau || !Tp || !X || !X2) { cx.top = mark; return; }
-  qr_blocked(cx, m, n, A, lda, tau, Tp);
+  {
+    const QrMat M{A, tau, Tp, m, n, lda};
+    qr_blocked_team(cx, &M, 1);
+  }
   // Y explicit unit-lower-trapezoidal; zero A below the diagonal
   for (int j = threadIdx.x >> 5; j < n; j += NWARP)
     for (int i = threadIdx.x & 31; i < m; i += 32) {

@@ -5,7 +5,10 @@
 // running a large rounded addition posts *team jobs* for its parallel
 // stages; idle CTAs of the persistent kernel (which poll a ticket ring before
 // the task queues) join them:
-//   TK_QR2    the two independent QRs of [U_A U_B] and [V_A V_B];
+//   TK_QRB    blocked Householder QRs (the rounded addition's [U_A U_B] and
+//             [V_A V_B] together, its second QR, DiagQR's GEQRT): fixed
+//             64-column trailing-update chunks, chunk g on member g mod T, one
+//             barrier per 16-column panel with look-ahead;
 //   TK_JACOBI jacobi_blocked's block Jacobi of the core: the block pairs of
 //             one round-robin round touch disjoint columns, so member t takes
 //             pairs t, t+T, ... and a team barrier separates rounds;
@@ -29,15 +32,14 @@ namespace blr {
 
 constexpr int TEAM_MAX = 16;  // members including the leader
 constexpr int TEAM_JOBS = 128;
-constexpr int TEAM_TICKETS = 1 << 20;
+constexpr int TEAM_TICKETS = 1 << 22;
 constexpr int TEAM_CLOSED = 0x8000;
 constexpr long long TEAM_WAIT_CYCLES = 40000;           // leader's wait for helpers (~20 us)
 constexpr long long TEAM_SPIN_TIMEOUT = 20000000000LL;  // ~10 s of spinning -> abort
 constexpr int BACK_CW = 32;                              // back-transform column chunk
-constexpr int TEAM_QR2_MIN = 64;   // [U_A U_B] width from which the two QRs split
 constexpr int TEAM_BACK_MIN = 64;  // Q_U width from which the back-transform splits
 
-enum TeamKind : int { TK_JACOBI = 1, TK_BACK = 2, TK_QR2 = 3 };
+enum TeamKind : int { TK_JACOBI = 1, TK_BACK = 2, TK_QRB = 3 };
 
 struct __align__(128) TeamJob {
   int state;  // 0 free, 9 being set up, 2 running (team size published)
@@ -56,7 +58,7 @@ struct __align__(128) TeamJob {
 struct TeamCtx {
   TeamJob* jobs;  // TEAM_JOBS
   int* tickets;   // ring of slot << 16 | (gen & 0x7fff), -1 = not yet written
-  int* tk;        // [0] head, [1] tail
+  int* tk;        // [0] head, [1] tail, [2] CTAs currently polling, [16..17] task counters
   int tk_cap;
 };
 
@@ -111,6 +113,8 @@ __device__ int team_launch(Ctx& cx, TeamJob* job, int want) {
     job->bar_count = 0;
     job->rot[0] = job->rot[1] = job->rot[2] = 0;
     job->done = 0;
+    // only ask for as many helpers as there are CTAs polling right now
+    want = min(want, 1 + max(0, vload(tc->tk + 2)));
     __threadfence();
     atomicExch(&job->join, gen << 16);  // open
     const int ticket = (slot << 16) | gen;
@@ -119,7 +123,8 @@ __device__ int team_launch(Ctx& cx, TeamJob* job, int want) {
       if (idx < tc->tk_cap) atomicExch(tc->tickets + idx, ticket);
     }
     const long long t0 = sm_clock();
-    while ((vload(&job->join) & 0x7fff) < want - 1 && sm_clock() - t0 < TEAM_WAIT_CYCLES) __nanosleep(64);
+    while (want > 1 && (vload(&job->join) & 0x7fff) < want - 1 && sm_clock() - t0 < TEAM_WAIT_CYCLES)
+      __nanosleep(64);
     const int got = atomicOr(&job->join, TEAM_CLOSED) & 0x7fff;
     const int team = 1 + min(got, want - 1);
     job->team = team;
@@ -164,7 +169,7 @@ __device__ void team_barrier(Ctx& cx, TeamJob* job, int team) {
     }
     __threadfence();
   }
-  __syncthreads();
+  cta_acquire();  // every thread may now read the other members' writes
 }
 
 // ---- TK_JACOBI ---------------------------------------------------------------
@@ -327,12 +332,51 @@ __device__ void team_back_member(Ctx& cx, TeamJob* job, int t, int team) {
   for (int ch = t; ch < nch; ch += team) back_chunk(cx, job->iv, job->pv, ch * BACK_CW);
 }
 
-// ---- TK_QR2 ------------------------------------------------------------------
-// iv: m, n, c; pv: Uc, tauU, TpU, Vc, tauV, TpV
-__device__ void team_qr2_member(Ctx& cx, TeamJob* job, int t) {
-  const int m = job->iv[0], n = job->iv[1], c = job->iv[2];
-  if (t == 0) qr_blocked(cx, m, c, job->pv[0], m, job->pv[1], job->pv[2]);
-  else qr_blocked(cx, n, c, job->pv[3], n, job->pv[4], job->pv[5]);
+// ---- TK_QRB ------------------------------------------------------------------
+// Blocked Householder QR of 1-2 matrices (householder.cuh qr_blocked_multi).
+// iv: nm, then (m, n, lda) per matrix; pv: (A, tau, Tp) per matrix.
+__device__ void team_qrb_member(Ctx& cx, TeamJob* job, int t, int team) {
+  QrMat mats[2];
+  const int nm = job->iv[0];
+  for (int i = 0; i < nm; ++i)
+    mats[i] = QrMat{job->pv[3 * i], job->pv[3 * i + 1], job->pv[3 * i + 2], job->iv[1 + 3 * i], job->iv[2 + 3 * i],
+                    job->iv[3 + 3 * i]};
+  qr_blocked_multi(cx, mats, nm, t, team, [&] { team_barrier(cx, job, team); });
+}
+
+// QR of nm matrices (all operands in global memory), with a team of up to one
+// CTA per trailing-update chunk when idle CTAs are available.  Bitwise the
+// same as qr_blocked on each matrix.
+__device__ void qr_blocked_team(Ctx& cx, const QrMat* mats, int nm) {
+  int chunks = 0;
+  bool global = true;
+  for (int i = 0; i < nm; ++i) {
+    chunks += (mats[i].n + QR_CW - 1) / QR_CW;
+    global &= !in_smem(cx, mats[i].A) && !in_smem(cx, mats[i].tau) && !in_smem(cx, mats[i].Tp);
+  }
+  TeamJob* job = (chunks >= 2 && global) ? team_reserve(cx) : nullptr;
+  int team = 1;
+  if (job) {
+    if (threadIdx.x == 0) {
+      job->kind = TK_QRB;
+      job->iv[0] = nm;
+      for (int i = 0; i < nm; ++i) {
+        job->iv[1 + 3 * i] = mats[i].m;
+        job->iv[2 + 3 * i] = mats[i].n;
+        job->iv[3 + 3 * i] = mats[i].lda;
+        job->pv[3 * i] = mats[i].A;
+        job->pv[3 * i + 1] = mats[i].tau;
+        job->pv[3 * i + 2] = mats[i].Tp;
+      }
+    }
+    team = team_launch(cx, job, min(TEAM_MAX, chunks));
+  }
+  if (team > 1) {
+    qr_blocked_multi(cx, mats, nm, 0, team, [&] { team_barrier(cx, job, team); });
+    team_finish(cx, job, team);
+  } else {
+    qr_blocked_multi(cx, mats, nm, 0, 1, [] { __syncthreads(); });
+  }
 }
 
 // ---- helper side -------------------------------------------------------------
@@ -361,6 +405,61 @@ __device__ int team_try_join(TeamCtx* tc, int* member) {
   return slot;
 }
 
+__device__ void team_help(Ctx& cx, TeamCtx* tc, int slot, int member);
+
+// Persistent task loop for a flat batch of n independent tasks (batched
+// rounded additions, one level of the level scheduler): CTAs claim tasks
+// from ctr[0]; a CTA that finds none left helps team jobs until ctr[1]
+// (finished tasks) reaches n.  With cx.team == nullptr it is a plain dynamic
+// loop.  run(t) executes task t with the whole CTA.
+template <class F>
+__device__ void team_task_loop(Ctx& cx, long long n, int* ctr, F run) {
+  __shared__ long long s_t;
+  __shared__ int s_member;
+  while (true) {
+    if (threadIdx.x == 0) {
+      long long t = -1;
+      if (cx.team) atomicAdd(cx.team->tk + 2, 1);  // polling
+      while (true) {
+        if (cx.team) {
+          int member;
+          const int slot = team_try_join(cx.team, &member);
+          if (slot >= 0) {
+            t = -2 - slot;
+            s_member = member;
+            break;
+          }
+        }
+        const int h = vload(ctr);
+        if (h < n) {
+          if (atomicCAS(ctr, h, h + 1) == h) {
+            t = h;
+            break;
+          }
+          continue;
+        }
+        if (vload(ctr + 1) >= n) break;
+        __nanosleep(64);
+      }
+      if (cx.team) atomicSub(cx.team->tk + 2, 1);
+      s_t = t;
+    }
+    __syncthreads();
+    const long long t = s_t;
+    if (t == -1) break;
+    __threadfence();
+    if (t < -1) team_help(cx, cx.team, (int)(-2 - t), s_member);
+    else run(t);
+    cx.top = 0;
+    cx.stop = 0;
+    __syncthreads();
+    if (t >= 0 && threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(ctr + 1, 1);
+    }
+  }
+}
+
 __device__ void team_help(Ctx& cx, TeamCtx* tc, int slot, int member) {
   TeamJob* job = tc->jobs + slot;
   cta_acquire();
@@ -368,7 +467,7 @@ __device__ void team_help(Ctx& cx, TeamCtx* tc, int slot, int member) {
   switch (job->kind) {
     case TK_JACOBI: team_jacobi_member(cx, job, member, team); break;
     case TK_BACK: team_back_member(cx, job, member, team); break;
-    case TK_QR2: team_qr2_member(cx, job, member); break;
+    case TK_QRB: team_qrb_member(cx, job, member, team); break;
     default: break;
   }
   __syncthreads();

@@ -43,4 +43,4 @@ for b, ra, rb in CASES:
     tot = sum(ph.values())
     print(json.dumps({"b": b, "c": ra + rb, "rank_out": int(ro[0].item()), "ms_per_wave": round(ms, 3), "batch": nb,
                       "phase_share": {k: round(v / tot, 3) for k, v in ph.items() if not k.startswith("jacobi")}, "sweeps_per_call": ph.get("jacobi_sweeps", 0) / max(1, ph.get("jacobi_calls", 1)),
-                      "us_per_radd_per_cta": round(ms * 1e3, 1)}), flush=True)
+                      "us_per_radd_per_cta": round(ms * 1e3, 1), "team_jobs": rt.last_stats[5], "team_members": rt.last_stats[6]}), flush=True)

@@ -62,6 +62,12 @@ print(json.dumps({"wall_s": wall, "makespan_s": (en.max() - t0g) / 1e9, "sum_tas
                   "sum_task_per_sm_s": float(dur.sum()) / rt.nctas, "critical_path_s": float(finish.max()),
                   "critical_path_tasks": len(path), "time_by_kind_s": kind_time, "critical_path_by_kind_s": path_kinds,
                   "critical_path_by_phase_s": path_phases,
+                  "kind_stats_ms": {k: {"n": int((tasks[:, 0] == i).sum()),
+                                        "mean": round(float(dur[tasks[:, 0] == i].mean() * 1e3), 3),
+                                        "max": round(float(dur[tasks[:, 0] == i].max() * 1e3), 3)}
+                                    for i, k in enumerate(kinds) if (tasks[:, 0] == i).any()},
+                  "path_update_phases_s": {nm: round(float(ph[[t for t in path if tasks[t, 0] == 2], i].sum()), 4)
+                                           for i, nm in enumerate(_lib.PHASES[:13])},
                   "top_tasks": [[kinds[tasks[t, 0]], int(tasks[t, 1]), int(tasks[t, 2]), int(tasks[t, 3]), round(float(dur[t]), 4)]
                                 for t in np.argsort(-dur)[:15]],
                   "path_sample": [[kinds[tasks[t, 0]], int(tasks[t, 1]), int(tasks[t, 2]), int(tasks[t, 3]), round(float(dur[t]), 4)]
