@@ -94,10 +94,10 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
   const int k = kU;  // square blocks: kU == kV
   // small per-core vectors first, so the k x k core is the top of the shared
   // arena and can be dropped once its reflectors are saved
-  double* col2 = alloc_fast(cx, k);
-  double* col2o = alloc_fast(cx, k);
-  double* taus = alloc(cx, k);  // global: read by back-transform helpers
-  int* piv = reinterpret_cast<int*>(alloc_fast(cx, k));
+  double* col2 = alloc(cx, k);  // global (as taus, piv): shared with team helpers
+  double* col2o = alloc(cx, k);
+  double* taus = alloc(cx, k);
+  int* piv = reinterpret_cast<int*>(alloc(cx, k));
   double* tau2 = alloc(cx, k);  // global: the second QR may run as a team
   if (!col2 || !col2o || !taus || !piv || !tau2) { release(cx, mk); return 0; }
   const int smem_before_g = cx.stop;
@@ -147,7 +147,7 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
   const double eps_m = 2.220446049250313e-16;
   double rem2 = 0.0;
   PhaseTimer tqp;
-  const int kp = pivoted_qr(k, k, G, k, eps_m * eps_m * core2, k, core2, col2, col2o, piv, taus, &rem2);
+  const int kp = pivoted_qr_team(cx, k, k, G, k, eps_m * eps_m * core2, k, core2, col2, col2o, piv, taus, &rem2);
   tqp.stop(cx, PH_QRCP);
   if (threadIdx.x == 0 && cx.flops && k >= 64) {  // stats: sum k, sum kp, count, sum k^3, sum kp^3
     atomicAdd(cx.flops + 48, (unsigned long long)k);

@@ -134,6 +134,55 @@ __device__ __noinline__ void build_t_full(Ctx& cx, int n, const double* S, int l
 }
 
 // ---------------------------------------------------------------------------
+// Full forward-columnwise T (n x n, ldt) of a block reflector with explicit
+// Y (m x n, ldy) whose diagonal QR_NB x QR_NB blocks T_JJ are already in T:
+//   T(0:j0, J) = -T(0:j0, 0:j0) S(0:j0, J) T_JJ,   S = Y^T Y.
+// Team form: phase 1 forms S(0:j0, J) for the TB_CW-column chunks a member
+// owns (trap: Y unit-lower-trapezoidal, so only rows >= j0 contribute);
+// barrier; phase 2 builds the rows of T in the TB_CW-row chunks it owns --
+// rows of T depend only on the same rows of earlier column blocks, so phase 2
+// needs no further synchronisation.  X_J = S(0:j0, J) T_JJ is formed by every
+// member.  Fixed chunks: results are bitwise independent of the team size.
+// ---------------------------------------------------------------------------
+constexpr int TB_CW = 64;
+
+template <class Bar>
+__device__ void build_t_multi(Ctx& cx, int n, int m, const double* Y, int ldy, bool trap, double* S, int lds,
+                              double* T, int ldt, int t, int team, Bar&& barrier) {
+  const int nch = (n + TB_CW - 1) / TB_CW;
+  for (int g = t; g < nch; g += team)
+    for (int j0 = max(g * TB_CW, QR_NB); j0 < min(n, (g + 1) * TB_CW); j0 += QR_NB) {
+      const int w = min(QR_NB, n - j0), r0 = trap ? j0 : 0;
+      gemm(true, false, j0, w, m - r0, 1.0, Y + r0, ldy, Y + r0 + (long long)j0 * ldy, ldy, 0.0,
+           S + (long long)j0 * lds, lds);
+    }
+  // strictly-lower blocks of own rows are zero
+  for (int g = t; g < nch; g += team) {
+    const int r0 = g * TB_CW, r1 = min(n, r0 + TB_CW);
+    for (int c = threadIdx.x >> 5; c < r1; c += NWARP) {
+      const int cb = (c / QR_NB) * QR_NB;
+      for (int r = max(r0, cb + QR_NB) + (threadIdx.x & 31); r < r1; r += 32) T[r + (long long)c * ldt] = 0.0;
+    }
+  }
+  barrier();
+  const Mark mk = mark(cx);
+  double* X = alloc(cx, (long long)n * QR_NB);
+  if (!X) return;
+  for (int j0 = QR_NB; j0 < n; j0 += QR_NB) {
+    const int w = min(QR_NB, n - j0);
+    bool any = false;
+    for (int g = t; g < nch && g * TB_CW < j0; g += team) any = true;
+    if (!any) continue;
+    gemm(false, false, j0, w, w, 1.0, S + (long long)j0 * lds, lds, T + j0 + (long long)j0 * ldt, ldt, 0.0, X, j0);
+    for (int g = t; g < nch && g * TB_CW < j0; g += team) {
+      const int r0 = g * TB_CW, nr = min(min(n, r0 + TB_CW), j0) - r0;
+      gemm(false, false, nr, w, j0, -1.0, T + r0, ldt, X, j0, 0.0, T + r0 + (long long)j0 * ldt, ldt);
+    }
+  }
+  release(cx, mk);
+}
+
+// ---------------------------------------------------------------------------
 // Blocked Householder QR of A (m x n, any shape).  k = min(m, n) reflectors.
 // On exit: R in the upper triangle, reflectors below, tau[0:k] (tau[j] = 0 for
 // j >= m), and per-panel T factors: Tp (QR_NB x k, panel p at column p*QR_NB,
@@ -291,12 +340,14 @@ __device__ __noinline__ void qr_apply(Ctx& cx, int m, int k, const double* A, in
 // n x n upper triangular, B k x n.  On exit R = R_new, B = Y (k x n), T full
 // n x n upper (ldt).
 // ---------------------------------------------------------------------------
-__device__ __noinline__ void tpqrt(Ctx& cx, int n, int k, double* R, int ldr, double* B, int ldb, double* T, int ldt) {
+// Panels only: R, Y (in B) and the diagonal QR_NB blocks of T; S (n x n,
+// ld n) is caller scratch.  The rest of T: build_t_multi with trap = false.
+__device__ __noinline__ void tpqrt_panels(Ctx& cx, int n, int k, double* R, int ldr, double* B, int ldb, double* T,
+                                          int ldt, double* S) {
   const long long mark = cx.top;
   double* tau = alloc(cx, n);
-  double* S = alloc(cx, (long long)n * n);
   double* W = alloc(cx, (long long)QR_NB * n);
-  if (!tau || !S || !W) { cx.top = mark; return; }
+  if (!tau || !W) { cx.top = mark; return; }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int c0 = 0; c0 < n; c0 += QR_NB) {
     const int w = min(QR_NB, n - c0);
@@ -354,10 +405,16 @@ __device__ __noinline__ void tpqrt(Ctx& cx, int n, int k, double* R, int ldr, do
       gemm(false, false, k, n2, w, -1.0, YJ, ldb, W, QR_NB, 1.0, BL, ldb);
     }
   }
-  // full T: S = Y^T Y (upper blocks needed), then blocked combine
-  gemm(true, false, n, n, k, 1.0, B, ldb, B, ldb, 0.0, S, n);
-  build_t_full(cx, n, S, n, tau, T, ldt);
   cx.top = mark;
+}
+
+__device__ __noinline__ void tpqrt(Ctx& cx, int n, int k, double* R, int ldr, double* B, int ldb, double* T, int ldt) {
+  const Mark mk = mark(cx);
+  double* S = alloc(cx, (long long)n * n);
+  if (!S) return;
+  tpqrt_panels(cx, n, k, R, ldr, B, ldb, T, ldt, S);
+  build_t_multi(cx, n, k, B, ldb, false, S, n, T, ldt, 0, 1, [] { __syncthreads(); });
+  release(cx, mk);
 }
 
 

@@ -334,8 +334,19 @@ __device__ __noinline__ bool jacobi_blocked(Ctx& cx, int rows, int ncols, double
 // is <= stop2, when min(m, n) steps are done, or (returning -1) when another
 // step would exceed max_steps.  col2/col2o/piv/taus are caller scratch
 // (n, n, n, min(m,n)).  *remaining2 receives the final remainder.
-__device__ __noinline__ int pivoted_qr(int m, int n, double* A, int lda, double stop2, int max_steps, double fro2,
-                                       double* col2, double* col2o, int* piv, double* taus, double* remaining2) {
+//
+// Team form: member t of `team` owns the PQ_CW-column chunks g with
+// g mod team == t.  Per step: every member picks the same pivot from col2;
+// the owner of position k swaps, forms the reflector and publishes it
+// (barrier); every member updates and downdates its own columns (barrier).
+// Per-column arithmetic does not depend on the owner, so the result is
+// bitwise the lone-CTA one.
+constexpr int PQ_CW = 32;
+
+template <class Bar>
+__device__ int pivoted_qr_multi(int m, int n, double* A, int lda, double stop2, int max_steps, double fro2,
+                                double* col2, double* col2o, int* piv, double* taus, double* remaining2, int t,
+                                int team, Bar&& barrier) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int limit = min(m, n);
   int rank = 0;
@@ -352,58 +363,64 @@ __device__ __noinline__ int pivoted_qr(int m, int n, double* A, int lda, double 
       if (v > bv) { bv = v; bi = c; }
     }
     const int j = cta_argmax(bv, bi);
-    if (j != k) {
-      double* ak = A + (long long)k * lda;
-      double* aj = A + (long long)j * lda;
-      for (int i = threadIdx.x; i < m; i += NT) { const double t = ak[i]; ak[i] = aj[i]; aj[i] = t; }
-      if (threadIdx.x == 0) {
-        double t = col2[k]; col2[k] = col2[j]; col2[j] = t;
-        t = col2o[k]; col2o[k] = col2o[j]; col2o[j] = t;
-        const int ti = piv[k]; piv[k] = piv[j]; piv[j] = ti;
-      }
-      __syncthreads();
-    }
     double* ak = A + (long long)k * lda;
-    double tau, beta;
-    house_gen(ak[k], ak + k + 1, m - k - 1, 1, tau, beta);
-    if (tau != 0.0) {
-      for (int l = k + 1 + warp; l < n; l += NWARP) {
-        double* al = A + (long long)l * lda;
-        double d = 0.0;
-        for (int i = k + 1 + lane; i < m; i += 32) d = fma(ak[i], al[i], d);
-        d = (warp_sum(d) + al[k]) * tau;
-        if (lane == 0) al[k] -= d;
-        for (int i = k + 1 + lane; i < m; i += 32) al[i] = fma(-d, ak[i], al[i]);
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) { ak[k] = beta; taus[k] = tau; }
-    __syncthreads();
-    rank += 1;
-    if (k + 1 < n) {
-      for (int l = k + 1 + threadIdx.x; l < n; l += NT) {
-        const double r = A[k + (long long)l * lda];
-        col2[l] -= r * r;
-      }
-      __syncthreads();
-      for (int l = k + 1 + warp; l < n; l += NWARP) {
-        if (col2[l] < 1e-14 * col2o[l]) {
-          const double* al = A + (long long)l * lda;
-          double s = 0.0;
-          for (int i = k + 1 + lane; i < m; i += 32) s = fma(al[i], al[i], s);
-          s = warp_sum(s);
-          if (lane == 0) col2[l] = s;
+    if ((k / PQ_CW) % team == t) {  // owner of position k: swap, reflector
+      if (j != k) {
+        double* aj = A + (long long)j * lda;
+        for (int i = threadIdx.x; i < m; i += NT) { const double x = ak[i]; ak[i] = aj[i]; aj[i] = x; }
+        if (threadIdx.x == 0) {
+          double x = col2[k]; col2[k] = col2[j]; col2[j] = x;
+          x = col2o[k]; col2o[k] = col2o[j]; col2o[j] = x;
+          const int ti = piv[k]; piv[k] = piv[j]; piv[j] = ti;
         }
+        __syncthreads();
       }
-      __syncthreads();
+      double tau, beta;
+      house_gen(ak[k], ak + k + 1, m - k - 1, 1, tau, beta);
+      if (threadIdx.x == 0) { ak[k] = beta; taus[k] = tau; }
     }
-    double s = 0.0;
-    for (int c = rank + threadIdx.x; c < n; c += NT) s += col2[c];
-    s = cta_sum(s);
-    remaining = rank < n ? fmax(s, 0.0) : 0.0;
+    barrier();
+    const double tau = taus[k];
+    rank += 1;
+    // update + downdate (+ exact recompute) of this member's columns l > k
+    for (int c = (k + 1) / PQ_CW; c * PQ_CW < n; ++c) {
+      if (c % team != t) continue;
+      const int l1 = min(n, (c + 1) * PQ_CW);
+      for (int l = max(c * PQ_CW, k + 1) + warp; l < l1; l += NWARP) {
+        double* al = A + (long long)l * lda;
+        if (tau != 0.0) {
+          double d = 0.0;
+          for (int i = k + 1 + lane; i < m; i += 32) d = fma(ak[i], al[i], d);
+          d = (warp_sum(d) + al[k]) * tau;
+          if (lane == 0) al[k] -= d;
+          for (int i = k + 1 + lane; i < m; i += 32) al[i] = fma(-d, ak[i], al[i]);
+        }
+        __syncwarp();
+        const double r = al[k];
+        double c2 = col2[l] - r * r;
+        if (c2 < 1e-14 * col2o[l]) {
+          double s2 = 0.0;
+          for (int i = k + 1 + lane; i < m; i += 32) s2 = fma(al[i], al[i], s2);
+          c2 = warp_sum(s2);
+        }
+        __syncwarp();
+        if (lane == 0) col2[l] = c2;
+      }
+    }
+    barrier();
+    double s2 = 0.0;
+    for (int c = rank + threadIdx.x; c < n; c += NT) s2 += col2[c];
+    s2 = cta_sum(s2);
+    remaining = rank < n ? fmax(s2, 0.0) : 0.0;
   }
   *remaining2 = remaining;
   return result < 0 ? -1 : rank;
+}
+
+__device__ __noinline__ int pivoted_qr(int m, int n, double* A, int lda, double stop2, int max_steps, double fro2,
+                                       double* col2, double* col2o, int* piv, double* taus, double* remaining2) {
+  return pivoted_qr_multi(m, n, A, lda, stop2, max_steps, fro2, col2, col2o, piv, taus, remaining2, 0, 1,
+                          [] { __syncthreads(); });
 }
 
 // Apply the first nref reflectors of a pivoted_qr factorization (vectors

@@ -52,9 +52,8 @@ __device__ void geqrt_inplace(Ctx& cx, int m, int n, double* A, int lda, double*
   const long long mark = cx.top;
   double* tau = alloc(cx, n);
   double* Tp = alloc(cx, (long long)QR_NB * n);
-  double* X = alloc(cx, (long long)n * QR_NB);
-  double* X2 = alloc(cx, (long long)n * QR_NB);
-  if (!tau || !Tp || !X || !X2) { cx.top = mark; return; }
+  double* S = alloc(cx, (long long)n * n);
+  if (!tau || !Tp || !S) { cx.top = mark; return; }
   {
     const QrMat M{A, tau, Tp, m, n, lda};
     qr_blocked_team(cx, &M, 1);
@@ -70,22 +69,17 @@ __device__ void geqrt_inplace(Ctx& cx, int m, int n, double* A, int lda, double*
       Y[i + (long long)j * ldy] = y;
     }
   __syncthreads();
-  // full forward-columnwise T from the panel T's: T(0:J0, J) = -T(0:J0,0:J0)
-  // (Y(:,0:J0)^T Y(:,J)) T_JJ, where Y(:,J) vanishes above row J0, so the
-  // inner products only run over rows J0..m
+  // full forward-columnwise T: diagonal blocks = the panel T's, the rest from
+  // T(0:J0, J) = -T(0:J0,0:J0) (Y(:,0:J0)^T Y(:,J)) T_JJ (Y(:,J) vanishes
+  // above row J0, so the inner products run over rows J0..m)
   for (int j0 = 0; j0 < n; j0 += QR_NB) {
     const int w = min(QR_NB, n - j0);
     const double* TJ = Tp + (long long)j0 * QR_NB;
     for (int c = threadIdx.x >> 5; c < w; c += NWARP)
-      for (int i = threadIdx.x & 31; i < n; i += 32)
-        T[i + (long long)(j0 + c) * ldt] = (i >= j0 && i < j0 + w) ? TJ[(i - j0) + c * QR_NB] : 0.0;
-    __syncthreads();
-    if (j0 > 0) {
-      gemm(true, false, j0, w, m - j0, 1.0, Y + j0, ldy, Y + j0 + (long long)j0 * ldy, ldy, 0.0, X, j0);
-      gemm(false, false, j0, w, w, 1.0, X, j0, TJ, QR_NB, 0.0, X2, j0);
-      gemm(false, false, j0, w, j0, -1.0, T, ldt, X2, j0, 0.0, T + (long long)j0 * ldt, ldt);
-    }
+      for (int i = threadIdx.x & 31; i < w; i += 32) T[j0 + i + (long long)(j0 + c) * ldt] = TJ[i + c * QR_NB];
   }
+  __syncthreads();
+  build_t_team(cx, n, m, Y, ldy, true, S, n, T, ldt);
   add_flops(cx, FK_PANEL_QR, qr_cost(m, n) + tgen_cost(m, n));
   cx.top = mark;
 }
@@ -152,9 +146,11 @@ __device__ void tiled_update(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf,
         tpqrt_small<32>(cx, b, r, rk.u, rk.ld, x.v, x.ld, T, b);
       } else {
         double* B = alloc(cx, (long long)r * b);
-        if (!B) return;
+        double* S = alloc(cx, (long long)b * b);
+        if (!B || !S) return;
         transpose_mat(b, r, x.v, x.ld, B, r);          // B = V_ik^T (r x b)
-        tpqrt(cx, b, r, rk.u, rk.ld, B, r, T, b);
+        tpqrt_panels(cx, b, r, rk.u, rk.ld, B, r, T, b, S);
+        build_t_team(cx, b, r, B, r, false, S, b, T, b);
         transpose_mat(r, b, B, r, x.v, x.ld);          // Ytilde.v = Y^T stored in the V slab
       }
       add_flops(cx, FK_UPDATE_QR, qr_cost(b + r, b) + tgen_cost(b + r, b));
@@ -163,7 +159,12 @@ __device__ void tiled_update(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf,
   } else {
     double* Yd = rf.pool + rf.y_off[c];
     copy_mat(b, b, x.u, x.ld, Yd, b);
-    tpqrt(cx, b, b, rk.u, rk.ld, Yd, b, T, b);
+    {
+      double* S = alloc(cx, (long long)b * b);
+      if (!S) return;
+      tpqrt_panels(cx, b, b, rk.u, rk.ld, Yd, b, T, b, S);
+      build_t_team(cx, b, b, Yd, b, false, S, b, T, b);
+    }
     zero_mat(b, b, x.u, x.ld);
     add_flops(cx, FK_UPDATE_QR, qr_cost(2 * b, b) + tgen_cost(2 * b, b));
     if (threadIdx.x == 0) rf.yrank[c] = -1;

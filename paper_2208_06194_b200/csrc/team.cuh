@@ -12,6 +12,11 @@
 //   TK_JACOBI jacobi_blocked's block Jacobi of the core: the block pairs of
 //             one round-robin round touch disjoint columns, so member t takes
 //             pairs t, t+T, ... and a team barrier separates rounds;
+//   TK_QRCP   the core's column-pivoted QR: 32-column chunks, two barriers
+//             per pivot step (reflector published / columns updated);
+//   TK_TBUILD full compact-WY T of GEQRT / TPQRT (householder.cuh
+//             build_t_multi): Gram blocks by column chunk, then T rows by row
+//             chunk with no further synchronisation;
 //   TK_BACK   the back-transform U_C = Q_U [Q1 J_r; 0], V_C = Q_V [Q2 W_r; 0]
 //             in fixed 32-column chunks, chunk c on member c mod T.
 // Every kind performs exactly the single-CTA operation sequence on the same
@@ -38,8 +43,9 @@ constexpr long long TEAM_WAIT_CYCLES = 40000;           // leader's wait for hel
 constexpr long long TEAM_SPIN_TIMEOUT = 20000000000LL;  // ~10 s of spinning -> abort
 constexpr int BACK_CW = 32;                              // back-transform column chunk
 constexpr int TEAM_BACK_MIN = 64;  // Q_U width from which the back-transform splits
+constexpr int TEAM_QRCP_MIN = 128;  // core order from which the pivoted QR splits
 
-enum TeamKind : int { TK_JACOBI = 1, TK_BACK = 2, TK_QRB = 3 };
+enum TeamKind : int { TK_JACOBI = 1, TK_BACK = 2, TK_QRB = 3, TK_QRCP = 4, TK_TBUILD = 5 };
 
 struct __align__(128) TeamJob {
   int state;  // 0 free, 9 being set up, 2 running (team size published)
@@ -53,6 +59,7 @@ struct __align__(128) TeamJob {
   int kind;
   int iv[12];
   double* pv[16];
+  double dv[4];
 };
 
 struct TeamCtx {
@@ -379,6 +386,68 @@ __device__ void qr_blocked_team(Ctx& cx, const QrMat* mats, int nm) {
   }
 }
 
+// ---- TK_QRCP -----------------------------------------------------------------
+// iv: m, n, lda, max_steps; pv: A, col2, col2o, piv (int*), taus; dv: stop2, fro2
+__device__ void team_qrcp_member(Ctx& cx, TeamJob* job, int t, int team) {
+  double rem;
+  pivoted_qr_multi(job->iv[0], job->iv[1], job->pv[0], job->iv[2], job->dv[0], job->iv[3], job->dv[1], job->pv[1],
+                   job->pv[2], reinterpret_cast<int*>(job->pv[3]), job->pv[4], &rem, t, team,
+                   [&] { team_barrier(cx, job, team); });
+}
+
+// pivoted_qr with a team when the operands are global and the core is large
+__device__ int pivoted_qr_team(Ctx& cx, int m, int n, double* A, int lda, double stop2, int max_steps, double fro2,
+                               double* col2, double* col2o, int* piv, double* taus, double* remaining2) {
+  const bool global = !in_smem(cx, A) && !in_smem(cx, col2) && !in_smem(cx, col2o) &&
+                      !in_smem(cx, reinterpret_cast<double*>(piv)) && !in_smem(cx, taus);
+  TeamJob* job = (n >= TEAM_QRCP_MIN && global) ? team_reserve(cx) : nullptr;
+  int team = 1;
+  if (job) {
+    if (threadIdx.x == 0) {
+      job->kind = TK_QRCP;
+      job->iv[0] = m; job->iv[1] = n; job->iv[2] = lda; job->iv[3] = max_steps;
+      job->pv[0] = A; job->pv[1] = col2; job->pv[2] = col2o; job->pv[3] = reinterpret_cast<double*>(piv);
+      job->pv[4] = taus;
+      job->dv[0] = stop2; job->dv[1] = fro2;
+    }
+    team = team_launch(cx, job, min(TEAM_MAX, (n + PQ_CW - 1) / PQ_CW));
+  }
+  if (team == 1) return pivoted_qr(m, n, A, lda, stop2, max_steps, fro2, col2, col2o, piv, taus, remaining2);
+  const int r = pivoted_qr_multi(m, n, A, lda, stop2, max_steps, fro2, col2, col2o, piv, taus, remaining2, 0, team,
+                                 [&] { team_barrier(cx, job, team); });
+  team_finish(cx, job, team);
+  return r;
+}
+
+// ---- TK_TBUILD ---------------------------------------------------------------
+// iv: n, m, ldy, trap, lds, ldt; pv: Y, S, T
+__device__ void team_tbuild_member(Ctx& cx, TeamJob* job, int t, int team) {
+  build_t_multi(cx, job->iv[0], job->iv[1], job->pv[0], job->iv[2], job->iv[3] != 0, job->pv[1], job->iv[4],
+                job->pv[2], job->iv[5], t, team, [&] { team_barrier(cx, job, team); });
+}
+
+__device__ void build_t_team(Ctx& cx, int n, int m, const double* Y, int ldy, bool trap, double* S, int lds, double* T,
+                             int ldt) {
+  const int nch = (n + TB_CW - 1) / TB_CW;
+  const bool global = !in_smem(cx, Y) && !in_smem(cx, S) && !in_smem(cx, T);
+  TeamJob* job = (nch >= 2 && global) ? team_reserve(cx) : nullptr;
+  int team = 1;
+  if (job) {
+    if (threadIdx.x == 0) {
+      job->kind = TK_TBUILD;
+      job->iv[0] = n; job->iv[1] = m; job->iv[2] = ldy; job->iv[3] = trap; job->iv[4] = lds; job->iv[5] = ldt;
+      job->pv[0] = const_cast<double*>(Y); job->pv[1] = S; job->pv[2] = T;
+    }
+    team = team_launch(cx, job, min(TEAM_MAX, nch));
+  }
+  if (team > 1) {
+    build_t_multi(cx, n, m, Y, ldy, trap, S, lds, T, ldt, 0, team, [&] { team_barrier(cx, job, team); });
+    team_finish(cx, job, team);
+  } else {
+    build_t_multi(cx, n, m, Y, ldy, trap, S, lds, T, ldt, 0, 1, [] { __syncthreads(); });
+  }
+}
+
 // ---- helper side -------------------------------------------------------------
 // thread 0 of an idle CTA: claim a ticket and join its job.
 // Returns the job slot (>= 0) with *member set, or -1.
@@ -468,6 +537,8 @@ __device__ void team_help(Ctx& cx, TeamCtx* tc, int slot, int member) {
     case TK_JACOBI: team_jacobi_member(cx, job, member, team); break;
     case TK_BACK: team_back_member(cx, job, member, team); break;
     case TK_QRB: team_qrb_member(cx, job, member, team); break;
+    case TK_QRCP: team_qrcp_member(cx, job, member, team); break;
+    case TK_TBUILD: team_tbuild_member(cx, job, member, team); break;
     default: break;
   }
   __syncthreads();
