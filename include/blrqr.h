@@ -170,7 +170,9 @@ int blrqr_tiled_run(const blrqr_grid* g, const blrqr_refl* rf, const blrqr_task*
 /* Dynamic tiled scheduler: the same DAG as explicit successor lists.
  * blrqr_tiled_dag_size returns the task count (and *nedges); blrqr_tiled_dag
  * fills tasks (canonical sweep order), initial in-degrees, CSR successors and
- * a priority flag (1 = DiagQR/UpdateQR).  blrqr_tiled_run_dag runs the whole
+ * priority flags (bit 0: high-priority ready ring -- DiagQR, UpdateQR and the
+ * R_{k,k+1} TrapA chain; bit 1: the task may recruit a CTA team -- unit-weight
+ * slack <= 1 on the DAG).  blrqr_tiled_run_dag runs the whole
  * factorization with one persistent CTA per SM pulling ready tasks; work_dev
  * is 3*ntasks + 8 ints of scratch. */
 int64_t blrqr_tiled_dag_size(int p, int q, int64_t* nedges);
@@ -180,9 +182,11 @@ void blrqr_debug_trace(void* dev_buf);
 /* Debug: per task of subsequent dynamic runs, 16 uint64 SM-cycle counters
  * per phase (PHASES in _lib.py) into a zeroed device buffer (NULL disables). */
 void blrqr_debug_phase_trace(void* dev_buf);
-/* CTA teams in the dynamic scheduler (default on): idle CTAs join the
- * one-sided Jacobi of large rounded-addition cores.  The rotation sequence
- * is the single-CTA one, so results do not depend on this switch. */
+/* CTA teams (default on): idle CTAs of the persistent / batched kernels join
+ * the QRs, pivoted QR, Jacobi SVD, back-transform and T builds of large
+ * operations (team.cuh).  Every team performs the lone-CTA operation
+ * sequence, so results do not depend on this switch.  enable = 0 off, 1 on,
+ * 2 + s: on, and DAG tasks with slack <= s may recruit (default s = 1). */
 void blrqr_set_teams(int enable);
 /* Debug: one-sided Jacobi of X (rows x ncols, column-major, ld rows) with J
  * (ncols x ncols) -- mode 0 single-CTA blocked, 1 single-CTA column pairs,

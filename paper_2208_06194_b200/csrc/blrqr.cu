@@ -396,7 +396,7 @@ __device__ __forceinline__ long long global_ns() {
 __device__ __forceinline__ int ld_volatile(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
 
 __device__ __forceinline__ void dag_push(const DagDev& d, int t) {
-  const int c = d.prio[t] ? 0 : 1;
+  const int c = (d.prio[t] & 1) ? 0 : 1;
   const int slot = atomicAdd(d.ctr + 2 * c + 1, 1);
   atomicExch(d.q[c] + slot, t);
 }
@@ -458,6 +458,7 @@ __global__ void __launch_bounds__(NT, 1) k_tiled_dag(DagDev d, blrqr_grid g, blr
       continue;
     }
     const blrqr_task tk = d.tasks[t];
+    cx.team = (d.prio[t] & 2) ? d.team : nullptr;  // only near-critical tasks recruit helpers
     if (d.trace && threadIdx.x == 0) d.trace[3 * (long long)t] = global_ns();
     cx.tph = d.ptrace ? d.ptrace + 16LL * t : nullptr;
     PhaseTimer tt;
@@ -576,6 +577,7 @@ static void init_kernels() {
 #define INIT_KERNELS() init_kernels()
 
 static int g_teams_enabled = 1;
+static int g_team_slack = 1 << 20;  // DAG tasks with unit-weight slack <= this may form teams (all by default: measured best)
 
 // Team-job table + ticket ring + two task counters, one per (device, stream)
 // so concurrent launches on different streams never share them; allocated
@@ -892,7 +894,10 @@ static long long* g_dag_trace = nullptr;
 void blrqr_debug_trace(void* dev_buf) { g_dag_trace = reinterpret_cast<long long*>(dev_buf); }
 static unsigned long long* g_phase_trace = nullptr;
 void blrqr_debug_phase_trace(void* dev_buf) { g_phase_trace = reinterpret_cast<unsigned long long*>(dev_buf); }
-void blrqr_set_teams(int enable) { g_teams_enabled = enable ? 1 : 0; }
+void blrqr_set_teams(int enable) {
+  g_teams_enabled = enable ? 1 : 0;
+  if (enable > 1) g_team_slack = enable - 2;  // tuning: enable = 2 + max slack (1 << 20: every task)
+}
 
 
 
@@ -917,10 +922,23 @@ int blrqr_tiled_dag(int p, int q, blrqr_task* tasks_host, int* indeg_host, int64
   std::copy(indeg.begin(), indeg.end(), indeg_host);
   std::copy(off.begin(), off.end(), succ_off_host);
   std::copy(succ.begin(), succ.end(), succ_host);
-  // high priority: DiagQR, UpdateQR and the R_kj chain of the next panel column
-  for (size_t t = 0; t < tasks.size(); ++t)
-    prio_host[t] = (tasks[t].kind == 0 || tasks[t].kind == 2 || (tasks[t].kind == 4 && tasks[t].j == tasks[t].k + 1))
-                       ? 1 : 0;
+  // unit-weight slack of every task: the critical chains (DiagQR -> UpdateQR
+  // -> the column-(k+1) traps -> DiagQR(k+1)) have slack 0
+  const int n = (int)tasks.size();
+  std::vector<int> top(n, 0), bot(n, 0);
+  for (int t = 0; t < n; ++t)  // canonical order is topological
+    for (int64_t e = off[t]; e < off[t + 1]; ++e) top[succ[e]] = std::max(top[succ[e]], top[t] + 1);
+  for (int t = n - 1; t >= 0; --t)
+    for (int64_t e = off[t]; e < off[t + 1]; ++e) bot[t] = std::max(bot[t], bot[succ[e]] + 1);
+  int cp = 0;
+  for (int t = 0; t < n; ++t) cp = std::max(cp, top[t] + bot[t]);
+  // bit 0: high-priority ready ring (DiagQR, UpdateQR, the R_kj chain of the
+  // next panel column); bit 1: may form CTA teams (slack <= 1)
+  for (int t = 0; t < n; ++t) {
+    const int slack = cp - top[t] - bot[t];
+    const bool hi = tasks[t].kind == 0 || tasks[t].kind == 2 || (tasks[t].kind == 4 && tasks[t].j == tasks[t].k + 1);
+    prio_host[t] = (hi ? 1 : 0) | (slack <= g_team_slack ? 2 : 0);
+  }
   return 0;
 }
 

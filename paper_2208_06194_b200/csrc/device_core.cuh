@@ -199,19 +199,42 @@ __device__ __forceinline__ int cta_argmax(double v, int idx) {
 // ---------------------------------------------------------------------------
 
 // B(0:m,0:n) = alpha * A(0:m,0:n)   (warp per column, lanes down the rows)
+// Column-parallel element loops: a column is handled by `wpc` warps (all 16
+// warps stay busy for narrow matrices); each lane keeps 4 loads in flight
+// (L2 latency, not bandwidth, bounds a single CTA's copies).
+struct ColSplit {
+  int wpc, group, ngroups, i0, stride;
+  __device__ __forceinline__ ColSplit(int n) {
+    const int warp = threadIdx.x >> 5;
+    wpc = n >= NWARP ? 1 : (n >= NWARP / 2 ? 2 : (n >= NWARP / 4 ? 4 : (n >= NWARP / 8 ? 8 : 16)));
+    group = warp / wpc;
+    ngroups = NWARP / wpc;
+    i0 = (threadIdx.x & 31) + 32 * (warp % wpc);
+    stride = 32 * wpc;
+  }
+};
+
 __device__ void copy_mat(int m, int n, const double* A, int lda, double* B, int ldb, double alpha = 1.0) {
-  for (int j = threadIdx.x >> 5; j < n; j += NWARP) {
+  const ColSplit cs(n);
+  const int S = cs.stride;
+  for (int j = cs.group; j < n; j += cs.ngroups) {
     const double* a = A + (long long)j * lda;
     double* b = B + (long long)j * ldb;
-    for (int i = threadIdx.x & 31; i < m; i += 32) b[i] = alpha * a[i];
+    int i = cs.i0;
+    for (; i + 3 * S < m; i += 4 * S) {
+      const double x0 = a[i], x1 = a[i + S], x2 = a[i + 2 * S], x3 = a[i + 3 * S];
+      b[i] = alpha * x0; b[i + S] = alpha * x1; b[i + 2 * S] = alpha * x2; b[i + 3 * S] = alpha * x3;
+    }
+    for (; i < m; i += S) b[i] = alpha * a[i];
   }
   __syncthreads();
 }
 
 __device__ void zero_mat(int m, int n, double* A, int lda) {
-  for (int j = threadIdx.x >> 5; j < n; j += NWARP) {
+  const ColSplit cs(n);
+  for (int j = cs.group; j < n; j += cs.ngroups) {
     double* a = A + (long long)j * lda;
-    for (int i = threadIdx.x & 31; i < m; i += 32) a[i] = 0.0;
+    for (int i = cs.i0; i < m; i += cs.stride) a[i] = 0.0;
   }
   __syncthreads();
 }

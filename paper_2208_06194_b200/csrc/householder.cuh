@@ -71,14 +71,20 @@ __device__ __forceinline__ void qr_panel_unblocked(int m, int c0, int w, double*
 // ldy) as an explicit unit-lower-trapezoidal block: Y(i, jj) for i in [0, m-c0).
 __device__ void extract_y(int m, int c0, int w, const double* A, int lda, double* Y, int ldy) {
   const int h = m - c0;
-  const long long tot = (long long)h * w;
-  for (long long e = threadIdx.x; e < tot; e += NT) {
-    const int i = (int)(e % h), jj = (int)(e / h);
-    double v;
-    if (i < jj) v = 0.0;
-    else if (i == jj) v = 1.0;
-    else v = A[(c0 + i) + (long long)(c0 + jj) * lda];
-    Y[i + (long long)jj * ldy] = v;
+  const ColSplit cs(w);
+  const int S = cs.stride;
+  for (int jj = cs.group; jj < w; jj += cs.ngroups) {
+    const double* a = A + c0 + (long long)(c0 + jj) * lda;
+    double* y = Y + (long long)jj * ldy;
+    int i = cs.i0;
+    for (; i + 3 * S < h; i += 4 * S) {
+      const double x0 = a[i], x1 = a[i + S], x2 = a[i + 2 * S], x3 = a[i + 3 * S];
+      y[i] = i < jj ? 0.0 : (i == jj ? 1.0 : x0);
+      y[i + S] = i + S < jj ? 0.0 : (i + S == jj ? 1.0 : x1);
+      y[i + 2 * S] = i + 2 * S < jj ? 0.0 : (i + 2 * S == jj ? 1.0 : x2);
+      y[i + 3 * S] = i + 3 * S < jj ? 0.0 : (i + 3 * S == jj ? 1.0 : x3);
+    }
+    for (; i < h; i += S) y[i] = i < jj ? 0.0 : (i == jj ? 1.0 : a[i]);
   }
   __syncthreads();
 }
@@ -340,72 +346,105 @@ __device__ __noinline__ void qr_apply(Ctx& cx, int m, int k, const double* A, in
 // n x n upper triangular, B k x n.  On exit R = R_new, B = Y (k x n), T full
 // n x n upper (ldt).
 // ---------------------------------------------------------------------------
-// Panels only: R, Y (in B) and the diagonal QR_NB blocks of T; S (n x n,
-// ld n) is caller scratch.  The rest of T: build_t_multi with trap = false.
-__device__ __noinline__ void tpqrt_panels(Ctx& cx, int n, int k, double* R, int ldr, double* B, int ldb, double* T,
-                                          int ldt, double* S) {
-  const long long mark = cx.top;
-  double* tau = alloc(cx, n);
-  double* W = alloc(cx, (long long)QR_NB * n);
-  if (!tau || !W) { cx.top = mark; return; }
+// Panel J of the TP factorization: reflectors of columns c0..c0+w-1 (the
+// in-panel updates included), S_J = Y_J^T Y_J into S's diagonal block and
+// T_JJ into T.
+__device__ void tp_factor_panel(int n, int k, double* R, int ldr, double* B, int ldb, double* T, int ldt, double* S,
+                                double* tau, int c0, int w) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int c0 = 0; c0 < n; c0 += QR_NB) {
-    const int w = min(QR_NB, n - c0);
-    for (int jj = 0; jj < w; ++jj) {
-      const int j = c0 + jj;
-      double* bj = B + (long long)j * ldb;
-      double t, bta;
-      house_gen(R[j + (long long)j * ldr], bj, k, 1, t, bta);
-      if (threadIdx.x == 0) { tau[j] = t; R[j + (long long)j * ldr] = bta; }
-      __syncthreads();
-      if (t != 0.0) {
-        for (int l = j + 1 + warp; l < c0 + w; l += NWARP) {
-          double* bl = B + (long long)l * ldb;
-          double d = 0.0;
-          for (int i = lane; i < k; i += 32) d = fma(bj[i], bl[i], d);
-          d = (warp_sum(d) + R[j + (long long)l * ldr]) * t;
-          if (lane == 0) R[j + (long long)l * ldr] -= d;
-          for (int i = lane; i < k; i += 32) bl[i] = fma(-d, bj[i], bl[i]);
-        }
+  for (int jj = 0; jj < w; ++jj) {
+    const int j = c0 + jj;
+    double* bj = B + (long long)j * ldb;
+    double t, bta;
+    house_gen(R[j + (long long)j * ldr], bj, k, 1, t, bta);
+    if (threadIdx.x == 0) { tau[j] = t; R[j + (long long)j * ldr] = bta; }
+    __syncthreads();
+    if (t != 0.0) {
+      for (int l = j + 1 + warp; l < c0 + w; l += NWARP) {
+        double* bl = B + (long long)l * ldb;
+        double d = 0.0;
+        for (int i = lane; i < k; i += 32) d = fma(bj[i], bl[i], d);
+        d = (warp_sum(d) + R[j + (long long)l * ldr]) * t;
+        if (lane == 0) R[j + (long long)l * ldr] -= d;
+        for (int i = lane; i < k; i += 32) bl[i] = fma(-d, bj[i], bl[i]);
       }
-      __syncthreads();
     }
-    // panel T (w x w) into T's diagonal block, from S_J = Y_J^T Y_J
-    gemm(true, false, w, w, k, 1.0, B + (long long)c0 * ldb, ldb, B + (long long)c0 * ldb, ldb, 0.0,
-         S + c0 + (long long)c0 * n, n);
-    t_block_recurrence(c0, w, S, n, tau, T, ldt);
-    const int n2 = n - (c0 + w);
-    if (n2 > 0) {
-      double* RJL = R + c0 + (long long)(c0 + w) * ldr;
-      double* BL = B + (long long)(c0 + w) * ldb;
-      const double* YJ = B + (long long)c0 * ldb;
-      const double* TJ = T + c0 + (long long)c0 * ldt;
-      // W = R_JL + Y_J^T B_L
-      copy_mat(w, n2, RJL, ldr, W, QR_NB);
-      gemm(true, false, w, n2, k, 1.0, YJ, ldb, BL, ldb, 1.0, W, QR_NB);
-      // W <- T_J^T W  (in place, per column)
-      for (long long e = threadIdx.x; e < (long long)n2; e += NT) {
-        double* wc = W + e * QR_NB;
-        double tmp[QR_NB];
-        for (int a = 0; a < w; ++a) tmp[a] = wc[a];
-        for (int a = w - 1; a >= 0; --a) {
-          double s = 0.0;
-          for (int b2 = 0; b2 <= a; ++b2) s = fma(TJ[b2 + (long long)a * ldt], tmp[b2], s);
-          wc[a] = s;
-        }
-      }
-      __syncthreads();
-      // R_JL -= W ; B_L -= Y_J W
-      for (int c = threadIdx.x >> 5; c < n2; c += NWARP)
-        for (int a = threadIdx.x & 31; a < w; a += 32) {
-        const long long e = (long long)c * w + a;
-        RJL[a + (long long)c * ldr] -= W[a + (long long)c * QR_NB];
-      }
-      __syncthreads();
-      gemm(false, false, k, n2, w, -1.0, YJ, ldb, W, QR_NB, 1.0, BL, ldb);
+    __syncthreads();
+  }
+  gemm(true, false, w, w, k, 1.0, B + (long long)c0 * ldb, ldb, B + (long long)c0 * ldb, ldb, 0.0,
+       S + c0 + (long long)c0 * n, n);
+  t_block_recurrence(c0, w, S, n, tau, T, ldt);
+}
+
+// [R(J, L); B(:, L)] <- H_J^T [R(J, L); B(:, L)] for columns L = [col0, col1)
+__device__ void tp_apply_panel(int k, double* R, int ldr, double* B, int ldb, const double* T, int ldt, int c0, int w,
+                               int col0, int col1, double* W) {
+  const int n2 = col1 - col0;
+  if (n2 <= 0) return;
+  double* RJL = R + c0 + (long long)col0 * ldr;
+  double* BL = B + (long long)col0 * ldb;
+  const double* YJ = B + (long long)c0 * ldb;
+  const double* TJ = T + c0 + (long long)c0 * ldt;
+  copy_mat(w, n2, RJL, ldr, W, QR_NB);  // W = R_JL + Y_J^T B_L
+  gemm(true, false, w, n2, k, 1.0, YJ, ldb, BL, ldb, 1.0, W, QR_NB);
+  for (int e = threadIdx.x; e < n2; e += NT) {  // W <- T_J^T W
+    double* wc = W + (long long)e * QR_NB;
+    double tmp[QR_NB];
+    for (int a = 0; a < w; ++a) tmp[a] = wc[a];
+    for (int a = w - 1; a >= 0; --a) {
+      double s = 0.0;
+      for (int b2 = 0; b2 <= a; ++b2) s = fma(TJ[b2 + (long long)a * ldt], tmp[b2], s);
+      wc[a] = s;
     }
   }
-  cx.top = mark;
+  __syncthreads();
+  for (int c = threadIdx.x >> 5; c < n2; c += NWARP)  // R_JL -= W
+    for (int a = threadIdx.x & 31; a < w; a += 32) RJL[a + (long long)c * ldr] -= W[a + (long long)c * QR_NB];
+  __syncthreads();
+  gemm(false, false, k, n2, w, -1.0, YJ, ldb, W, QR_NB, 1.0, BL, ldb);  // B_L -= Y_J W
+}
+
+// Panels of the TP factorization by member t of a team (lone CTA: t = 0,
+// team = 1): fixed QR_CW-column chunks, look-ahead, one barrier per panel --
+// the qr_blocked_multi pattern.  S (n x n, ld n) and tau (n) are scratch
+// visible to the whole team; on exit R, Y (in B) and T's diagonal blocks.
+template <class Bar>
+__device__ void tpqrt_panels_multi(Ctx& cx, int n, int k, double* R, int ldr, double* B, int ldb, double* T, int ldt,
+                                   double* S, double* tau, int t, int team, Bar&& barrier) {
+  const Mark mk = mark(cx);
+  double* W = alloc_fast(cx, (long long)QR_NB * QR_CW);
+  if (!W) return;
+  const int np = (n + QR_NB - 1) / QR_NB, clast = (n - 1) / QR_CW;
+  auto owns = [&](int c) { return c % team == t; };
+  if (n > 0 && owns(0)) tp_factor_panel(n, k, R, ldr, B, ldb, T, ldt, S, tau, 0, min(QR_NB, n));
+  barrier();
+  for (int p = 0; p < np; ++p) {
+    const int c0 = p * QR_NB, w = min(QR_NB, n - c0), nxt = c0 + w;
+    if (nxt < n) {
+      int done = -1;
+      if (owns(nxt / QR_CW)) {  // look-ahead: next panel's chunk first
+        done = nxt / QR_CW;
+        tp_apply_panel(k, R, ldr, B, ldb, T, ldt, c0, w, nxt, min((done + 1) * QR_CW, n), W);
+        tp_factor_panel(n, k, R, ldr, B, ldb, T, ldt, S, tau, nxt, min(QR_NB, n - nxt));
+      }
+      for (int c = nxt / QR_CW; c <= clast; ++c)
+        if (c != done && owns(c))
+          tp_apply_panel(k, R, ldr, B, ldb, T, ldt, c0, w, max(c * QR_CW, nxt), min((c + 1) * QR_CW, n), W);
+    }
+    barrier();
+  }
+  release(cx, mk);
+}
+
+// Panels only (lone CTA); S (n x n, ld n) is caller scratch.  The rest of T:
+// build_t_multi with trap = false.
+__device__ __noinline__ void tpqrt_panels(Ctx& cx, int n, int k, double* R, int ldr, double* B, int ldb, double* T,
+                                          int ldt, double* S) {
+  const Mark mk = mark(cx);
+  double* tau = alloc(cx, n);
+  if (!tau) return;
+  tpqrt_panels_multi(cx, n, k, R, ldr, B, ldb, T, ldt, S, tau, 0, 1, [] { __syncthreads(); });
+  release(cx, mk);
 }
 
 __device__ __noinline__ void tpqrt(Ctx& cx, int n, int k, double* R, int ldr, double* B, int ldb, double* T, int ldt) {

@@ -100,10 +100,30 @@ __device__ __noinline__ void jacobi_cols(int rows, int ncols, double* X, int ldx
   __syncthreads();
 }
 
+// Warp-wide column copies between global memory (through L2, 4 loads in
+// flight per lane) and the shared arena.
+__device__ __forceinline__ void warp_ld_cg(double* dst, const double* src, int n, int lane) {
+  int i = lane;
+  for (; i + 96 < n; i += 128) {
+    const double a0 = __ldcg(src + i), a1 = __ldcg(src + i + 32), a2 = __ldcg(src + i + 64), a3 = __ldcg(src + i + 96);
+    dst[i] = a0; dst[i + 32] = a1; dst[i + 64] = a2; dst[i + 96] = a3;
+  }
+  for (; i < n; i += 32) dst[i] = __ldcg(src + i);
+}
+__device__ __forceinline__ void warp_st_cg(double* dst, const double* src, int n, int lane) {
+  int i = lane;
+  for (; i + 96 < n; i += 128) {
+    const double a0 = src[i], a1 = src[i + 32], a2 = src[i + 64], a3 = src[i + 96];
+    __stcg(dst + i, a0); __stcg(dst + i + 32, a1); __stcg(dst + i + 64, a2); __stcg(dst + i + 96, a3);
+  }
+  for (; i < n; i += 32) __stcg(dst + i, src[i]);
+}
+
 // Jacobi rotation of one column pair (p, q): returns true if rotated.
 __device__ __forceinline__ void jac_dots(const double* gp, const double* gq, int rows, int lane, double& a, double& b,
                                          double& g) {
   a = 0.0; b = 0.0; g = 0.0;
+#pragma unroll 4
   for (int i = lane; i < rows; i += 32) {
     const double x = gp[i], y = gq[i];
     a = fma(x, x, a);
@@ -124,6 +144,7 @@ __device__ __forceinline__ bool jac_angle(double a, double b, double g, double t
   return true;
 }
 __device__ __forceinline__ void jac_rotate(double* xp, double* xq, int n, int lane, double c, double s) {
+#pragma unroll 4
   for (int i = lane; i < n; i += 32) {
     const double x = xp[i], y = xq[i];
     xp[i] = c * x - s * y;
@@ -138,6 +159,119 @@ __device__ __forceinline__ void rr_pair(int pi, int rnd, int kk, int& p, int& q)
   if (b >= kk - 1) b -= kk - 1;
   q = 1 + b;
   if (p > q) { const int t = p; p = q; q = t; }
+}
+
+// One warp, one column pair (p, q) of a staged block: the pair's X columns
+// stay in registers between the inner products and the rotation (RPL rows
+// per lane, rows <= 32*RPL); J's columns are rotated in place.  Same
+// arithmetic as jac_dots / jac_angle / jac_rotate.
+template <int RPL>
+__device__ __forceinline__ bool jac_pair_reg(double* xp, double* xq, int rows, double* jp, double* jq, int nj, int lane,
+                                             double tol2) {
+  double xr[RPL], yr[RPL];
+  double a = 0.0, b = 0.0, g = 0.0;
+#pragma unroll
+  for (int r = 0; r < RPL; ++r) {
+    const int i = lane + 32 * r;
+    xr[r] = i < rows ? xp[i] : 0.0;
+    yr[r] = i < rows ? xq[i] : 0.0;
+  }
+#pragma unroll
+  for (int r = 0; r < RPL; ++r) {
+    if (lane + 32 * r < rows) {
+      a = fma(xr[r], xr[r], a);
+      b = fma(yr[r], yr[r], b);
+      g = fma(xr[r], yr[r], g);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+    g += __shfl_xor_sync(0xffffffffu, g, o);
+  }
+  double c, s;
+  if (!jac_angle(a, b, g, tol2, c, s)) return false;
+#pragma unroll
+  for (int r = 0; r < RPL; ++r) {
+    const int i = lane + 32 * r;
+    if (i < rows) {
+      xp[i] = c * xr[r] - s * yr[r];
+      xq[i] = s * xr[r] + c * yr[r];
+    }
+  }
+  jac_rotate(jp, jq, nj, lane, c, s);
+  return true;
+}
+
+// Full cyclic sweep over the nc staged columns of one block pair (Xs rows x
+// nc, Js nj x nc, both in shared memory), one warp per column pair per
+// round-robin round.  Returns true (in every thread) if any pair rotated.
+template <int RPL>
+__device__ bool block_pair_sweep_t(double* Xs, int rows, double* Js, int nj, int nc, double tol2) {
+  __shared__ int s_any;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) s_any = 0;
+  __syncthreads();
+  const int kk = (nc + 1) & ~1;
+  bool rot = false;
+  for (int r2 = 0; r2 < kk - 1; ++r2) {
+    for (int pi = warp; pi < kk / 2; pi += NWARP) {
+      int p, q;
+      rr_pair(pi, r2, kk, p, q);
+      if (q >= nc) continue;
+      rot |= jac_pair_reg<RPL>(Xs + p * rows, Xs + q * rows, rows, Js + p * nj, Js + q * nj, nj, lane, tol2);
+    }
+    __syncthreads();
+  }
+  if (rot && lane == 0) s_any = 1;
+  __syncthreads();
+  const bool any = s_any != 0;
+  __syncthreads();
+  return any;
+}
+
+// Xs, Js: shared-arena pointers (passed as offsets from dyn_smem so the
+// loads compile to LDS inside this non-inlined function).
+__device__ __noinline__ bool block_pair_sweep_off(int xoff, int rows, int joff, int nj, int nc, double tol2) {
+  double* Xs = dyn_smem + xoff;
+  double* Js = dyn_smem + joff;
+  if (rows <= 64) return block_pair_sweep_t<2>(Xs, rows, Js, nj, nc, tol2);
+  if (rows <= 128) return block_pair_sweep_t<4>(Xs, rows, Js, nj, nc, tol2);
+  if (rows <= 256) return block_pair_sweep_t<8>(Xs, rows, Js, nj, nc, tol2);
+  if (rows <= 384) return block_pair_sweep_t<12>(Xs, rows, Js, nj, nc, tol2);
+  if (rows <= 512) return block_pair_sweep_t<16>(Xs, rows, Js, nj, nc, tol2);
+  // longer columns (b > 512 with a wide core): stream them through
+  __shared__ int s_any;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) s_any = 0;
+  __syncthreads();
+  const int kk = (nc + 1) & ~1;
+  for (int r2 = 0; r2 < kk - 1; ++r2) {
+    for (int pi = warp; pi < kk / 2; pi += NWARP) {
+      int p, q;
+      rr_pair(pi, r2, kk, p, q);
+      if (q >= nc) continue;
+      double a, b, g;
+      jac_dots(Xs + p * rows, Xs + q * rows, rows, lane, a, b, g);
+      a = warp_sum(a);
+      b = warp_sum(b);
+      g = warp_sum(g);
+      double c, sn;
+      if (!jac_angle(a, b, g, tol2, c, sn)) continue;
+      jac_rotate(Xs + p * rows, Xs + q * rows, rows, lane, c, sn);
+      jac_rotate(Js + p * nj, Js + q * nj, nj, lane, c, sn);
+      if (lane == 0) s_any = 1;
+    }
+    __syncthreads();
+  }
+  const bool any = s_any != 0;
+  __syncthreads();
+  return any;
+}
+
+__device__ __forceinline__ bool block_pair_sweep(double* Xs, int rows, double* Js, int nj, int nc, double tol2) {
+  return block_pair_sweep_off((int)(Xs - dyn_smem), rows, (int)(Js - dyn_smem), nj, nc, tol2);
 }
 
 // Shared-memory one-sided Jacobi: X (rows x ncols, ld rows) and J (ncols x
@@ -266,35 +400,17 @@ __device__ __noinline__ bool jacobi_blocked(Ctx& cx, int rows, int ncols, double
           const int gc = c < ni ? bi * jb + c : bj * jb + (c - ni);
           const double* xg = X + (long long)gc * ldx;
           const double* jg = J + (long long)gc * ldj;
-          for (int i = lane; i < rows; i += 32) Xs[i + c * rows] = xg[i];
-          for (int i = lane; i < ncols; i += 32) Js[i + c * ncols] = jg[i];
+          warp_ld_cg(Xs + c * rows, xg, rows, lane);
+          warp_ld_cg(Js + c * ncols, jg, ncols, lane);
         }
         __syncthreads();
-        const int kk = (nc + 1) & ~1;
-        for (int r2 = 0; r2 < kk - 1; ++r2) {
-          for (int pi = warp; pi < kk / 2; pi += NWARP) {
-            int p, q;
-            rr_pair(pi, r2, kk, p, q);
-            if (q >= nc) continue;
-            double a, b, g;
-            jac_dots(Xs + p * rows, Xs + q * rows, rows, lane, a, b, g);
-            a = warp_sum(a);
-            b = warp_sum(b);
-            g = warp_sum(g);
-            double c, s;
-            if (!jac_angle(a, b, g, tol2, c, s)) continue;
-            jac_rotate(Xs + p * rows, Xs + q * rows, rows, lane, c, s);
-            jac_rotate(Js + p * ncols, Js + q * ncols, ncols, lane, c, s);
-            if (lane == 0) s_rot = 1;
-          }
-          __syncthreads();
-        }
+        if (block_pair_sweep(Xs, rows, Js, ncols, nc, tol2) && threadIdx.x == 0) s_rot = 1;
         for (int c = warp; c < nc; c += NWARP) {
           const int gc = c < ni ? bi * jb + c : bj * jb + (c - ni);
           double* xg = X + (long long)gc * ldx;
           double* jg = J + (long long)gc * ldj;
-          for (int i = lane; i < rows; i += 32) xg[i] = Xs[i + c * rows];
-          for (int i = lane; i < ncols; i += 32) jg[i] = Js[i + c * ncols];
+          warp_st_cg(xg, Xs + c * rows, rows, lane);
+          warp_st_cg(jg, Js + c * ncols, ncols, lane);
         }
         __syncthreads();
       }

@@ -147,10 +147,10 @@ __device__ void tiled_update(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf,
       } else {
         double* B = alloc(cx, (long long)r * b);
         double* S = alloc(cx, (long long)b * b);
-        if (!B || !S) return;
+        double* tau = alloc(cx, b);
+        if (!B || !S || !tau) return;
         transpose_mat(b, r, x.v, x.ld, B, r);          // B = V_ik^T (r x b)
-        tpqrt_panels(cx, b, r, rk.u, rk.ld, B, r, T, b, S);
-        build_t_team(cx, b, r, B, r, false, S, b, T, b);
+        tpqrt_team(cx, b, r, rk.u, rk.ld, B, r, T, b, S, tau);
         transpose_mat(r, b, B, r, x.v, x.ld);          // Ytilde.v = Y^T stored in the V slab
       }
       add_flops(cx, FK_UPDATE_QR, qr_cost(b + r, b) + tgen_cost(b + r, b));
@@ -161,9 +161,9 @@ __device__ void tiled_update(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf,
     copy_mat(b, b, x.u, x.ld, Yd, b);
     {
       double* S = alloc(cx, (long long)b * b);
-      if (!S) return;
-      tpqrt_panels(cx, b, b, rk.u, rk.ld, Yd, b, T, b, S);
-      build_t_team(cx, b, b, Yd, b, false, S, b, T, b);
+      double* tau = alloc(cx, b);
+      if (!S || !tau) return;
+      tpqrt_team(cx, b, b, rk.u, rk.ld, Yd, b, T, b, S, tau);
     }
     zero_mat(b, b, x.u, x.ld);
     add_flops(cx, FK_UPDATE_QR, qr_cost(2 * b, b) + tgen_cost(2 * b, b));

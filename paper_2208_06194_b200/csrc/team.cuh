@@ -17,6 +17,8 @@
 //   TK_TBUILD full compact-WY T of GEQRT / TPQRT (householder.cuh
 //             build_t_multi): Gram blocks by column chunk, then T rows by row
 //             chunk with no further synchronisation;
+//   TK_TPQRT  UpdateQR's triangular-pentagonal QR: panels as TK_QRB, then
+//             the T build as TK_TBUILD, with the same team;
 //   TK_BACK   the back-transform U_C = Q_U [Q1 J_r; 0], V_C = Q_V [Q2 W_r; 0]
 //             in fixed 32-column chunks, chunk c on member c mod T.
 // Every kind performs exactly the single-CTA operation sequence on the same
@@ -45,7 +47,7 @@ constexpr int BACK_CW = 32;                              // back-transform colum
 constexpr int TEAM_BACK_MIN = 64;  // Q_U width from which the back-transform splits
 constexpr int TEAM_QRCP_MIN = 128;  // core order from which the pivoted QR splits
 
-enum TeamKind : int { TK_JACOBI = 1, TK_BACK = 2, TK_QRB = 3, TK_QRCP = 4, TK_TBUILD = 5 };
+enum TeamKind : int { TK_JACOBI = 1, TK_BACK = 2, TK_QRB = 3, TK_QRCP = 4, TK_TBUILD = 5, TK_TPQRT = 6 };
 
 struct __align__(128) TeamJob {
   int state;  // 0 free, 9 being set up, 2 running (team size published)
@@ -212,35 +214,17 @@ __device__ void team_jacobi_member(Ctx& cx, TeamJob* job, int t, int team) {
           const int gc = c < ni ? bi * jb + c : bj * jb + (c - ni);
           const double* xg = X + (long long)gc * ldx;
           const double* jg = J + (long long)gc * ldj;
-          for (int i = lane; i < rows; i += 32) Xs[i + c * rows] = __ldcg(xg + i);
-          for (int i = lane; i < ncols; i += 32) Js[i + c * ncols] = __ldcg(jg + i);
+          warp_ld_cg(Xs + c * rows, xg, rows, lane);
+          warp_ld_cg(Js + c * ncols, jg, ncols, lane);
         }
         __syncthreads();
-        const int kk = (nc + 1) & ~1;
-        for (int r2 = 0; r2 < kk - 1; ++r2) {
-          for (int pi = warp; pi < kk / 2; pi += NWARP) {
-            int p, q;
-            rr_pair(pi, r2, kk, p, q);
-            if (q >= nc) continue;
-            double a, b, g;
-            jac_dots(Xs + p * rows, Xs + q * rows, rows, lane, a, b, g);
-            a = warp_sum(a);
-            b = warp_sum(b);
-            g = warp_sum(g);
-            double cs, sn;
-            if (!jac_angle(a, b, g, tol2, cs, sn)) continue;
-            jac_rotate(Xs + p * rows, Xs + q * rows, rows, lane, cs, sn);
-            jac_rotate(Js + p * ncols, Js + q * ncols, ncols, lane, cs, sn);
-            if (lane == 0) s_rot = 1;
-          }
-          __syncthreads();
-        }
+        if (block_pair_sweep(Xs, rows, Js, ncols, nc, tol2) && threadIdx.x == 0) s_rot = 1;
         for (int c = warp; c < nc; c += NWARP) {
           const int gc = c < ni ? bi * jb + c : bj * jb + (c - ni);
           double* xg = X + (long long)gc * ldx;
           double* jg = J + (long long)gc * ldj;
-          for (int i = lane; i < rows; i += 32) __stcg(xg + i, Xs[i + c * rows]);
-          for (int i = lane; i < ncols; i += 32) __stcg(jg + i, Js[i + c * ncols]);
+          warp_st_cg(xg, Xs + c * rows, rows, lane);
+          warp_st_cg(jg, Js + c * ncols, ncols, lane);
         }
         __syncthreads();
       }
@@ -448,6 +432,42 @@ __device__ void build_t_team(Ctx& cx, int n, int m, const double* Y, int ldy, bo
   }
 }
 
+// ---- TK_TPQRT ----------------------------------------------------------------
+// iv: n, k, ldr, ldb, ldt; pv: R, B, T, S, tau
+__device__ void team_tpqrt_member(Ctx& cx, TeamJob* job, int t, int team) {
+  const int n = job->iv[0], k = job->iv[1], ldr = job->iv[2], ldb = job->iv[3], ldt = job->iv[4];
+  double *R = job->pv[0], *B = job->pv[1], *T = job->pv[2], *S = job->pv[3], *tau = job->pv[4];
+  auto bar = [&] { team_barrier(cx, job, team); };
+  tpqrt_panels_multi(cx, n, k, R, ldr, B, ldb, T, ldt, S, tau, t, team, bar);
+  build_t_multi(cx, n, k, B, ldb, false, S, n, T, ldt, t, team, bar);
+}
+
+// TPQRT (R n x n upper, B k x n -> Y) with full T; S (n x n) and tau (n) are
+// caller scratch in global memory.  Team when idle CTAs are available.
+__device__ void tpqrt_team(Ctx& cx, int n, int k, double* R, int ldr, double* B, int ldb, double* T, int ldt, double* S,
+                           double* tau) {
+  const int nch = (n + QR_CW - 1) / QR_CW;
+  const bool global = !in_smem(cx, R) && !in_smem(cx, B) && !in_smem(cx, T) && !in_smem(cx, S) && !in_smem(cx, tau);
+  TeamJob* job = (nch >= 2 && global) ? team_reserve(cx) : nullptr;
+  int team = 1;
+  if (job) {
+    if (threadIdx.x == 0) {
+      job->kind = TK_TPQRT;
+      job->iv[0] = n; job->iv[1] = k; job->iv[2] = ldr; job->iv[3] = ldb; job->iv[4] = ldt;
+      job->pv[0] = R; job->pv[1] = B; job->pv[2] = T; job->pv[3] = S; job->pv[4] = tau;
+    }
+    team = team_launch(cx, job, min(TEAM_MAX, nch));
+  }
+  if (team > 1) {
+    team_tpqrt_member(cx, job, 0, team);
+    team_finish(cx, job, team);
+  } else {
+    auto bar = [] { __syncthreads(); };
+    tpqrt_panels_multi(cx, n, k, R, ldr, B, ldb, T, ldt, S, tau, 0, 1, bar);
+    build_t_multi(cx, n, k, B, ldb, false, S, n, T, ldt, 0, 1, bar);
+  }
+}
+
 // ---- helper side -------------------------------------------------------------
 // thread 0 of an idle CTA: claim a ticket and join its job.
 // Returns the job slot (>= 0) with *member set, or -1.
@@ -539,6 +559,7 @@ __device__ void team_help(Ctx& cx, TeamCtx* tc, int slot, int member) {
     case TK_QRB: team_qrb_member(cx, job, member, team); break;
     case TK_QRCP: team_qrcp_member(cx, job, member, team); break;
     case TK_TBUILD: team_tbuild_member(cx, job, member, team); break;
+    case TK_TPQRT: team_tpqrt_member(cx, job, member, team); break;
     default: break;
   }
   __syncthreads();

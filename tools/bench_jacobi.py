@@ -69,6 +69,6 @@ for k in sizes:
         ph = rt.last_phases
         got = np.sort(sig.cpu().numpy())[::-1]
         err = float(np.max(np.abs(got - ref)) / ref[0])
-        print(json.dumps({"k": k, "kp": kp, "mode": ["blocked", "team", "cols"][mode], "ms": round(min(times), 3),
+        print(json.dumps({"k": k, "kp": kp, "mode": {0: "blocked", 1: "cols", 2: "team"}[mode], "ms": round(min(times), 3),
                           "sweeps": ph.get("jacobi_sweeps", 0), "team_members": rt.last_stats[6],
                           "max_sigma_err_rel": err}), flush=True)

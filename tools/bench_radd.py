@@ -33,7 +33,7 @@ for b, ra, rb in CASES:
     rb_t = torch.full((nb,), rb, dtype=torch.int32, device=dev)
     pa = [_ptrs([x[0] for x in A]), _ptrs([x[1] for x in A]), _ptrs([x[0] for x in B]), _ptrs([x[1] for x in B]), _ptrs(uo), _ptrs(vo)]
     ws, per, nct = rt.workspace(b, cap)
-    nct = min(nct, nb)
+    nct = nct if os.environ.get("TEAMS", "1") != "0" else min(nct, nb)
     def run():
         _lib.check(rt.lib.blrqr_rounded_add_batched(nb, b, b, pa[0].data_ptr(), pa[1].data_ptr(), ra_t.data_ptr(), pa[2].data_ptr(), pa[3].data_ptr(), rb_t.data_ptr(), pa[4].data_ptr(), pa[5].data_ptr(), ro.data_ptr(), cap, 1e-8, ws, per, nct, rt.status.data_ptr(), rt.flops.data_ptr(), _lib.stream_ptr()), "radd")
     run(); torch.cuda.synchronize(); rt.harvest()

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--profile-levels", action="store_true")
     ap.add_argument("--sched", default="dag")
     ap.add_argument("--no-teams", action="store_true")
+    ap.add_argument("--team-slack", type=int, default=None)
     args = ap.parse_args()
     ge.build()
     from paper_2208_06194_b200 import _lib, configs, flops
@@ -37,6 +38,8 @@ def main():
 
     if args.no_teams:
         _lib.runtime().lib.blrqr_set_teams(0)
+    elif args.team_slack is not None:
+        _lib.runtime().lib.blrqr_set_teams(2 + args.team_slack)
     cfg = configs.CONFIGS[args.config]
     n = args.n or cfg.n
     method = args.method or cfg.method
