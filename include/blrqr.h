@@ -170,11 +170,11 @@ int blrqr_tiled_run(const blrqr_grid* g, const blrqr_refl* rf, const blrqr_task*
 /* Dynamic tiled scheduler: the same DAG as explicit successor lists.
  * blrqr_tiled_dag_size returns the task count (and *nedges); blrqr_tiled_dag
  * fills tasks (canonical sweep order), initial in-degrees, CSR successors and
- * priority flags (bit 0: high-priority ready ring -- DiagQR, UpdateQR and the
- * R_{k,k+1} TrapA chain; bit 1: the task may recruit a CTA team -- unit-weight
- * slack <= 1 on the DAG).  blrqr_tiled_run_dag runs the whole
- * factorization with one persistent CTA per SM pulling ready tasks; work_dev
- * is 3*ntasks + 8 ints of scratch. */
+ * priority flags (bit 0: DiagQR, UpdateQR or the R_{k,k+1} TrapA chain;
+ * bit 1: the task may recruit a CTA team; bits 2+: ready ring 0..7 from the
+ * task's bottom level on the DAG, longest remaining chain served first).
+ * blrqr_tiled_run_dag runs the whole factorization with one persistent CTA
+ * per SM pulling ready tasks; work_dev is 9*ntasks + 32 ints of scratch. */
 int64_t blrqr_tiled_dag_size(int p, int q, int64_t* nedges);
 /* Debug: record (start ns, end ns, SM id) per task of subsequent dynamic runs
  * into a device buffer of 3*ntasks int64 (NULL disables). */
@@ -188,6 +188,9 @@ void blrqr_debug_phase_trace(void* dev_buf);
  * sequence, so results do not depend on this switch.  enable = 0 off, 1 on,
  * 2 + s: on, and DAG tasks with slack <= s may recruit (default s = 1). */
 void blrqr_set_teams(int enable);
+/* Ready-ring policy of subsequent blrqr_tiled_dag calls: 8 (default) bottom-
+ * level classes, or 2 (kind-based: DiagQR/UpdateQR/R_{k,k+1} chain first). */
+void blrqr_set_dag_rings(int policy);
 /* Debug: one-sided Jacobi of X (rows x ncols, column-major, ld rows) with J
  * (ncols x ncols) -- mode 0 single-CTA blocked, 1 single-CTA column pairs,
  * 2 CTA team over nctas CTAs.  sigma (ncols), perm (ncols) outputs. */

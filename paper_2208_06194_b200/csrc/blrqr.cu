@@ -373,6 +373,10 @@ __global__ void __launch_bounds__(NT, 1) k_mgs_update(blrqr_grid a, blrqr_grid q
 // semantics without level barriers).  Memory ordering follows the grid-sync
 // pattern: producer __threadfence before publishing, consumer thread 0
 // acquires then __threadfence + __syncthreads before the CTA reads.
+// ready rings, ring 0 served first; a task's ring is prio >> 2 (host-assigned
+// from its bottom level on the DAG, longest remaining chain first)
+constexpr int DAG_RINGS = 8;
+
 struct DagDev {
   int n;
   const blrqr_task* tasks;
@@ -380,8 +384,8 @@ struct DagDev {
   const int* succ;
   const int* prio;
   int* indeg;
-  int* q[2];
-  int* ctr;  // [0] head hi, [1] tail hi, [2] head lo, [3] tail lo, [4] done
+  int* q[DAG_RINGS];
+  int* ctr;  // [2c] head / [2c+1] tail of ring c, [2*DAG_RINGS] done
   long long* trace;  // optional: per task (start ns, end ns, sm id)
   TeamCtx* team;     // optional: CTA teams for large Jacobi cores (team.cuh)
   unsigned long long* ptrace;  // optional: per task PH_COUNT phase cycle counters
@@ -396,7 +400,7 @@ __device__ __forceinline__ long long global_ns() {
 __device__ __forceinline__ int ld_volatile(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
 
 __device__ __forceinline__ void dag_push(const DagDev& d, int t) {
-  const int c = (d.prio[t] & 1) ? 0 : 1;
+  const int c = min(DAG_RINGS - 1, d.prio[t] >> 2);
   const int slot = atomicAdd(d.ctr + 2 * c + 1, 1);
   atomicExch(d.q[c] + slot, t);
 }
@@ -423,7 +427,7 @@ __global__ void __launch_bounds__(NT, 1) k_tiled_dag(DagDev d, blrqr_grid g, blr
             break;
           }
         }
-        for (int c = 0; c < 2 && !got; ++c) {
+        for (int c = 0; c < DAG_RINGS && !got; ++c) {
           const int h = ld_volatile(d.ctr + 2 * c);
           const int tl = ld_volatile(d.ctr + 2 * c + 1);
           if (h < tl && atomicCAS(d.ctr + 2 * c, h, h + 1) == h) {
@@ -434,10 +438,10 @@ __global__ void __launch_bounds__(NT, 1) k_tiled_dag(DagDev d, blrqr_grid g, blr
           }
         }
         if (got) break;
-        if (ld_volatile(d.ctr + 4) >= d.n) break;
+        if (ld_volatile(d.ctr + 2 * DAG_RINGS) >= d.n) break;
         if (sm_clock() - t0 > timeout_cycles) {
           atomicOr(status, ST_SCHED_TIMEOUT);
-          atomicExch(d.ctr + 4, d.n);  // release everyone
+          atomicExch(d.ctr + 2 * DAG_RINGS, d.n);  // release everyone
           break;
         }
         __nanosleep(64);
@@ -486,7 +490,7 @@ __global__ void __launch_bounds__(NT, 1) k_tiled_dag(DagDev d, blrqr_grid g, blr
         const int s2 = d.succ[e];
         if (atomicSub(d.indeg + s2, 1) == 1) dag_push(d, s2);
       }
-      atomicAdd(d.ctr + 4, 1);
+      atomicAdd(d.ctr + 2 * DAG_RINGS, 1);
     }
     __syncthreads();
   }
@@ -577,6 +581,7 @@ static void init_kernels() {
 #define INIT_KERNELS() init_kernels()
 
 static int g_teams_enabled = 1;
+static int g_dag_rings = DAG_RINGS;  // 2: the kind-based two-ring policy
 static int g_team_slack = 1 << 20;  // DAG tasks with unit-weight slack <= this may form teams (all by default: measured best)
 
 // Team-job table + ticket ring + two task counters, one per (device, stream)
@@ -898,6 +903,7 @@ void blrqr_set_teams(int enable) {
   g_teams_enabled = enable ? 1 : 0;
   if (enable > 1) g_team_slack = enable - 2;  // tuning: enable = 2 + max slack (1 << 20: every task)
 }
+void blrqr_set_dag_rings(int policy) { g_dag_rings = policy == 2 ? 2 : DAG_RINGS; }
 
 
 
@@ -932,12 +938,16 @@ int blrqr_tiled_dag(int p, int q, blrqr_task* tasks_host, int* indeg_host, int64
     for (int64_t e = off[t]; e < off[t + 1]; ++e) bot[t] = std::max(bot[t], bot[succ[e]] + 1);
   int cp = 0;
   for (int t = 0; t < n; ++t) cp = std::max(cp, top[t] + bot[t]);
-  // bit 0: high-priority ready ring (DiagQR, UpdateQR, the R_kj chain of the
-  // next panel column); bit 1: may form CTA teams (slack <= 1)
+  // bit 0: DiagQR / UpdateQR / the R_kj chain of the next panel column;
+  // bit 1: may form CTA teams (slack <= g_team_slack); bits 2+: ready ring,
+  // by bottom level (longest remaining chain first, DAG_RINGS classes)
   for (int t = 0; t < n; ++t) {
     const int slack = cp - top[t] - bot[t];
     const bool hi = tasks[t].kind == 0 || tasks[t].kind == 2 || (tasks[t].kind == 4 && tasks[t].j == tasks[t].k + 1);
-    prio_host[t] = (hi ? 1 : 0) | (slack <= g_team_slack ? 2 : 0);
+    int ring;
+    if (g_dag_rings == 2) ring = hi ? 0 : 1;
+    else ring = std::min(DAG_RINGS - 1, (cp - bot[t]) * DAG_RINGS / (cp + 1));
+    prio_host[t] = (hi ? 1 : 0) | (slack <= g_team_slack ? 2 : 0) | (ring << 2);
   }
   return 0;
 }
@@ -957,17 +967,16 @@ int blrqr_tiled_run_dag(const blrqr_grid* g, const blrqr_refl* rf, int ntasks, c
   d.succ = succ_dev;
   d.prio = prio_dev;
   d.indeg = work_dev;
-  d.q[0] = work_dev + ntasks;
-  d.q[1] = work_dev + 2 * (int64_t)ntasks;
-  d.ctr = work_dev + 3 * (int64_t)ntasks;
+  for (int c = 0; c < DAG_RINGS; ++c) d.q[c] = work_dev + (int64_t)(c + 1) * ntasks;
+  d.ctr = work_dev + (int64_t)(DAG_RINGS + 1) * ntasks;
   d.trace = g_dag_trace;
   d.ptrace = g_phase_trace;
   int dev = 0, clk_khz = 1965000;
   cudaGetDevice(&dev);
   if (int e = team_for_launch(st, &d.team, nullptr)) return e;
   CK(cudaMemcpyAsync(d.indeg, indeg0_dev, sizeof(int) * ntasks, cudaMemcpyDeviceToDevice, st));
-  CK(cudaMemsetAsync(d.q[0], 0xFF, sizeof(int) * 2 * (size_t)ntasks, st));
-  CK(cudaMemsetAsync(d.ctr, 0, sizeof(int) * 8, st));
+  CK(cudaMemsetAsync(d.q[0], 0xFF, sizeof(int) * DAG_RINGS * (size_t)ntasks, st));
+  CK(cudaMemsetAsync(d.ctr, 0, sizeof(int) * (2 * DAG_RINGS + 1), st));
   k_dag_init<<<1, 256, 0, st>>>(d);
   CK(cudaGetLastError());
   cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev);
@@ -1067,6 +1076,22 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_probe(int rows, int ncols, dou
                                                         unsigned long long* flops, TeamCtx* team, int* ctr) {
   Ctx cx = make_ctx(ws, wsp, status, flops);
   cx.team = mode == 2 ? team : nullptr;
+  if (mode >= 3) {  // inner block-pair sweep only: first min(32, ncols) columns staged; 1 (mode 3) or 50 sweeps
+    if (blockIdx.x != 0) return;
+    const int nc = min(32, ncols);
+    double* Xs = dyn_smem;
+    double* Js = dyn_smem + nc * rows;
+    for (int c = threadIdx.x >> 5; c < nc; c += NWARP) {
+      warp_ld_cg(Xs + c * rows, X + (long long)c * rows, rows, threadIdx.x & 31);
+      for (int i = threadIdx.x & 31; i < ncols; i += 32) Js[i + c * ncols] = (i == c) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    PhaseTimer t;
+    const double tol = 2.220446049250313e-16 * (double)max(rows, 1);
+    for (int rep = 0; rep < (mode == 3 ? 1 : 50); ++rep) block_pair_sweep(Xs, rows, Js, ncols, nc, tol * tol);
+    t.stop(cx, PH_SVD);
+    return;
+  }
   team_task_loop(cx, 1, ctr, [&](long long) {
     PhaseTimer t;
     if (mode == 1 || !((mode == 2 && team_jacobi_lead(cx, rows, ncols, X, rows, J, ncols, sigma, perm)) ||

@@ -136,7 +136,7 @@ class DeviceFactorization:
                 self.dag = {"n": len(dt), "tasks": torch.from_numpy(dt).to(dev),
                             "indeg": torch.from_numpy(ind).to(dev), "off": torch.from_numpy(off).to(dev),
                             "succ": torch.from_numpy(succ).to(dev), "prio": torch.from_numpy(prio).to(dev),
-                            "work": torch.empty(3 * len(dt) + 8, dtype=torch.int32, device=dev)}
+                            "work": torch.empty(9 * len(dt) + 32, dtype=torch.int32, device=dev)}
         elif method == "blocked-hh":
             g = self.g
             self.rf = DeviceRefl(self.g)

@@ -45,7 +45,7 @@ for k in sizes:
     r2, s = make_r2(k)
     kp = r2.shape[0]
     ref = np.linalg.svd(r2, compute_uv=False)
-    for mode in (0, 2, 1):
+    for mode in (int(m) for m in os.environ.get("MODES", "0,2,1,3").split(",")):
         if mode == 1 and kp > 160:
             continue
         x = torch.from_numpy(np.asfortranarray(r2).ravel(order="F").copy()).to(dev)
@@ -69,6 +69,7 @@ for k in sizes:
         ph = rt.last_phases
         got = np.sort(sig.cpu().numpy())[::-1]
         err = float(np.max(np.abs(got - ref)) / ref[0])
-        print(json.dumps({"k": k, "kp": kp, "mode": {0: "blocked", 1: "cols", 2: "team"}[mode], "ms": round(min(times), 3),
+        print(json.dumps({"k": k, "kp": kp, "mode": {0: "blocked", 1: "cols", 2: "team", 3: "pair_sweep_x1", 4: "pair_sweep_x50"}[mode], "ms": round(min(times), 3),
                           "sweeps": ph.get("jacobi_sweeps", 0), "team_members": rt.last_stats[6],
+                          "svd_phase_ms": round(ph.get("svd", 0) / 1.965e6, 3),
                           "max_sigma_err_rel": err}), flush=True)

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--sched", default="dag")
     ap.add_argument("--no-teams", action="store_true")
     ap.add_argument("--team-slack", type=int, default=None)
+    ap.add_argument("--rings", type=int, default=None)
     args = ap.parse_args()
     ge.build()
     from paper_2208_06194_b200 import _lib, configs, flops
@@ -40,6 +41,8 @@ def main():
         _lib.runtime().lib.blrqr_set_teams(0)
     elif args.team_slack is not None:
         _lib.runtime().lib.blrqr_set_teams(2 + args.team_slack)
+    if args.rings is not None:
+        _lib.runtime().lib.blrqr_set_dag_rings(args.rings)
     cfg = configs.CONFIGS[args.config]
     n = args.n or cfg.n
     method = args.method or cfg.method
