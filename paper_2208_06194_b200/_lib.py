@@ -139,6 +139,26 @@ class Runtime:
         self.nctas = int(self.lib.blrqr_default_ctas())
         self._ws = None
         self._ws_per_cta = 0
+        self._pinned = None
+        self._pinned_ev = None
+        self.dag_cache = {}
+
+    def pinned(self, ndoubles: int) -> torch.Tensor:
+        """Persistent pinned host staging buffer (float64, >= ndoubles), reused
+        by the host <-> device BLR transfers; waits for the previous transfer
+        that used it before handing it out again."""
+        if self._pinned_ev is not None:
+            self._pinned_ev.synchronize()
+        if self._pinned is None or self._pinned.numel() < ndoubles:
+            self._pinned = None
+            self._pinned = torch.empty(max(ndoubles, 1), dtype=torch.float64, pin_memory=True)
+        return self._pinned
+
+    def pinned_in_flight(self) -> None:
+        """Mark the pinned buffer busy until the work queued so far completes."""
+        ev = torch.cuda.Event()
+        ev.record()
+        self._pinned_ev = ev
 
     def workspace(self, b: int, cap: int, panel_rows: int = 0, nctas: int | None = None):
         """(ptr, doubles_per_cta, nctas) — grows the shared arena on demand."""

@@ -10,6 +10,7 @@ update can overflow; smaller caps trade memory for an overflow check.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 import torch
@@ -21,6 +22,24 @@ from .core import BlrMatrix, BlrStructure, LowRankBlock, is_lowrank
 def _f(a: np.ndarray) -> np.ndarray:
     """column-major flat copy of a 2-D array"""
     return np.asarray(a, dtype=np.float64).ravel(order="F")
+
+
+_POOL = None
+
+
+def _host_parallel(fn, n: int, min_chunk: int = 64) -> None:
+    """fn(lo, hi) over [0, n) in chunks on a host thread pool (numpy copies
+    release the GIL); serial for small n."""
+    global _POOL
+    workers = min(32, os.cpu_count() or 1)
+    if n <= min_chunk or workers == 1:
+        fn(0, n)
+        return
+    if _POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _POOL = ThreadPoolExecutor(max_workers=workers)
+    step = max(min_chunk, -(-n // (4 * workers)))
+    list(_POOL.map(lambda lo: fn(lo, min(n, lo + step)), range(0, n, step)))
 
 
 class DeviceGrid:
@@ -86,55 +105,73 @@ class DeviceGrid:
                                        _lib.stream_ptr()), "grid_pack")
 
     @classmethod
-    def from_host(cls, a: BlrMatrix, cap: int | None = None, pinned: bool = False) -> "DeviceGrid":
+    def from_host(cls, a: BlrMatrix, cap: int | None = None, pinned: bool = True) -> "DeviceGrid":
+        """Upload a host BlrMatrix: cells are packed column-major into the
+        runtime's persistent pinned staging buffer by a host thread pool, sent
+        with one H2D copy and scattered into the slabs by the pack kernel."""
         s = a.structure
         g = cls(s.m, s.n, s.b, s.admissible, cap)
-        ranks = np.array([x.rank if is_lowrank(x) else -1 for row in a.blocks for x in row], dtype=np.int32)
+        flat = [x for row in a.blocks for x in row]
+        ranks = np.array([x.rank if is_lowrank(x) else -1 for x in flat], dtype=np.int32)
         if (ranks > g.cap).any():
             raise ValueError("input rank exceeds the slab capacity")
         offs, tot = g._stage_offsets(ranks)
-        host = np.empty(tot, dtype=np.float64)
-        c = 0
-        for row in a.blocks:
-            for x in row:
-                o = offs[c]
-                if is_lowrank(x):
-                    r = x.rank
-                    host[o:o + s.b * r] = _f(x.u)
-                    host[o + s.b * r:o + 2 * s.b * r] = _f(x.v)
+        b = s.b
+        rt = _lib.runtime()
+        pin = rt.pinned(tot) if pinned else torch.empty(max(tot, 1), dtype=torch.float64)
+        host = pin.numpy()
+
+        def pack(lo, hi):
+            for c in range(lo, hi):
+                x, o = flat[c], int(offs[c])
+                if ranks[c] >= 0:
+                    r = int(ranks[c])
+                    host[o:o + b * r].reshape(r, b)[...] = x.u.T
+                    host[o + b * r:o + 2 * b * r].reshape(r, b)[...] = x.v.T
                 else:
-                    host[o:o + s.b * s.b] = _f(x)
-                c += 1
-        ht = torch.from_numpy(host)
+                    host[o:o + b * b].reshape(b, b)[...] = np.asarray(x).T
+
+        _host_parallel(pack, len(flat))
+        stage = torch.empty(max(tot, 1), dtype=torch.float64, device=g.pool.device)
+        stage[:tot].copy_(pin[:tot], non_blocking=pinned)
         if pinned:
-            ht = ht.pin_memory()
-        stage = ht.to(g.pool.device, non_blocking=pinned)
+            rt.pinned_in_flight()
         g.rank.copy_(torch.from_numpy(ranks))
         g._pack(stage, offs, True)
         return g
 
     def to_host(self) -> BlrMatrix:
+        """Download into a host BlrMatrix (pack kernel, one D2H copy into the
+        pinned staging buffer, thread-parallel unpack into fresh arrays)."""
+        rt = _lib.runtime()
         ranks = self.rank.cpu().numpy()
         offs, tot = self._stage_offsets(ranks)
         stage = torch.empty(max(tot, 1), dtype=torch.float64, device=self.pool.device)
         self._pack(stage, offs, False)
-        host = stage.cpu().numpy()
+        pin = rt.pinned(tot)
+        pin[:tot].copy_(stage[:tot])
+        host = pin.numpy()
         b = self.b
-        blocks = []
-        c = 0
-        for i in range(self.p):
-            row = []
-            for j in range(self.q):
-                o = offs[c]
-                if self.kind_host[i, j]:
+        kind = self.kind_host.ravel()
+        cells = [None] * (self.p * self.q)
+
+        def unpack(lo, hi):
+            for c in range(lo, hi):
+                o = int(offs[c])
+                if kind[c]:
                     r = int(ranks[c])
-                    u = host[o:o + b * r].reshape(r, b).T
-                    v = host[o + b * r:o + 2 * b * r].reshape(r, b).T
-                    row.append(LowRankBlock(np.ascontiguousarray(u), np.ascontiguousarray(v)))
+                    u = np.empty((b, r))
+                    v = np.empty((b, r))
+                    u[...] = host[o:o + b * r].reshape(r, b).T
+                    v[...] = host[o + b * r:o + 2 * b * r].reshape(r, b).T
+                    cells[c] = LowRankBlock(u, v)
                 else:
-                    row.append(np.ascontiguousarray(host[o:o + b * b].reshape(b, b).T))
-                c += 1
-            blocks.append(row)
+                    d = np.empty((b, b))
+                    d[...] = host[o:o + b * b].reshape(b, b).T
+                    cells[c] = d
+
+        _host_parallel(unpack, len(cells))
+        blocks = [cells[i * self.q:(i + 1) * self.q] for i in range(self.p)]
         return BlrMatrix(self.structure, blocks)
 
     @classmethod

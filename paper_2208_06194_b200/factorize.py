@@ -131,12 +131,16 @@ class DeviceFactorization:
             self.nlevels = len(self.levels) - 1
             if scheduler == "dag":
                 self.rf.enable_split_traps()
-                dt, ind, off, succ, prio = tiled_dag_arrays(self.g.p, self.g.q)
+                key = (self.g.p, self.g.q)
                 dev = self.rt.dev
-                self.dag = {"n": len(dt), "tasks": torch.from_numpy(dt).to(dev),
-                            "indeg": torch.from_numpy(ind).to(dev), "off": torch.from_numpy(off).to(dev),
-                            "succ": torch.from_numpy(succ).to(dev), "prio": torch.from_numpy(prio).to(dev),
-                            "work": torch.empty(9 * len(dt) + 32, dtype=torch.int32, device=dev)}
+                if key not in self.rt.dag_cache:  # read-only device copy of the DAG, once per shape
+                    dt, ind, off, succ, prio = tiled_dag_arrays(*key)
+                    self.rt.dag_cache[key] = {
+                        "n": len(dt), "tasks": torch.from_numpy(dt).to(dev), "indeg": torch.from_numpy(ind).to(dev),
+                        "off": torch.from_numpy(off).to(dev), "succ": torch.from_numpy(succ).to(dev),
+                        "prio": torch.from_numpy(prio).to(dev)}
+                self.dag = dict(self.rt.dag_cache[key])
+                self.dag["work"] = torch.empty(9 * self.dag["n"] + 32, dtype=torch.int32, device=dev)
         elif method == "blocked-hh":
             g = self.g
             self.rf = DeviceRefl(self.g)
