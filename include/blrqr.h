@@ -191,6 +191,10 @@ void blrqr_set_teams(int enable);
 /* Ready-ring policy of subsequent blrqr_tiled_dag calls: 8 (default) bottom-
  * level classes, or 2 (kind-based: DiagQR/UpdateQR/R_{k,k+1} chain first). */
 void blrqr_set_dag_rings(int policy);
+/* Stopping level of the rounded addition's core QRCP: the dropped remainder
+ * is <= (tol * eps_mach) * ||core||_F (tol >= 1; default 1 = rounding level).
+ * Returns 0, or -1 for tol out of range. */
+int blrqr_set_qrcp_tol(double tol);
 /* Debug: one-sided Jacobi of X (rows x ncols, column-major, ld rows) with J
  * (ncols x ncols) -- mode 0 single-CTA blocked, 1 single-CTA column pairs,
  * 2 CTA team over nctas CTAs.  sigma (ncols), perm (ncols) outputs. */
@@ -225,6 +229,20 @@ int blrqr_mgs_step(const blrqr_grid* a, const blrqr_grid* qg, const blrqr_grid* 
                    double* panel_ws, int64_t panel_doubles, double* ws, int64_t ws_per_cta, int nctas, int* status,
                    unsigned long long* flops, void* stream);
 
+/* Multi-GPU forms of the two steps above (block columns 1-D
+ * block-cyclic, column j on rank j mod world).  phases: 1 = panel only (run
+ * by the owner of column k / j), 2 = chain + updates (resp. projections +
+ * updates) restricted to the update columns owned by `rank`, 3 = both.  The
+ * panel's reflector column (blocked: y_kk, T_k, Ytilde_ik; MGS: Q column j) is
+ * broadcast by the caller between the two phases.  world = 1, phases = 3 is
+ * the single-GPU step.  -4: bad phases, -5: bad world / rank. */
+int blrqr_blocked_step_dist(const blrqr_grid* g, const blrqr_refl* rf, int k, double eps, double* zbuf, int* zrank,
+                            double* panel_ws, int64_t panel_doubles, double* ws, int64_t ws_per_cta, int nctas,
+                            int phases, int world, int rank, int* status, unsigned long long* flops, void* stream);
+int blrqr_mgs_step_dist(const blrqr_grid* a, const blrqr_grid* qg, const blrqr_grid* rg, int j, double eps,
+                        double* panel_ws, int64_t panel_doubles, double* ws, int64_t ws_per_cta, int nctas,
+                        int phases, int world, int rank, int* status, unsigned long long* flops, void* stream);
+
 /* ---- Q application and expansion (metrics; factorize.py:295-352, 461-524) */
 /* C (m x nc, column-major, ldc >= m) <- Q C (transpose = 0) or Q^T C, Q the
  * orthogonal factor stored by a tiled (method 0) or blocked (method 1)
@@ -232,6 +250,17 @@ int blrqr_mgs_step(const blrqr_grid* a, const blrqr_grid* qg, const blrqr_grid* 
 int blrqr_apply_q(const blrqr_grid* g, const blrqr_refl* rf, int method, double* C, int64_t ldc, int nc,
                   int transpose, double* ws, int64_t ws_per_cta, int nctas, int* status, unsigned long long* flops,
                   void* stream);
+/* Q (transpose = 0) or Q^T (1) of a blocked (method 1) or tiled (method 0)
+ * factorization (gr, rf) applied in place to a block low-rank operand grid c
+ * with the same row blocking (blocked_apply_q factorize.py:326-350,
+ * tiled_apply_q :495-568 for BlrMatrix operands): kind-aware block updates
+ * with rounded additions at tolerance eps, written with c's kind map.
+ * zbuf (c->q * 2 * b * b doubles) and zrank (c->q ints) are needed for the
+ * blocked method only.  -4: row blocking mismatch, -6: bad eps, -7: no zbuf. */
+int blrqr_apply_q_blr(const blrqr_grid* gr, const blrqr_refl* rf, int method, const blrqr_grid* c, int transpose,
+                      double eps, double* zbuf, int* zrank, double* ws, int64_t ws_per_cta, int nctas, int* status,
+                      unsigned long long* flops, void* stream);
+
 /* D (m x n, column-major, ldd >= m) = the grid expanded (blr_to_dense, core.py:192-201). */
 int blrqr_blr_to_dense(const blrqr_grid* g, double* D, int64_t ldd, void* stream);
 

@@ -211,6 +211,17 @@ def blocked_q_dense(st: BlockedState, c: np.ndarray, transpose: bool) -> np.ndar
     return out
 
 
+def blocked_q_blr(st: BlockedState, c: Grid, transpose: bool, eps: float) -> Grid:
+    """blocked_apply_q on a block low-rank operand (factorize.py:343-350):
+    for each reflector column in order, _refcol_apply_blr on every column j."""
+    out = c.clone()
+    order = range(len(st.cols)) if transpose else range(len(st.cols) - 1, -1, -1)
+    for k in order:
+        for j in range(out.q):
+            blocked_apply(st.cols[k], out, j, eps, transpose)
+    return out
+
+
 # ---------------------------------------------------------------------------
 # tiled Householder (factorize.py:369-458)
 # ---------------------------------------------------------------------------
@@ -275,6 +286,40 @@ def trap_pair(yt, t, top, bot, transpose, top_lr, bot_lr, eps):
     w = dense_times(t.T if transpose else t, ssum)
     return (sub_into(top, w, top_lr, eps),
             sub_into(bot, mul(yt, w), bot_lr, eps))
+
+
+def tiled_q_blr(st: "TiledState", c: Grid, transpose: bool, eps: float) -> Grid:
+    """tiled_apply_q on a block low-rank operand (factorize.py:534-567)."""
+    out = c.clone()
+    p, q = st.g.p, st.g.q
+    adm = out.lowrank
+
+    def diag_apply(k):
+        y, t = st.diag[k]
+        for j in range(out.q):
+            x = out[k, j]
+            if is_lr(x):
+                if x.rank:
+                    out[k, j] = LR(panels.apply_wy(y, t, x.u, transpose), x.v)
+            else:
+                out[k, j] = panels.apply_wy(y, t, x, transpose)
+
+    def trap(k, i):
+        yt, t = st.upd[(i, k)]
+        for j in range(out.q):
+            out[k, j], out[i, j] = trap_pair(yt, t, out[k, j], out[i, j], transpose, adm[k, j], adm[i, j], eps)
+
+    if transpose:
+        for k in range(q):
+            diag_apply(k)
+            for i in range(k + 1, p):
+                trap(k, i)
+    else:
+        for k in range(q - 1, -1, -1):
+            for i in range(p - 1, k, -1):
+                trap(k, i)
+            diag_apply(k)
+    return out
 
 
 def tiled_tasks(p: int, q: int) -> list[tuple]:

@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libblrqr.so")
+LIB_PATH = os.environ.get("BLRQR_LIB") or os.path.join(_HERE, "lib", "libblrqr.so")
 
 FLOP_KINDS = ("compress", "rounded_add", "expand", "lr_mul", "gemm", "panel_qr",
               "apply_wy", "update_qr", "apply_tp")
@@ -70,15 +70,22 @@ _SIGS = {
     "blrqr_debug_trace": ([_P], None),
     "blrqr_set_teams": ([_I], None),
     "blrqr_set_dag_rings": ([_I], None),
+    "blrqr_set_qrcp_tol": ([_D], _I),
     "blrqr_debug_phase_trace": ([_P], None),
     "blrqr_apply_q": ([C.POINTER(Grid), C.POINTER(Refl), _I, _P, _L, _I, _I, _P, _L, _I, _P, _P, _P], _I),
     "blrqr_blr_to_dense": ([C.POINTER(Grid), _P, _L, _P], _I),
+    "blrqr_apply_q_blr": ([C.POINTER(Grid), C.POINTER(Refl), _I, C.POINTER(Grid), _I, _D, _P, _P, _P, _L, _I, _P,
+                           _P, _P], _I),
     "blrqr_debug_jacobi": ([_I, _I, _P, _P, _P, _P, _I, _P, _L, _I, _P, _P, _P], _I),
     "blrqr_debug_gemm": ([_I, _I, _I, _I, _I, _P, _I, _P, _I, _P, _I, _I, _I, _P], _I),
     "blrqr_tiled_dag": ([_I, _I, _P, _P, _P, _P, _P], _I),
     "blrqr_tiled_run_dag": ([C.POINTER(Grid), C.POINTER(Refl), _I, _P, _P, _P, _P, _P, _P, _D, _P, _L, _I, _D, _P,
                              _P, _P], _I),
     "blrqr_blocked_step": ([C.POINTER(Grid), C.POINTER(Refl), _I, _D, _P, _P, _P, _L, _P, _L, _I, _P, _P, _P], _I),
+    "blrqr_blocked_step_dist": ([C.POINTER(Grid), C.POINTER(Refl), _I, _D, _P, _P, _P, _L, _P, _L, _I, _I, _I, _I,
+                                 _P, _P, _P], _I),
+    "blrqr_mgs_step_dist": ([C.POINTER(Grid), C.POINTER(Grid), C.POINTER(Grid), _I, _D, _P, _L, _P, _L, _I, _I, _I,
+                             _I, _P, _P, _P], _I),
     "blrqr_mgs_step": ([C.POINTER(Grid), C.POINTER(Grid), C.POINTER(Grid), _I, _D, _P, _L, _P, _L, _I, _P, _P, _P],
                        _I),
 }

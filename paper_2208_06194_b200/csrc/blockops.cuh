@@ -10,6 +10,10 @@ namespace blr {
 
 constexpr double NOISE_FLOOR = 64.0 * 2.220446049250313e-16;  // lowrank.py:170
 
+// The core's QRCP stops once the dropped remainder is <= (tol * eps_mach)^2
+// ||core||_F^2 (tol = 1: rounding level).  Host knob blrqr_set_qrcp_tol.
+__device__ double g_qrcp_tol = 1.0;
+
 struct Blk {
   int lr;        // 1: s * u v^T (rank columns), 0: s * u as dense rows x cols
   int rank;
@@ -147,7 +151,8 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
   const double eps_m = 2.220446049250313e-16;
   double rem2 = 0.0;
   PhaseTimer tqp;
-  const int kp = pivoted_qr_team(cx, k, k, G, k, eps_m * eps_m * core2, k, core2, col2, col2o, piv, taus, &rem2);
+  const double qtol = g_qrcp_tol * eps_m;
+  const int kp = pivoted_qr_team(cx, k, k, G, k, qtol * qtol * core2, k, core2, col2, col2o, piv, taus, &rem2);
   tqp.stop(cx, PH_QRCP);
   if (threadIdx.x == 0 && cx.flops && k >= 64) {  // stats: sum k, sum kp, count, sum k^3, sum kp^3
     atomicAdd(cx.flops + 48, (unsigned long long)k);

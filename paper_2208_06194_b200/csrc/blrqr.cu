@@ -296,19 +296,32 @@ __global__ void __launch_bounds__(NT) k_lr_product(int op, int m, int k, int n, 
 #include "tasks_blocked_mgs.cuh"
 
 // ---- blocked Householder step kernels ------------------------------------
-__global__ void __launch_bounds__(NT, 1) k_blocked_panel(blrqr_grid g, blrqr_refl rf, int k, double* P, double* Yp,
+__global__ void __launch_bounds__(NT, CTAS_PER_SM) k_blocked_panel(blrqr_grid g, blrqr_refl rf, int k, double* P, double* Yp,
                                                          double* ws, long long wsp, int* status,
                                                          unsigned long long* flops) {
   Ctx cx = make_ctx(ws, wsp, status, flops);
   blocked_panel(cx, g, rf, k, P, Yp);
 }
 
-__global__ void __launch_bounds__(NT, 1) k_blocked_chain(blrqr_grid g, blrqr_refl rf, int k, double eps, double* zbuf,
+// Column ownership for the block-cyclic multi-GPU drivers: this launch
+// touches only the update columns j with j mod world == rank (world = 1: all).
+__device__ __forceinline__ int owned_col(int first, int world, int rank, int idx) {
+  const int j0 = first + ((rank - first % world) % world + world) % world;  // first owned column >= first
+  return j0 + idx * world;
+}
+__host__ __device__ __forceinline__ int owned_count(int first, int end, int world, int rank) {
+  const int j0 = first + ((rank - first % world) % world + world) % world;
+  return j0 >= end ? 0 : (end - j0 + world - 1) / world;
+}
+
+__global__ void __launch_bounds__(NT, CTAS_PER_SM) k_blocked_chain(blrqr_grid g, blrqr_refl rf, int k, double eps, double* zbuf,
                                                          int* zrank, double* ws, long long wsp, int* status,
-                                                         unsigned long long* flops) {
+                                                         unsigned long long* flops, int world, int rank) {
   Ctx cx = make_ctx(ws, wsp, status, flops);
   const long long bb = (long long)g.b * g.b;
-  for (int j = k + 1 + blockIdx.x; j < g.q; j += gridDim.x) {
+  const int nj = owned_count(k + 1, g.q, world, rank);
+  for (int jj = blockIdx.x; jj < nj; jj += gridDim.x) {
+    const int j = owned_col(k + 1, world, rank, jj);
     blocked_chain(cx, g, rf, eps, k, j, zbuf + 2 * bb * j, zbuf + 2 * bb * j + bb, zrank + j);
     cx.top = 0;
     cx.stop = 0;
@@ -316,14 +329,14 @@ __global__ void __launch_bounds__(NT, 1) k_blocked_chain(blrqr_grid g, blrqr_ref
   }
 }
 
-__global__ void __launch_bounds__(NT, 1) k_blocked_update(blrqr_grid g, blrqr_refl rf, int k, double eps,
+__global__ void __launch_bounds__(NT, CTAS_PER_SM) k_blocked_update(blrqr_grid g, blrqr_refl rf, int k, double eps,
                                                           double* zbuf, const int* zrank, double* ws, long long wsp,
-                                                          int* status, unsigned long long* flops) {
+                                                          int* status, unsigned long long* flops, int world, int rank) {
   Ctx cx = make_ctx(ws, wsp, status, flops);
   const long long bb = (long long)g.b * g.b;
-  const int ni = g.p - k, nj = g.q - k - 1;
+  const int ni = g.p - k, nj = owned_count(k + 1, g.q, world, rank);
   for (int t = blockIdx.x; t < ni * nj; t += gridDim.x) {
-    const int i = k + t % ni, j = k + 1 + t / ni;
+    const int i = k + t % ni, j = owned_col(k + 1, world, rank, t / ni);
     blocked_update(cx, g, rf, eps, k, i, j, zbuf + 2 * bb * j, zbuf + 2 * bb * j + bb, zrank + j);
     cx.top = 0;
     cx.stop = 0;
@@ -332,18 +345,20 @@ __global__ void __launch_bounds__(NT, 1) k_blocked_update(blrqr_grid g, blrqr_re
 }
 
 // ---- blocked MGS step kernels ---------------------------------------------
-__global__ void __launch_bounds__(NT, 1) k_mgs_panel_task(blrqr_grid a, blrqr_grid qg, blrqr_grid rg, int j,
+__global__ void __launch_bounds__(NT, CTAS_PER_SM) k_mgs_panel_task(blrqr_grid a, blrqr_grid qg, blrqr_grid rg, int j,
                                                           double* P, double* ws, long long wsp, int* status,
                                                           unsigned long long* flops) {
   Ctx cx = make_ctx(ws, wsp, status, flops);
   mgs_panel_task(cx, a, qg, rg, j, P);
 }
 
-__global__ void __launch_bounds__(NT, 1) k_mgs_project(blrqr_grid a, blrqr_grid qg, blrqr_grid rg, int j, double eps,
+__global__ void __launch_bounds__(NT, CTAS_PER_SM) k_mgs_project(blrqr_grid a, blrqr_grid qg, blrqr_grid rg, int j, double eps,
                                                        double* ws, long long wsp, int* status,
-                                                       unsigned long long* flops) {
+                                                       unsigned long long* flops, int world, int rank) {
   Ctx cx = make_ctx(ws, wsp, status, flops);
-  for (int k = j + 1 + blockIdx.x; k < a.q; k += gridDim.x) {
+  const int nk = owned_count(j + 1, a.q, world, rank);
+  for (int kk = blockIdx.x; kk < nk; kk += gridDim.x) {
+    const int k = owned_col(j + 1, world, rank, kk);
     mgs_project(cx, a, qg, rg, eps, j, k);
     cx.top = 0;
     cx.stop = 0;
@@ -351,13 +366,13 @@ __global__ void __launch_bounds__(NT, 1) k_mgs_project(blrqr_grid a, blrqr_grid 
   }
 }
 
-__global__ void __launch_bounds__(NT, 1) k_mgs_update(blrqr_grid a, blrqr_grid qg, blrqr_grid rg, int j, double eps,
+__global__ void __launch_bounds__(NT, CTAS_PER_SM) k_mgs_update(blrqr_grid a, blrqr_grid qg, blrqr_grid rg, int j, double eps,
                                                       double* ws, long long wsp, int* status,
-                                                      unsigned long long* flops) {
+                                                      unsigned long long* flops, int world, int rank) {
   Ctx cx = make_ctx(ws, wsp, status, flops);
-  const int nk = a.q - j - 1;
+  const int nk = owned_count(j + 1, a.q, world, rank);
   for (int t = blockIdx.x; t < nk * a.p; t += gridDim.x) {
-    const int i = t % a.p, k = j + 1 + t / a.p;
+    const int i = t % a.p, k = owned_col(j + 1, world, rank, t / a.p);
     mgs_update(cx, a, qg, rg, eps, j, i, k);
     cx.top = 0;
     cx.stop = 0;
@@ -405,7 +420,7 @@ __device__ __forceinline__ void dag_push(const DagDev& d, int t) {
   atomicExch(d.q[c] + slot, t);
 }
 
-__global__ void __launch_bounds__(NT, 1) k_tiled_dag(DagDev d, blrqr_grid g, blrqr_refl rf, double eps, double* ws,
+__global__ void __launch_bounds__(NT, CTAS_PER_SM) k_tiled_dag(DagDev d, blrqr_grid g, blrqr_refl rf, double eps, double* ws,
                                                      long long wsp, int* status, unsigned long long* flops,
                                                      long long timeout_cycles) {
   Ctx cx = make_ctx(ws, wsp, status, flops);
@@ -503,7 +518,7 @@ __global__ void k_dag_init(DagDev d) {
 }
 
 // one level (or any contiguous range) of tiled tasks, one CTA per task
-__global__ void __launch_bounds__(NT, 1) k_tiled(const blrqr_task* tasks, long long t0, long long t1, blrqr_grid g,
+__global__ void __launch_bounds__(NT, CTAS_PER_SM) k_tiled(const blrqr_task* tasks, long long t0, long long t1, blrqr_grid g,
                                                blrqr_refl rf, double eps, double* ws, long long wsp, int* status,
                                                unsigned long long* flops, TeamCtx* team, int* ctr) {
   Ctx cx = make_ctx(ws, wsp, status, flops);
@@ -633,7 +648,7 @@ int64_t blrqr_workspace_doubles(int b, int cap, int max_panel_rows) {
 int blrqr_default_ctas(void) {
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return sms;  // one 512-thread CTA per SM (180 KB shared arena each)
+  return sms * CTAS_PER_SM;  // default: one 512-thread CTA per SM (180 KB shared arena each)
 }
 
 int blrqr_rounded_add_batched(int nbatch, int m, int n, const double* const* ua, const double* const* va,
@@ -904,6 +919,11 @@ void blrqr_set_teams(int enable) {
   if (enable > 1) g_team_slack = enable - 2;  // tuning: enable = 2 + max slack (1 << 20: every task)
 }
 void blrqr_set_dag_rings(int policy) { g_dag_rings = policy == 2 ? 2 : DAG_RINGS; }
+int blrqr_set_qrcp_tol(double tol) {
+  if (!(tol >= 1.0 && tol < 1e8)) return -1;
+  CK(cudaMemcpyToSymbol(g_qrcp_tol, &tol, sizeof(double)));
+  return 0;
+}
 
 
 
@@ -1014,26 +1034,63 @@ int blrqr_grid_pack(const blrqr_grid* g, double* stage, const int64_t* stage_off
   return 0;
 }
 
-int blrqr_blocked_step(const blrqr_grid* g, const blrqr_refl* rf, int k, double eps, double* zbuf, int* zrank,
-                       double* panel_ws, int64_t panel_doubles, double* ws, int64_t ws_per_cta, int nctas,
-                       int* status, unsigned long long* flops, void* stream) {
+int blrqr_blocked_step_dist(const blrqr_grid* g, const blrqr_refl* rf, int k, double eps, double* zbuf, int* zrank,
+                            double* panel_ws, int64_t panel_doubles, double* ws, int64_t ws_per_cta, int nctas,
+                            int phases, int world, int rank, int* status, unsigned long long* flops, void* stream) {
   if (!g || !rf || k < 0 || k >= g->q) return -1;
   if (!(eps > 0.0 && eps < 1.0)) return -2;
   if (panel_doubles < 2LL * g->p * g->b * g->b) return -3;
+  if (phases < 1 || phases > 3) return -4;
+  if (world < 1 || rank < 0 || rank >= world) return -5;
   INIT_KERNELS();
   cudaStream_t st = as_stream(stream);
-  double* P = panel_ws;
-  double* Yp = panel_ws + (int64_t)g->p * g->b * g->b;
-  k_blocked_panel<<<1, NT, SMEM_BYTES, st>>>(*g, *rf, k, P, Yp, ws, ws_per_cta, status, flops);
-  CK(cudaGetLastError());
-  const int nj = g->q - k - 1;
-  if (nj > 0) {
+  if (phases & 1) {
+    double* P = panel_ws;
+    double* Yp = panel_ws + (int64_t)g->p * g->b * g->b;
+    k_blocked_panel<<<1, NT, SMEM_BYTES, st>>>(*g, *rf, k, P, Yp, ws, ws_per_cta, status, flops);
+    CK(cudaGetLastError());
+  }
+  const int nj = owned_count(k + 1, g->q, world, rank);
+  if ((phases & 2) && nj > 0) {
     k_blocked_chain<<<std::min(nj, nctas), NT, SMEM_BYTES, st>>>(*g, *rf, k, eps, zbuf, zrank, ws, ws_per_cta,
-                                                                 status, flops);
+                                                                 status, flops, world, rank);
     CK(cudaGetLastError());
     const int nt = (g->p - k) * nj;
     k_blocked_update<<<std::min(nt, nctas), NT, SMEM_BYTES, st>>>(*g, *rf, k, eps, zbuf, zrank, ws, ws_per_cta,
-                                                                  status, flops);
+                                                                  status, flops, world, rank);
+    CK(cudaGetLastError());
+  }
+  return 0;
+}
+
+int blrqr_blocked_step(const blrqr_grid* g, const blrqr_refl* rf, int k, double eps, double* zbuf, int* zrank,
+                       double* panel_ws, int64_t panel_doubles, double* ws, int64_t ws_per_cta, int nctas,
+                       int* status, unsigned long long* flops, void* stream) {
+  return blrqr_blocked_step_dist(g, rf, k, eps, zbuf, zrank, panel_ws, panel_doubles, ws, ws_per_cta, nctas, 3, 1, 0,
+                                 status, flops, stream);
+}
+
+int blrqr_mgs_step_dist(const blrqr_grid* a, const blrqr_grid* qg, const blrqr_grid* rg, int j, double eps,
+                        double* panel_ws, int64_t panel_doubles, double* ws, int64_t ws_per_cta, int nctas,
+                        int phases, int world, int rank, int* status, unsigned long long* flops, void* stream) {
+  if (!a || !qg || !rg || j < 0 || j >= a->q) return -1;
+  if (!(eps > 0.0 && eps < 1.0)) return -2;
+  if (panel_doubles < (int64_t)a->p * a->b * a->b) return -3;
+  if (phases < 1 || phases > 3) return -4;
+  if (world < 1 || rank < 0 || rank >= world) return -5;
+  INIT_KERNELS();
+  cudaStream_t st = as_stream(stream);
+  if (phases & 1) {
+    k_mgs_panel_task<<<1, NT, SMEM_BYTES, st>>>(*a, *qg, *rg, j, panel_ws, ws, ws_per_cta, status, flops);
+    CK(cudaGetLastError());
+  }
+  const int nk = owned_count(j + 1, a->q, world, rank);
+  if ((phases & 2) && nk > 0) {
+    k_mgs_project<<<std::min(nk, nctas), NT, SMEM_BYTES, st>>>(*a, *qg, *rg, j, eps, ws, ws_per_cta, status, flops,
+                                                               world, rank);
+    CK(cudaGetLastError());
+    k_mgs_update<<<std::min(nk * a->p, nctas), NT, SMEM_BYTES, st>>>(*a, *qg, *rg, j, eps, ws, ws_per_cta, status,
+                                                                     flops, world, rank);
     CK(cudaGetLastError());
   }
   return 0;
@@ -1042,28 +1099,14 @@ int blrqr_blocked_step(const blrqr_grid* g, const blrqr_refl* rf, int k, double 
 int blrqr_mgs_step(const blrqr_grid* a, const blrqr_grid* qg, const blrqr_grid* rg, int j, double eps,
                    double* panel_ws, int64_t panel_doubles, double* ws, int64_t ws_per_cta, int nctas, int* status,
                    unsigned long long* flops, void* stream) {
-  if (!a || !qg || !rg || j < 0 || j >= a->q) return -1;
-  if (!(eps > 0.0 && eps < 1.0)) return -2;
-  if (panel_doubles < (int64_t)a->p * a->b * a->b) return -3;
-  INIT_KERNELS();
-  cudaStream_t st = as_stream(stream);
-  k_mgs_panel_task<<<1, NT, SMEM_BYTES, st>>>(*a, *qg, *rg, j, panel_ws, ws, ws_per_cta, status, flops);
-  CK(cudaGetLastError());
-  const int nk = a->q - j - 1;
-  if (nk > 0) {
-    k_mgs_project<<<std::min(nk, nctas), NT, SMEM_BYTES, st>>>(*a, *qg, *rg, j, eps, ws, ws_per_cta, status, flops);
-    CK(cudaGetLastError());
-    k_mgs_update<<<std::min(nk * a->p, nctas), NT, SMEM_BYTES, st>>>(*a, *qg, *rg, j, eps, ws, ws_per_cta, status,
-                                                                     flops);
-    CK(cudaGetLastError());
-  }
-  return 0;
+  return blrqr_mgs_step_dist(a, qg, rg, j, eps, panel_ws, panel_doubles, ws, ws_per_cta, nctas, 3, 1, 0, status,
+                             flops, stream);
 }
 
 }  // extern "C"
 
 // ---- debug: single-CTA GEMM throughput probe -------------------------------
-__global__ void __launch_bounds__(NT, 1) k_gemm_probe(int ta, int tb, int M, int N, int K, const double* A, int lda,
+__global__ void __launch_bounds__(NT, CTAS_PER_SM) k_gemm_probe(int ta, int tb, int M, int N, int K, const double* A, int lda,
                                                       const double* B, int ldb, double* C, int ldc, int reps) {
   for (int r = 0; r < reps; ++r) gemm(ta != 0, tb != 0, M, N, K, 1.0, A, lda, B, ldb, r == 0 ? 0.0 : 1.0, C, ldc);
 }
@@ -1071,7 +1114,7 @@ __global__ void __launch_bounds__(NT, 1) k_gemm_probe(int ta, int tb, int M, int
 // Jacobi probe: one task = the one-sided Jacobi of X (rows x ncols, global)
 // with J (ncols x ncols); mode 0 jacobi_blocked, 1 jacobi_cols, 2 team (idle
 // CTAs of the launch help).  Used by tools/bench_jacobi.py.
-__global__ void __launch_bounds__(NT, 1) k_jacobi_probe(int rows, int ncols, double* X, double* J, double* sigma,
+__global__ void __launch_bounds__(NT, CTAS_PER_SM) k_jacobi_probe(int rows, int ncols, double* X, double* J, double* sigma,
                                                         int* perm, int mode, double* ws, long long wsp, int* status,
                                                         unsigned long long* flops, TeamCtx* team, int* ctr) {
   Ctx cx = make_ctx(ws, wsp, status, flops);
@@ -1165,7 +1208,7 @@ __device__ void trap_apply_dense_dev(Ctx& cx, const Blk& yt, const double* T, in
   release(cx, mk);
 }
 
-__global__ void __launch_bounds__(NT, 1) k_apply_q(blrqr_grid g, blrqr_refl rf, int method, double* C, long long ldc,
+__global__ void __launch_bounds__(NT, CTAS_PER_SM) k_apply_q(blrqr_grid g, blrqr_refl rf, int method, double* C, long long ldc,
                                                    int nc, int transpose, double* ws, long long wsp, int* status,
                                                    unsigned long long* flops) {
   Ctx cx = make_ctx(ws, wsp, status, flops);
@@ -1236,7 +1279,7 @@ __global__ void __launch_bounds__(NT, 1) k_apply_q(blrqr_grid g, blrqr_refl rf, 
 }
 
 // dense D (m x n, column-major, ldd) = expanded grid
-__global__ void __launch_bounds__(NT, 1) k_blr_to_dense(blrqr_grid g, double* D, long long ldd) {
+__global__ void __launch_bounds__(NT, CTAS_PER_SM) k_blr_to_dense(blrqr_grid g, double* D, long long ldd) {
   const int b = g.b;
   for (int c = blockIdx.x; c < g.p * g.q; c += gridDim.x) {
     const int i = c / g.q, j = c % g.q;
@@ -1272,5 +1315,78 @@ extern "C" int blrqr_blr_to_dense(const blrqr_grid* g, double* D, int64_t ldd, v
   cudaFuncSetAttribute(k_blr_to_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   k_blr_to_dense<<<std::min(g->p * g->q, 4096), NT, SMEM_BYTES, as_stream(stream)>>>(*g, D, ldd);
   CK(cudaGetLastError());
+  return 0;
+}
+
+// ---- apply Q / Q^T to a block low-rank operand (factorize.py:343-350 blocked,
+// :534-567 tiled): the factorization's kind-aware block updates with rounded
+// additions, on an operand grid gt with its own kind map.  One launch per
+// step, parallel over the operand's block columns j (each step's j-loop is
+// independent in the reference).
+//   tiled:   phase 0 = diag_apply(k) over j; phase 1 = _trap_apply_pair(k, i) over j
+//   blocked: phase 0 = chain z_j over j;   phase 1 = C_ij -= Y_ik z_j over (i, j)
+__global__ void __launch_bounds__(NT, CTAS_PER_SM) k_apply_q_blr(blrqr_grid gr, blrqr_refl rf, blrqr_grid gt,
+                                                                 int method, int phase, int k, int i, int transpose,
+                                                                 double eps, double* zbuf, int* zrank, double* ws,
+                                                                 long long wsp, int* status,
+                                                                 unsigned long long* flops) {
+  Ctx cx = make_ctx(ws, wsp, status, flops);
+  const long long bb = (long long)gr.b * gr.b;
+  const int nj = gt.q, ni = gr.p - k;
+  const int items = (method == 1 && phase == 1) ? ni * nj : nj;
+  for (int t = blockIdx.x; t < items; t += gridDim.x) {
+    if (method == 0) {
+      if (phase == 0) tiled_block_op(cx, gr, rf, gt, k, t, transpose != 0);
+      else tiled_trap_op(cx, gr, rf, gt, eps, k, i, t, transpose != 0);
+    } else {
+      if (phase == 0) {
+        blocked_chain_op(cx, gr, rf, gt, eps, k, t, zbuf + 2 * bb * t, zbuf + 2 * bb * t + bb, zrank + t,
+                         transpose != 0);
+      } else {
+        const int ii = k + t % ni, j = t / ni;
+        blocked_update_op(cx, gr, rf, gt, eps, k, ii, j, zbuf + 2 * bb * j, zbuf + 2 * bb * j + bb, zrank + j);
+      }
+    }
+    cx.top = 0;
+    cx.stop = 0;
+    __syncthreads();
+  }
+}
+
+extern "C" int blrqr_apply_q_blr(const blrqr_grid* gr, const blrqr_refl* rf, int method, const blrqr_grid* c,
+                                 int transpose, double eps, double* zbuf, int* zrank, double* ws, int64_t ws_per_cta,
+                                 int nctas, int* status, unsigned long long* flops, void* stream) {
+  if (!gr || !rf || !c || method < 0 || method > 1) return -1;
+  if (c->p != gr->p || c->b != gr->b) return -4;
+  if (!(eps > 0.0 && eps < 1.0)) return -6;
+  if (method == 1 && (!zbuf || !zrank)) return -7;
+  INIT_KERNELS();
+  cudaFuncSetAttribute(k_apply_q_blr, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  cudaStream_t st = as_stream(stream);
+  const int p = gr->p, q = gr->q, nj = c->q;
+  if (nj == 0) return 0;
+  auto launch = [&](int phase, int k, int i, int items) -> int {
+    k_apply_q_blr<<<std::max(1, std::min(items, nctas)), NT, SMEM_BYTES, st>>>(
+        *gr, *rf, *c, method, phase, k, i, transpose, eps, zbuf, zrank, ws, ws_per_cta, status, flops);
+    CK(cudaGetLastError());
+    return 0;
+  };
+  for (int kk = 0; kk < q; ++kk) {
+    const int k = transpose ? kk : q - 1 - kk;
+    if (method == 0) {
+      if (transpose) {  // factorize.py:536-546
+        if (int e = launch(0, k, 0, nj)) return e;
+        for (int i = k + 1; i < p; ++i)
+          if (int e = launch(1, k, i, nj)) return e;
+      } else {  // factorize.py:548-558
+        for (int i = p - 1; i > k; --i)
+          if (int e = launch(1, k, i, nj)) return e;
+        if (int e = launch(0, k, 0, nj)) return e;
+      }
+    } else {  // factorize.py:343-350
+      if (int e = launch(0, k, 0, nj)) return e;
+      if (int e = launch(1, k, 0, (p - k) * nj)) return e;
+    }
+  }
   return 0;
 }

@@ -11,7 +11,17 @@
 
 namespace blr {
 
-constexpr int NT = 512;          // threads per CTA (one CTA per SM)
+#ifndef BLR_NT
+#define BLR_NT 512
+#endif
+#ifndef BLR_CTAS_PER_SM
+#define BLR_CTAS_PER_SM 1
+#endif
+#ifndef BLR_SMEM_ARENA
+#define BLR_SMEM_ARENA 23040
+#endif
+constexpr int NT = BLR_NT;          // threads per CTA (default: one 512-thread CTA per SM)
+constexpr int CTAS_PER_SM = BLR_CTAS_PER_SM;
 constexpr int NWARP = NT / 32;
 
 // status bits (OR-ed into a device word; see include/blrqr.h)
@@ -45,7 +55,7 @@ struct Ctx {
 
 // dynamic shared-memory arena per CTA (doubles): one 512-thread CTA per SM
 // owns ~180 KB next to the static GEMM scratch (see GEMM_SMEM)
-constexpr int SMEM_ARENA = 23040;  // 180 KB
+constexpr int SMEM_ARENA = BLR_SMEM_ARENA;  // 180 KB by default
 
 // the dynamic shared-memory arena (declared once; pointers derived from it
 // compile to LDS/STS instead of generic loads)

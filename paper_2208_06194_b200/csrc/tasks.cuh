@@ -112,19 +112,26 @@ __device__ void tiled_diag(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, i
   t.stop(cx, PH_GEQRT);
 }
 
-__device__ void tiled_block(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, int k, int j) {
-  const long long c = (long long)k * g.q + k;
+// diag_apply (factorize.py:387-396 / tiled_apply_q :521-532): Q_kk^T (or
+// Q_kk) applied to cell (k, j) of the target grid gt; reflectors of gr / rf.
+__device__ void tiled_block_op(Ctx& cx, const blrqr_grid& gr, const blrqr_refl& rf, const blrqr_grid& gt, int k,
+                               int j, bool transpose) {
+  const long long c = (long long)k * gr.q + k;
   const double* Y = rf.pool + rf.y_off[c];
   const double* T = rf.pool + rf.t_off[c];
-  Cell x = grid_cell(g, k, j);
+  Cell x = grid_cell(gt, k, j);
   PhaseTimer t;
   if (x.lr) {
     const int r = *x.rank;
-    if (r) apply_wy_dev(cx, g.b, g.b, r, Y, g.b, T, g.b, x.u, x.ld, true);
+    if (r) apply_wy_dev(cx, gr.b, gr.b, r, Y, gr.b, T, gr.b, x.u, x.ld, transpose);
   } else {
-    apply_wy_dev(cx, g.b, g.b, g.b, Y, g.b, T, g.b, x.u, x.ld, true);
+    apply_wy_dev(cx, gr.b, gr.b, gr.b, Y, gr.b, T, gr.b, x.u, x.ld, transpose);
   }
   t.stop(cx, PH_APPLYWY);
+}
+
+__device__ void tiled_block(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, int k, int j) {
+  tiled_block_op(cx, g, rf, g, k, j, true);
 }
 
 __device__ void tiled_update(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, int k, int i) {
@@ -174,18 +181,21 @@ __device__ void tiled_update(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf,
   cx.top = mark;
 }
 
-__device__ void tiled_trap(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, double eps, int k, int i, int j) {
+// _trap_apply_pair (factorize.py:428-444) on cells (k, j), (i, j) of the
+// target grid gt with the trapezoidal reflector (i, k) of gr / rf.
+__device__ void tiled_trap_op(Ctx& cx, const blrqr_grid& gr, const blrqr_refl& rf, const blrqr_grid& gt, double eps,
+                              int k, int i, int j, bool transpose) {
   const long long mark = cx.top;
-  const Blk yt = refl_blk(g, rf, i, k);
-  const double* T = rf.pool + rf.t_off[(long long)i * g.q + k];
-  Cell top = grid_cell(g, k, j), bot = grid_cell(g, i, j);
+  const Blk yt = refl_blk(gr, rf, i, k);
+  const double* T = rf.pool + rf.t_off[(long long)i * gr.q + k];
+  Cell top = grid_cell(gt, k, j), bot = grid_cell(gt, i, j);
   const Blk tb = cell_blk(top), bb = cell_blk(bot);
   PhaseTimer t1;
   Blk prod = blk_mul_t(cx, yt, bb);
   t1.stop(cx, PH_PRODUCT);
-  Blk ssum = blk_acc(cx, tb, prod, eps, g.b);
+  Blk ssum = blk_acc(cx, tb, prod, eps, gt.b);
   PhaseTimer t2;
-  Blk w = blk_dense_times(cx, T, g.b, true, ssum);
+  Blk w = blk_dense_times(cx, T, gr.b, transpose, ssum);
   t2.stop(cx, PH_PRODUCT);
   sub_into_cell(cx, top, w, eps);
   PhaseTimer t3;
@@ -193,6 +203,10 @@ __device__ void tiled_trap(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, d
   t3.stop(cx, PH_PRODUCT);
   sub_into_cell(cx, bot, yw, eps);
   cx.top = mark;
+}
+
+__device__ void tiled_trap(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, double eps, int k, int i, int j) {
+  tiled_trap_op(cx, g, rf, g, eps, k, i, j, true);
 }
 
 // Split ApplyTrapReflector for the dynamic scheduler: the top half computes

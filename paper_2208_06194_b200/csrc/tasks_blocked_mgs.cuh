@@ -97,21 +97,23 @@ __device__ __forceinline__ Blk column_entry(const blrqr_grid& g, const blrqr_ref
   return refl_blk(g, rf, i, k);
 }
 
-// _refcol_apply_blr first half (factorize.py:240-246): s = sum_i Y_ik^T A_ij
-// (ascending i, rounded additions), z = T^T s -> zbuf slot j.
-__device__ void blocked_chain(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, double eps, int k, int j,
-                              double* zu, double* zv, int* zrank) {
-  const int b = g.b;
+// _refcol_apply_blr first half (factorize.py:240-246): s = sum_i Y_ik^T C_ij
+// (ascending i, rounded additions), z = op(T) s -> zbuf slot j.  Reflector
+// column k of gr / rf; target column j of gt (gt = gr in the factorization,
+// an operand grid in blocked_apply_q).
+__device__ void blocked_chain_op(Ctx& cx, const blrqr_grid& gr, const blrqr_refl& rf, const blrqr_grid& gt, double eps,
+                                 int k, int j, double* zu, double* zv, int* zrank, bool transpose) {
+  const int b = gr.b;
   const Mark mk = mark(cx);
   double* bu[2] = {alloc(cx, (long long)b * b), alloc(cx, (long long)b * b)};
   double* bv[2] = {alloc(cx, (long long)b * b), alloc(cx, (long long)b * b)};
   if (!bu[0] || !bu[1] || !bv[0] || !bv[1]) { release(cx, mk); return; }
   Blk acc;
   int slot = 0;
-  for (int i = k; i < g.p; ++i) {
+  for (int i = k; i < gr.p; ++i) {
     const Mark it = mark(cx);
-    const Blk y = column_entry(g, rf, i, k);
-    const Blk a = cell_blk(grid_cell(g, i, j));
+    const Blk y = column_entry(gr, rf, i, k);
+    const Blk a = cell_blk(grid_cell(gt, i, j));
     PhaseTimer tp;
     Blk term = blk_mul_t(cx, y, a);
     tp.stop(cx, PH_PRODUCT);
@@ -123,9 +125,9 @@ __device__ void blocked_chain(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf
     slot ^= 1;
     release(cx, it);
   }
-  const double* T = rf.pool + rf.t_off[(long long)k * g.q + k];
+  const double* T = rf.pool + rf.t_off[(long long)k * gr.q + k];
   PhaseTimer tp;
-  Blk z = blk_dense_times(cx, T, b, true, acc);
+  Blk z = blk_dense_times(cx, T, b, transpose, acc);
   tp.stop(cx, PH_PRODUCT);
   if (z.lr) {
     copy_mat(b, z.rank, z.u, z.ldu, zu, b, z.s);
@@ -139,19 +141,29 @@ __device__ void blocked_chain(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf
   release(cx, mk);
 }
 
-// _refcol_apply_blr second half (factorize.py:247-249): A_ij -= Y_ik z_j
-__device__ void blocked_update(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, double eps, int k, int i, int j,
-                               double* zu, double* zv, const int* zrank) {
-  const int b = g.b;
+__device__ void blocked_chain(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, double eps, int k, int j,
+                              double* zu, double* zv, int* zrank) {
+  blocked_chain_op(cx, g, rf, g, eps, k, j, zu, zv, zrank, true);
+}
+
+// _refcol_apply_blr second half (factorize.py:247-249): C_ij -= Y_ik z_j
+__device__ void blocked_update_op(Ctx& cx, const blrqr_grid& gr, const blrqr_refl& rf, const blrqr_grid& gt,
+                                  double eps, int k, int i, int j, double* zu, double* zv, const int* zrank) {
+  const int b = gr.b;
   const Mark mk = mark(cx);
   const int zr = *zrank;
   const Blk z = zr >= 0 ? make_lr(b, b, zr, zu, b, zv, b, 1.0) : make_dense(b, b, zu, b, 1.0);
-  const Blk y = column_entry(g, rf, i, k);
+  const Blk y = column_entry(gr, rf, i, k);
   PhaseTimer tp;
   Blk upd = blk_mul(cx, y, z);
   tp.stop(cx, PH_PRODUCT);
-  sub_into_cell(cx, grid_cell(g, i, j), upd, eps);
+  sub_into_cell(cx, grid_cell(gt, i, j), upd, eps);
   release(cx, mk);
+}
+
+__device__ void blocked_update(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, double eps, int k, int i, int j,
+                               double* zu, double* zv, const int* zrank) {
+  blocked_update_op(cx, g, rf, g, eps, k, i, j, zu, zv, zrank);
 }
 
 // ---------------------------------------------------------------------------

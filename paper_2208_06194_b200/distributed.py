@@ -1,5 +1,8 @@
-"""Multi-GPU tiled Householder BLR-QR: 1-D block-cyclic columns + reflector
-broadcast.
+"""Multi-GPU BLR-QR: 1-D block-cyclic columns + panel broadcast.
+
+All three methods.  Tiled Householder is described first; blocked
+Householder and blocked MGS (``run_column_distributed``) follow the same
+ownership with one broadcast per panel.
 
 Column j (every block row of it, including R-tilde's row blocks) lives on
 rank j mod G.  Task ownership follows the written cells
@@ -152,4 +155,168 @@ def factorize_distributed(grid, cfg, world: int, rank: int, broadcast=None):
             dist.broadcast(t, src)
     st = GpuStore(grid, cfg, world, rank)
     run_tiled_distributed(st, st.plan, world, rank, broadcast)
+    return st
+
+
+# ---------------------------------------------------------------------------
+# blocked Householder and blocked MGS
+# ---------------------------------------------------------------------------
+# Both methods are "factor panel c, then update every column right of c
+# independently" (factorize.py:285-292, :661-671).  Column c's owner runs the
+# panel (triangularize_block_column, factorize.py:187-229 / MgsState.panel,
+# :605-632) and broadcasts its payload -- the ReflectorColumn (y_kk, T_k and
+# every Ytilde_ik) for blocked HH, the explicit Q column j for MGS -- and then
+# every rank applies it to the columns it owns (apply_block_column_reflector,
+# :252-262 / project + update, :634-655).  Each column's arithmetic is the
+# single-GPU one (same chain order), so the assembled result is bitwise the
+# single-GPU factorization.
+
+
+def run_column_distributed(store, ncols: int, world: int, rank: int, broadcast) -> None:
+    """store.panel(c)             -- factor panel c (called on its owner only)
+    store.panel_buffers(c)       -- tensors holding panel c's payload
+    store.received(c, buffers)   -- unpack on non-owners (no-op when in place)
+    store.apply(c)               -- apply panel c to this rank's columns > c
+    broadcast(tensor, src)       -- in-place collective broadcast"""
+    for c in range(ncols):
+        src = column_owner(c, world)
+        if src == rank:
+            store.panel(c)
+        if world > 1:
+            bufs = store.panel_buffers(c)
+            for buf in bufs:
+                broadcast(buf, src)
+            if src != rank:
+                store.received(c, bufs)
+        store.apply(c)
+    store.finish()
+
+
+class _ColumnGpuStore:
+    def __init__(self, world: int, rank: int, cfg):
+        from . import _lib
+
+        self.lib = _lib
+        self.rt = _lib.runtime()
+        self.world, self.rank, self.cfg = world, rank, cfg
+
+    def _cell_payload(self, g, i, j):
+        """Views of cell (i, j)'s storage: U and V slabs (LR) or the block."""
+        c = i * g.q + j
+        o = int(g.off_u_host[c])
+        if g.kind_host[i, j]:
+            return [g.pool[o:o + 2 * g.b * g.cap], g.rank[c:c + 1]]  # U slab then V slab
+        return [g.pool[o:o + g.b * g.b]]
+
+    def received(self, c, bufs):
+        pass  # broadcasts land in place
+
+    def finish(self):
+        pass
+
+
+class BlockedGpuStore(_ColumnGpuStore):
+    """A rank's device grid + reflector store for blocked Householder."""
+
+    def __init__(self, grid, cfg, world: int, rank: int):
+        from .device import DeviceRefl
+
+        super().__init__(world, rank, cfg)
+        self.g = grid
+        self.rf = DeviceRefl(grid)
+        dev = self.rt.dev
+        self.zbuf = torch.empty(grid.q * 2 * grid.b * grid.b, dtype=torch.float64, device=dev)
+        self.zrank = torch.zeros(grid.q, dtype=torch.int32, device=dev)
+        self.panel_ws = torch.empty(2 * grid.p * grid.b * grid.b, dtype=torch.float64, device=dev)
+
+    def _step(self, k, phases):
+        rt, g = self.rt, self.g
+        ws, per, nct = rt.workspace(g.b, g.cap)
+        gs, rs = g.cstruct(), self.rf.cstruct()
+        self.lib.check(rt.lib.blrqr_blocked_step_dist(
+            C.byref(gs), C.byref(rs), k, self.cfg.epsilon, self.zbuf.data_ptr(), self.zrank.data_ptr(),
+            self.panel_ws.data_ptr(), self.panel_ws.numel(), ws, per, nct, phases, self.world, self.rank,
+            rt.status.data_ptr(), rt.flops.data_ptr(), self.lib.stream_ptr()), "blocked_step_dist")
+
+    def panel(self, k):
+        self._step(k, 1)
+
+    def apply(self, k):
+        self._step(k, 2)
+
+    def panel_buffers(self, k):
+        """ReflectorColumn k (factorize.py:146-156): y_kk and T_k (adjacent in
+        the store), then per i > k the Ytilde_ik payload: the LR cell's U / V
+        slabs (V holds y_i^T) + yrank, or the dense Y block."""
+        g, rf, b, q = self.g, self.rf, self.g.b, self.g.q
+        c = k * q + k
+        y = int(rf.y_off_host[c])
+        bufs = [rf.pool[y:y + 2 * b * b]]
+        for i in range(k + 1, g.p):
+            c = i * q + k
+            if g.kind_host[i, k]:
+                o = int(g.off_u_host[c])
+                bufs.append(g.pool[o:o + 2 * b * g.cap])
+            else:
+                y = int(rf.y_off_host[c])
+                bufs.append(rf.pool[y:y + b * b])
+            bufs.append(rf.yrank[c:c + 1])
+        return bufs
+
+
+class MgsGpuStore(_ColumnGpuStore):
+    """A rank's device grids (A, explicit Q, R) for blocked MGS."""
+
+    def __init__(self, grid, cfg, world: int, rank: int):
+        from .device import DeviceGrid
+
+        super().__init__(world, rank, cfg)
+        g = grid
+        self.g = g
+        self.qg = DeviceGrid(g.m, g.n, g.b, g.kind_host, g.cap)
+        rl = g.kind_host[: g.q, :].copy()
+        d = np.arange(g.q)
+        rl[d, d] = False
+        self.rg = DeviceGrid(g.n, g.n, g.b, rl, g.cap)
+        self.panel_ws = torch.empty(g.p * g.b * g.b, dtype=torch.float64, device=self.rt.dev)
+
+    def _step(self, j, phases):
+        rt, g = self.rt, self.g
+        ws, per, nct = rt.workspace(g.b, g.cap)
+        gs, qs, rs = g.cstruct(), self.qg.cstruct(), self.rg.cstruct()
+        self.lib.check(rt.lib.blrqr_mgs_step_dist(
+            C.byref(gs), C.byref(qs), C.byref(rs), j, self.cfg.epsilon, self.panel_ws.data_ptr(),
+            self.panel_ws.numel(), ws, per, nct, phases, self.world, self.rank, rt.status.data_ptr(),
+            rt.flops.data_ptr(), self.lib.stream_ptr()), "mgs_step_dist")
+
+    def panel(self, j):
+        self._step(j, 1)
+
+    def apply(self, j):
+        self._step(j, 2)
+
+    def panel_buffers(self, j):
+        """Explicit Q column j: every block of qg's column j."""
+        bufs = []
+        for i in range(self.g.p):
+            bufs += self._cell_payload(self.qg, i, j)
+        return bufs
+
+
+def factorize_columns_distributed(method: str, grid, cfg, world: int, rank: int, broadcast=None):
+    """Distributed blocked-hh / mgs on this rank's GPU.  ``grid`` holds the
+    full input (only owned columns are read and written).  Returns the store:
+    owned columns of store.g (blocked) / store.rg (mgs) hold R-tilde."""
+    if broadcast is None:
+        import torch.distributed as dist
+
+        def broadcast(t, src):
+            dist.broadcast(t, src)
+    if method == "blocked-hh":
+        st = BlockedGpuStore(grid, cfg, world, rank)
+    elif method == "mgs":
+        st = MgsGpuStore(grid, cfg, world, rank)
+    else:
+        raise ValueError(f"column-cyclic driver covers blocked-hh and mgs, not {method!r}")
+    run_column_distributed(st, grid.q, world, rank, broadcast)
     return st

@@ -289,19 +289,26 @@ def blocked_mgs_qr(a: BlrMatrix, cfg: ToleranceConfig) -> FactorizationResult:
     return _host_entry("mgs", a, cfg)
 
 
-def _apply_q_dense(result, c: np.ndarray, transpose: bool, method: str) -> np.ndarray:
-    """Q (or Q^T) times a dense host operand, on the GPU."""
+def _upload_result(result, method: str) -> "DeviceFactorization":
+    """A host FactorizationResult's R-tilde grid + reflectors on the device."""
     from .metrics import _upload_reflectors
 
     rt = _lib.runtime()
-    m = result.r.structure.m
-    if c.ndim != 2 or c.shape[0] != m:
-        raise ValueError(f"operand has {c.shape[0]} rows, expected {m}")
     f = DeviceFactorization.__new__(DeviceFactorization)
     f.method, f.rt = method, rt
     f.g = DeviceGrid.from_host(result.r)
     f.rf = DeviceRefl(f.g)
     _upload_reflectors(f, result)
+    return f
+
+
+def _apply_q_dense(result, c: np.ndarray, transpose: bool, method: str) -> np.ndarray:
+    """Q (or Q^T) times a dense host operand, on the GPU."""
+    rt = _lib.runtime()
+    m = result.r.structure.m
+    if c.ndim != 2 or c.shape[0] != m:
+        raise ValueError(f"operand has {c.shape[0]} rows, expected {m}")
+    f = _upload_result(result, method)
     nc = c.shape[1]
     ct = torch.from_numpy(np.ascontiguousarray(np.asarray(c, dtype=np.float64).T)).to(rt.dev)
     ws, per, nct = rt.workspace(f.g.b, f.g.cap)
@@ -313,25 +320,53 @@ def _apply_q_dense(result, c: np.ndarray, transpose: bool, method: str) -> np.nd
     return np.ascontiguousarray(ct.cpu().numpy().T)
 
 
+def _apply_q_blr(result, c: BlrMatrix, transpose: bool, cfg: ToleranceConfig, method: str) -> BlrMatrix:
+    """Q (or Q^T) times a block low-rank host operand, on the GPU: the
+    factorization's kind-aware block updates with rounded additions
+    (factorize.py:343-350 blocked, :534-567 tiled); the input is not mutated."""
+    rt = _lib.runtime()
+    rm = result.r.structure
+    if c.structure.m != rm.m:
+        raise ValueError("operand row count does not match the factorization")
+    if c.structure.b != rm.b:
+        raise ValueError("operand block size does not match the factorization")
+    f = _upload_result(result, method)
+    gc = DeviceGrid.from_host(c)
+    b = gc.b
+    zbuf = zrank = None
+    if method == "blocked-hh":
+        zbuf = torch.empty(gc.q * 2 * b * b, dtype=torch.float64, device=rt.dev)
+        zrank = torch.zeros(gc.q, dtype=torch.int32, device=rt.dev)
+    ws, per, nct = rt.workspace(b, max(f.g.cap, gc.cap))
+    gs, rs, cs = f.g.cstruct(), f.rf.cstruct(), gc.cstruct()
+    _lib.check(rt.lib.blrqr_apply_q_blr(C.byref(gs), C.byref(rs), 0 if method == "tiled-hh" else 1, C.byref(cs),
+                                        int(transpose), cfg.epsilon,
+                                        zbuf.data_ptr() if zbuf is not None else None,
+                                        zrank.data_ptr() if zrank is not None else None, ws, per, nct,
+                                        rt.status.data_ptr(), rt.flops.data_ptr(), _lib.stream_ptr()), "apply_q_blr")
+    rt.harvest()
+    return gc.to_host()
+
+
 def blocked_apply_q(result, c, transpose, cfg=None):
-    """factorize.py:326-361 for dense operands (GPU).  Block low-rank operands
-    are not supported on the device path (they are not on the factorization
-    path)."""
+    """factorize.py:326-361 on the GPU: dense operands with plain dense
+    arithmetic, block low-rank operands with the factorization's kind-aware
+    updates (needs a tolerance config)."""
     if result.q_columns is None:
         raise ValueError("result does not carry blocked reflector columns")
     if not isinstance(c, np.ndarray):
         if cfg is None:
             raise ValueError("block low-rank operands need a tolerance config")
-        raise NotImplementedError("BLR operands for apply-Q are not built on the GPU path")
+        return _apply_q_blr(result, c, transpose, cfg, "blocked-hh")
     return _apply_q_dense(result, c, transpose, "blocked-hh")
 
 
 def tiled_apply_q(result, c, transpose, cfg=None):
-    """factorize.py:495-568 for dense operands (GPU)."""
+    """factorize.py:495-568 on the GPU (dense and block low-rank operands)."""
     if result.q_tiles is None:
         raise ValueError("result does not carry tiled reflectors")
     if not isinstance(c, np.ndarray):
         if cfg is None:
             raise ValueError("block low-rank operands need a tolerance config")
-        raise NotImplementedError("BLR operands for apply-Q are not built on the GPU path")
+        return _apply_q_blr(result, c, transpose, cfg, "tiled-hh")
     return _apply_q_dense(result, c, transpose, "tiled-hh")
