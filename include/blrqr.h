@@ -70,9 +70,10 @@ typedef struct {
   const int64_t* y_off;
   const int64_t* t_off;
   int* yrank;
-  /* dynamic scheduler only: per-cell slot (wslot doubles at wpool + c*wslot)
-   * holding w = T_ik^T (R_kj + Ytilde^T A_ij) between the two halves of a
-   * split ApplyTrapReflector; wrank[c] its rank (-1 dense).  NULL otherwise. */
+  /* dynamic scheduler only: two slots per cell (wslot doubles at wpool +
+   * s*wslot, s = (k & 1)*p*q + i*q + j) holding w = T_ik^T (R_kj + Ytilde^T
+   * A_ij) between the parts of a split ApplyTrapReflector(k, i, j); wrank[s]
+   * its rank (-1 dense).  NULL otherwise. */
   double* wpool;
   int* wrank;
   int64_t wslot; /* doubles per cell slot (2*b*cap; a dense w needs b*b <= wslot) */
@@ -80,9 +81,9 @@ typedef struct {
 
 /* one tiled task: kind 0 DiagQR(k), 1 ApplyBlockReflector(k,j),
  * 2 UpdateQR(k,i), 3 ApplyTrapReflector(k,i,j) (scheduler.py:61-70);
- * the dynamic scheduler splits kind 3 into 4 (top half: R_kj update, stores
- * w) and 5 (bottom half: A_ij -= Ytilde w), which may run concurrently with
- * the next link of the R_kj chain. */
+ * the dynamic scheduler splits kind 3 into 4 (w = T^T (R_kj + Ytilde^T A_ij)
+ * into the cell's w slot), 6 (R_kj -= w) and 5 (A_ij -= Ytilde w); 6 and 5
+ * run concurrently, and 5 no longer waits for the R_kj update. */
 typedef struct {
   int kind, k, i, j;
 } blrqr_task;

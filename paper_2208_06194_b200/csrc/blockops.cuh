@@ -197,7 +197,7 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
   for (int j = threadIdx.x >> 5; j < kp; j += NWARP)
     for (int i = threadIdx.x & 31; i < kp; i += 32) W2[i + (long long)j * kp] = i <= j ? X[i + (long long)j * k] : 0.0;
   __syncthreads();
-  if (in_smem(cx, W2) && in_smem(cx, J))
+  if (in_smem(cx, W2) && in_smem(cx, J) && kp <= JAC_SMEM_MAXC)
     jacobi_smem(cx, kp, kp, W2, J, sig, perm, cx.flops);  // shared-space loads, 2 pairs per warp
   else if (kp <= 32 || (!team_jacobi_lead(cx, kp, kp, W2, kp, J, kp, sig, perm) &&
                         !jacobi_blocked(cx, kp, kp, W2, kp, J, kp, sig, perm, cx.flops)))

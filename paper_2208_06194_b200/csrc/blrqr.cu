@@ -485,8 +485,9 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM) k_tiled_dag(DagDev d, blrqr_g
       case 0: tiled_diag(cx, g, rf, tk.k); break;
       case 1: tiled_block(cx, g, rf, tk.k, tk.j); break;
       case 2: tiled_update(cx, g, rf, tk.k, tk.i); break;
-      case 4: tiled_trap_a(cx, g, rf, eps, tk.k, tk.i, tk.j); break;
+      case 4: tiled_trap_a1(cx, g, rf, eps, tk.k, tk.i, tk.j); break;
       case 5: tiled_trap_b(cx, g, rf, eps, tk.k, tk.i, tk.j); break;
+      case 6: tiled_trap_a2(cx, g, rf, eps, tk.k, tk.i, tk.j); break;
       default: tiled_trap(cx, g, rf, eps, tk.k, tk.i, tk.j); break;
     }
     tt.stop(cx, PH_TASK);
@@ -767,14 +768,17 @@ static void tiled_access(const blrqr_task& t, std::vector<int64_t>& rd, std::vec
   auto A = [](int i, int j) { return ((int64_t)0 << 40) | ((int64_t)i << 20) | j; };
   auto D = [](int k) { return ((int64_t)1 << 40) | ((int64_t)k << 20) | k; };
   auto U = [](int i, int k) { return ((int64_t)2 << 40) | ((int64_t)i << 20) | k; };
-  auto W = [](int i, int j) { return ((int64_t)3 << 40) | ((int64_t)i << 20) | j; };
+  // w slots: two per cell, by the parity of k (tasks.cuh w_index)
+  auto W = [&t](int i, int j) { return ((int64_t)(3 + (t.k & 1)) << 40) | ((int64_t)i << 20) | j; };
   rd.clear();
   wr.clear();
   switch (t.kind) {
     case 0: rd = {A(t.k, t.k)}; wr = {A(t.k, t.k), D(t.k)}; break;
     case 1: rd = {D(t.k), A(t.k, t.j)}; wr = {A(t.k, t.j)}; break;
     case 2: rd = {A(t.k, t.k), A(t.i, t.k)}; wr = {A(t.k, t.k), A(t.i, t.k), U(t.i, t.k)}; break;
-    case 4: rd = {U(t.i, t.k), A(t.k, t.j), A(t.i, t.j)}; wr = {A(t.k, t.j), W(t.i, t.j)}; break;
+    // split ApplyTrap (dynamic scheduler): 4 = A1 (w), 6 = A2 (R_kj), 5 = B (A_ij)
+    case 4: rd = {U(t.i, t.k), A(t.k, t.j), A(t.i, t.j)}; wr = {W(t.i, t.j)}; break;
+    case 6: rd = {W(t.i, t.j), A(t.k, t.j)}; wr = {A(t.k, t.j)}; break;
     case 5: rd = {U(t.i, t.k), W(t.i, t.j), A(t.i, t.j)}; wr = {A(t.i, t.j)}; break;
     default: rd = {U(t.i, t.k), A(t.k, t.j), A(t.i, t.j)}; wr = {A(t.k, t.j), A(t.i, t.j)}; break;
   }
@@ -863,8 +867,9 @@ static void tiled_dag_host(int p, int q, std::vector<blrqr_task>& tasks, std::ve
     for (int i = k + 1; i < p; ++i) {
       tasks.push_back({2, k, i, -1});
       for (int j = k + 1; j < q; ++j) {
-        tasks.push_back({4, k, i, j});  // split ApplyTrap: top half
-        tasks.push_back({5, k, i, j});  //                   bottom half
+        tasks.push_back({4, k, i, j});  // split ApplyTrap: w
+        tasks.push_back({6, k, i, j});  //                   R_kj -= w
+        tasks.push_back({5, k, i, j});  //                   A_ij -= Ytilde w
       }
     }
   }
@@ -963,7 +968,7 @@ int blrqr_tiled_dag(int p, int q, blrqr_task* tasks_host, int* indeg_host, int64
   // by bottom level (longest remaining chain first, DAG_RINGS classes)
   for (int t = 0; t < n; ++t) {
     const int slack = cp - top[t] - bot[t];
-    const bool hi = tasks[t].kind == 0 || tasks[t].kind == 2 || (tasks[t].kind == 4 && tasks[t].j == tasks[t].k + 1);
+    const bool hi = tasks[t].kind == 0 || tasks[t].kind == 2 || ((tasks[t].kind == 4 || tasks[t].kind == 6) && tasks[t].j == tasks[t].k + 1);
     int ring;
     if (g_dag_rings == 2) ring = hi ? 0 : 1;
     else ring = std::min(DAG_RINGS - 1, (cp - bot[t]) * DAG_RINGS / (cp + 1));

@@ -131,17 +131,35 @@ __device__ __forceinline__ void jac_dots(const double* gp, const double* gq, int
     g = fma(x, y, g);
   }
 }
-__device__ __forceinline__ bool jac_angle(double a, double b, double g, double tol2, double& c, double& s) {
+__device__ __forceinline__ bool jac_angle_t(double a, double b, double g, double tol2, double& c, double& s,
+                                            double& t) {
   if (g == 0.0 || a == 0.0 || b == 0.0) return false;
   if (g * g <= tol2 * a * b) return false;
   // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (b - a) / (2g), written
   // with one sqrt and one division: t = 2g / (d + sign(d) sqrt(d^2 + 4g^2))
   const double d = b - a;
   const double h = sqrt(fma(d, d, 4.0 * g * g));
-  const double t = (2.0 * g) / (d + copysign(h, d));
+  t = (2.0 * g) / (d + copysign(h, d));
   c = rsqrt(fma(t, t, 1.0));
   s = c * t;
   return true;
+}
+__device__ __forceinline__ bool jac_angle(double a, double b, double g, double tol2, double& c, double& s) {
+  double t;
+  return jac_angle_t(a, b, g, tol2, c, s, t);
+}
+// Hestenes norm update after the rotation that annihilates g: a' = a - t g,
+// b' = b + t g exactly in exact arithmetic.  Returns false when either update
+// cancels (new value < a quarter of the old), so the caller recomputes.
+constexpr int JAC_SMEM_MAXC = 160;  // jacobi_smem column limit (tracked-norm slots)
+
+__device__ __forceinline__ bool jac_norm_update(double& a, double& b, double t, double g) {
+  const double tg = t * g;
+  const double a2 = a - tg, b2 = b + tg;
+  const bool ok = a2 >= 0.25 * a && b2 >= 0.25 * b;
+  a = a2;
+  b = b2;
+  return ok;
 }
 __device__ __forceinline__ void jac_rotate(double* xp, double* xq, int n, int lane, double c, double s) {
 #pragma unroll 4
@@ -162,46 +180,74 @@ __device__ __forceinline__ void rr_pair(int pi, int rnd, int kk, int& p, int& q)
 }
 
 // One warp, one column pair (p, q) of a staged block: the pair's X columns
-// stay in registers between the inner products and the rotation (RPL rows
-// per lane, rows <= 32*RPL); J's columns are rotated in place.  Same
-// arithmetic as jac_dots / jac_angle / jac_rotate.
+// stay in registers between the inner product and the rotation (RPL rows
+// per lane, rows <= 32*RPL); J's columns are rotated in place.  The squared
+// column norms are tracked (na, nb: shared-memory slots of p and q; Hestenes
+// update, exact recompute on cancellation), so only g = x_p . x_q is reduced
+// per pair.
 template <int RPL>
 __device__ __forceinline__ bool jac_pair_reg(double* xp, double* xq, int rows, double* jp, double* jq, int nj, int lane,
-                                             double tol2) {
+                                             double tol2, double* na, double* nb) {
   double xr[RPL], yr[RPL];
-  double a = 0.0, b = 0.0, g = 0.0;
+  double g = 0.0;
 #pragma unroll
   for (int r = 0; r < RPL; ++r) {
     const int i = lane + 32 * r;
     xr[r] = i < rows ? xp[i] : 0.0;
     yr[r] = i < rows ? xq[i] : 0.0;
   }
+  double a = *na, b = *nb;
+#pragma unroll
+  for (int r = 0; r < RPL; ++r) g = fma(xr[r], yr[r], g);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
+  double c, s, t;
+  if (!jac_angle_t(a, b, g, tol2, c, s, t)) return false;
 #pragma unroll
   for (int r = 0; r < RPL; ++r) {
-    if (lane + 32 * r < rows) {
-      a = fma(xr[r], xr[r], a);
-      b = fma(yr[r], yr[r], b);
-      g = fma(xr[r], yr[r], g);
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    a += __shfl_xor_sync(0xffffffffu, a, o);
-    b += __shfl_xor_sync(0xffffffffu, b, o);
-    g += __shfl_xor_sync(0xffffffffu, g, o);
-  }
-  double c, s;
-  if (!jac_angle(a, b, g, tol2, c, s)) return false;
-#pragma unroll
-  for (int r = 0; r < RPL; ++r) {
+    const double x = c * xr[r] - s * yr[r];
+    const double y = s * xr[r] + c * yr[r];
+    xr[r] = x;
+    yr[r] = y;
     const int i = lane + 32 * r;
     if (i < rows) {
-      xp[i] = c * xr[r] - s * yr[r];
-      xq[i] = s * xr[r] + c * yr[r];
+      xp[i] = x;
+      xq[i] = y;
     }
+  }
+  if (!jac_norm_update(a, b, t, g)) {  // warp-uniform: a, b, g, t agree in every lane
+    a = 0.0;
+    b = 0.0;
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      a = fma(xr[r], xr[r], a);
+      b = fma(yr[r], yr[r], b);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+  }
+  if (lane == 0) {
+    *na = a;
+    *nb = b;
   }
   jac_rotate(jp, jq, nj, lane, c, s);
   return true;
+}
+
+// squared norms of the nc staged columns (ld rows) into nrm
+__device__ __forceinline__ void stage_norms(const double* Xs, int rows, int nc, double* nrm) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int c = warp; c < nc; c += NWARP) {
+    const double* x = Xs + c * rows;
+    double a = 0.0;
+    for (int i = lane; i < rows; i += 32) a = fma(x[i], x[i], a);
+    a = warp_sum(a);
+    if (lane == 0) nrm[c] = a;
+  }
+  __syncthreads();
 }
 
 // Full cyclic sweep over the nc staged columns of one block pair (Xs rows x
@@ -210,9 +256,10 @@ __device__ __forceinline__ bool jac_pair_reg(double* xp, double* xq, int rows, d
 template <int RPL>
 __device__ bool block_pair_sweep_t(double* Xs, int rows, double* Js, int nj, int nc, double tol2) {
   __shared__ int s_any;
+  __shared__ double s_nrm[64];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) s_any = 0;
-  __syncthreads();
+  stage_norms(Xs, rows, nc, s_nrm);
   const int kk = (nc + 1) & ~1;
   bool rot = false;
   for (int r2 = 0; r2 < kk - 1; ++r2) {
@@ -220,7 +267,8 @@ __device__ bool block_pair_sweep_t(double* Xs, int rows, double* Js, int nj, int
       int p, q;
       rr_pair(pi, r2, kk, p, q);
       if (q >= nc) continue;
-      rot |= jac_pair_reg<RPL>(Xs + p * rows, Xs + q * rows, rows, Js + p * nj, Js + q * nj, nj, lane, tol2);
+      rot |= jac_pair_reg<RPL>(Xs + p * rows, Xs + q * rows, rows, Js + p * nj, Js + q * nj, nj, lane, tol2,
+                               s_nrm + p, s_nrm + q);
     }
     __syncthreads();
   }
@@ -274,13 +322,14 @@ __device__ __forceinline__ bool block_pair_sweep(double* Xs, int rows, double* J
   return block_pair_sweep_off((int)(Xs - dyn_smem), rows, (int)(Js - dyn_smem), nj, nc, tol2);
 }
 
-// Shared-memory one-sided Jacobi: X (rows x ncols, ld rows) and J (ncols x
+// Shared-memory one-sided Jacobi (ncols <= JAC_SMEM_MAXC): X (rows x ncols, ld rows) and J (ncols x
 // ncols) live in the CTA's shared arena (xs, js were returned by salloc).
 // Each warp works on two column pairs at once to overlap the dependent
 // reduction / sqrt / division latency.
 __device__ __noinline__ void jacobi_smem(const Ctx& cx, int rows, int ncols, double* xs_, double* js_, double* sigma,
                                          int* perm, unsigned long long* prof = nullptr) {
   __shared__ int s_rot;
+  __shared__ double s_jn[JAC_SMEM_MAXC];  // tracked squared column norms
   double* X = as_smem(cx, xs_);
   double* J = as_smem(cx, js_);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -293,7 +342,7 @@ __device__ __noinline__ void jacobi_smem(const Ctx& cx, int rows, int ncols, dou
   const int npairs = kk / 2;
   for (int sweep = 0; sweep < 40 && ncols > 1; ++sweep) {
     if (threadIdx.x == 0) s_rot = 0;
-    __syncthreads();
+    stage_norms(X, rows, ncols, s_jn);  // fresh norms every sweep (bounded drift)
     for (int rnd = 0; rnd < kk - 1; ++rnd) {
       for (int pi = warp; pi < npairs; pi += 2 * NWARP) {
         const int pi2 = pi + NWARP;
@@ -305,28 +354,54 @@ __device__ __noinline__ void jacobi_smem(const Ctx& cx, int rows, int ncols, dou
           rr_pair(pi2, rnd, kk, p1, q1);
           v1 = p1 < ncols && q1 < ncols;
         }
-        double a0 = 0, b0 = 0, g0 = 0, a1 = 0, b1 = 0, g1 = 0;
-        if (v0) jac_dots(X + p0 * rows, X + q0 * rows, rows, lane, a0, b0, g0);
-        if (v1) jac_dots(X + p1 * rows, X + q1 * rows, rows, lane, a1, b1, g1);
+        double g0 = 0, g1 = 0;
+        if (v0) {
+          const double* xp = X + p0 * rows;
+          const double* xq = X + q0 * rows;
+#pragma unroll 4
+          for (int i = lane; i < rows; i += 32) g0 = fma(xp[i], xq[i], g0);
+        }
+        if (v1) {
+          const double* xp = X + p1 * rows;
+          const double* xq = X + q1 * rows;
+#pragma unroll 4
+          for (int i = lane; i < rows; i += 32) g1 = fma(xp[i], xq[i], g1);
+        }
+        const double a0 = v0 ? s_jn[p0] : 0.0, b0 = v0 ? s_jn[q0] : 0.0;
+        const double a1 = v1 ? s_jn[p1] : 0.0, b1 = v1 ? s_jn[q1] : 0.0;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-          a0 += __shfl_xor_sync(0xffffffffu, a0, o);
-          b0 += __shfl_xor_sync(0xffffffffu, b0, o);
           g0 += __shfl_xor_sync(0xffffffffu, g0, o);
-          a1 += __shfl_xor_sync(0xffffffffu, a1, o);
-          b1 += __shfl_xor_sync(0xffffffffu, b1, o);
           g1 += __shfl_xor_sync(0xffffffffu, g1, o);
         }
-        double c0, s0, c1, s1;
-        const bool r0 = v0 && jac_angle(a0, b0, g0, tol2, c0, s0);
-        const bool r1 = v1 && jac_angle(a1, b1, g1, tol2, c1, s1);
+        double c0, s0, t0, c1, s1, t1;
+        const bool r0 = v0 && jac_angle_t(a0, b0, g0, tol2, c0, s0, t0);
+        const bool r1 = v1 && jac_angle_t(a1, b1, g1, tol2, c1, s1, t1);
         if (r0) {
           jac_rotate(X + p0 * rows, X + q0 * rows, rows, lane, c0, s0);
           jac_rotate(J + p0 * ncols, J + q0 * ncols, ncols, lane, c0, s0);
+          double a = a0, b = b0;
+          if (!jac_norm_update(a, b, t0, g0)) {
+            double gg;
+            __syncwarp();
+            jac_dots(X + p0 * rows, X + q0 * rows, rows, lane, a, b, gg);
+            a = warp_sum(a);
+            b = warp_sum(b);
+          }
+          if (lane == 0) { s_jn[p0] = a; s_jn[q0] = b; }
         }
         if (r1) {
           jac_rotate(X + p1 * rows, X + q1 * rows, rows, lane, c1, s1);
           jac_rotate(J + p1 * ncols, J + q1 * ncols, ncols, lane, c1, s1);
+          double a = a1, b = b1;
+          if (!jac_norm_update(a, b, t1, g1)) {
+            double gg;
+            __syncwarp();
+            jac_dots(X + p1 * rows, X + q1 * rows, rows, lane, a, b, gg);
+            a = warp_sum(a);
+            b = warp_sum(b);
+          }
+          if (lane == 0) { s_jn[p1] = a; s_jn[q1] = b; }
         }
         if ((r0 || r1) && lane == 0) s_rot = 1;
       }

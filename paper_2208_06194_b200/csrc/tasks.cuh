@@ -209,11 +209,19 @@ __device__ void tiled_trap(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, d
   tiled_trap_op(cx, g, rf, g, eps, k, i, j, true);
 }
 
-// Split ApplyTrapReflector for the dynamic scheduler: the top half computes
-// w and updates R_kj (the serial chain over i), the bottom half updates A_ij
-// from the stored w and can overlap the next link of the chain.  Same
-// operations as tiled_trap, so results are bitwise identical.
-__device__ void tiled_trap_a(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, double eps, int k, int i, int j) {
+// Split ApplyTrapReflector for the dynamic scheduler, three tasks with the
+// operations of tiled_trap (results bitwise identical):
+//  A1: prod = Ytilde^T A_ij, ssum = R_kj + prod, w = T^T ssum -> w slot (i, j)
+//  A2: R_kj -= w            (the serial R_kj chain over i)
+//  B:  A_ij -= Ytilde w     (can overlap A2 and the next link of the chain)
+// so the path into the next panel column leaves the R_kj chain after A1.
+// w slot of ApplyTrap (k, i, j): two per cell, by the parity of k, so
+// A1(k+1, i, j) does not wait for A2 / B of (k, i, j) to release the slot
+__device__ __forceinline__ long long w_index(const blrqr_grid& g, int k, int i, int j) {
+  return (long long)(k & 1) * g.p * g.q + (long long)i * g.q + j;
+}
+
+__device__ void tiled_trap_a1(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, double eps, int k, int i, int j) {
   const long long mark = cx.top;
   const int b = g.b;
   const Blk yt = refl_blk(g, rf, i, k);
@@ -227,7 +235,7 @@ __device__ void tiled_trap_a(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf,
   PhaseTimer t2;
   Blk w = blk_dense_times(cx, T, b, true, ssum);
   t2.stop(cx, PH_PRODUCT);
-  const long long cw = (long long)i * g.q + j;
+  const long long cw = w_index(g, k, i, j);
   double* wu = rf.wpool + cw * rf.wslot;
   double* wv = wu + rf.wslot / 2;
   if (w.lr) {
@@ -242,18 +250,27 @@ __device__ void tiled_trap_a(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf,
   }
   if (w.s != 1.0) set_status(cx, ST_BAD_ARG);  // w inherits ssum's unit scale
   __syncthreads();
-  sub_into_cell(cx, top, w, eps);
+  cx.top = mark;
+}
+
+__device__ __forceinline__ Blk w_slot(const blrqr_grid& g, const blrqr_refl& rf, int k, int i, int j) {
+  const int b = g.b;
+  const long long cw = w_index(g, k, i, j);
+  double* wu = rf.wpool + cw * rf.wslot;
+  const int wr = rf.wrank[cw];
+  return wr >= 0 ? make_lr(b, b, wr, wu, b, wu + rf.wslot / 2, b, 1.0) : make_dense(b, b, wu, b, 1.0);
+}
+
+__device__ void tiled_trap_a2(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, double eps, int k, int i, int j) {
+  const long long mark = cx.top;
+  sub_into_cell(cx, grid_cell(g, k, j), w_slot(g, rf, k, i, j), eps);
   cx.top = mark;
 }
 
 __device__ void tiled_trap_b(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, double eps, int k, int i, int j) {
   const long long mark = cx.top;
-  const int b = g.b;
   const Blk yt = refl_blk(g, rf, i, k);
-  const long long cw = (long long)i * g.q + j;
-  double* wu = rf.wpool + cw * rf.wslot;
-  const int wr = rf.wrank[cw];
-  const Blk w = wr >= 0 ? make_lr(b, b, wr, wu, b, wu + rf.wslot / 2, b, 1.0) : make_dense(b, b, wu, b, 1.0);
+  const Blk w = w_slot(g, rf, k, i, j);
   PhaseTimer t3;
   Blk yw = blk_mul(cx, yt, w);
   t3.stop(cx, PH_PRODUCT);

@@ -234,12 +234,13 @@ class DeviceRefl:
 
     def enable_split_traps(self) -> None:
         """Allocate the per-cell w slots used by the split ApplyTrap tasks of
-        the dynamic scheduler (2*b*cap doubles per cell)."""
+        the dynamic scheduler (2 slots of 2*b*cap doubles per cell)."""
         if self.wpool is None:
             g = self.grid
             self.wslot = 2 * g.b * g.cap
-            self.wpool = torch.empty(g.p * g.q * self.wslot, dtype=torch.float64, device=g.pool.device)
-            self.wrank = torch.zeros(g.p * g.q, dtype=torch.int32, device=g.pool.device)
+            # two slots per cell, by the parity of k (tasks.cuh w_index)
+            self.wpool = torch.empty(2 * g.p * g.q * self.wslot, dtype=torch.float64, device=g.pool.device)
+            self.wrank = torch.zeros(2 * g.p * g.q, dtype=torch.int32, device=g.pool.device)
 
     def cstruct(self) -> _lib.Refl:
         return _lib.Refl(self.pool.data_ptr(), self.y_off.data_ptr(), self.t_off.data_ptr(),

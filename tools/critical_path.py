@@ -52,7 +52,7 @@ while t >= 0:
     path.append(t)
     t = pred[t]
 path = path[::-1]
-kinds = ["diag", "block", "update", "trap", "trapA", "trapB"]
+kinds = ["diag", "block", "update", "trap", "trapA1", "trapB", "trapA2"]
 kind_time = {k: float(dur[tasks[:, 0] == i].sum()) for i, k in enumerate(kinds)}
 path_kinds = {k: 0.0 for k in kinds}
 for t in path:
@@ -72,3 +72,7 @@ print(json.dumps({"wall_s": wall, "makespan_s": (en.max() - t0g) / 1e9, "sum_tas
                                 for t in np.argsort(-dur)[:15]],
                   "path_sample": [[kinds[tasks[t, 0]], int(tasks[t, 1]), int(tasks[t, 2]), int(tasks[t, 3]), round(float(dur[t]), 4)]
                                   for t in path[::max(1, len(path) // 25)]]}, indent=1))
+if len(sys.argv) > 2:  # full path, one task per line: kind k i j seconds
+    with open(sys.argv[2], "w") as fh:
+        for t in path:
+            fh.write(f"{kinds[tasks[t, 0]]} {int(tasks[t, 1])} {int(tasks[t, 2])} {int(tasks[t, 3])} {dur[t]:.5f}\n")
