@@ -196,6 +196,11 @@ void blrqr_set_dag_rings(int policy);
  * is <= (tol * eps_mach) * ||core||_F (tol >= 1; default 1 = rounding level).
  * Returns 0, or -1 for tol out of range. */
 int blrqr_set_qrcp_tol(double tol);
+/* Dynamic scheduler: the last `nctas` CTAs of blrqr_tiled_run_dag (capped at a
+ * quarter of the grid) take no tasks and only join the team jobs of
+ * critical-chain tasks (DiagQR, UpdateQR, the column-(k+1) ApplyTraps).
+ * Results do not depend on it.  Default 16; 0 disables. */
+void blrqr_set_team_reserve(int nctas);
 /* Debug: one-sided Jacobi of X (rows x ncols, column-major, ld rows) with J
  * (ncols x ncols) -- mode 0 single-CTA blocked, 1 single-CTA column pairs,
  * 2 CTA team over nctas CTAs.  sigma (ncols), perm (ncols) outputs. */

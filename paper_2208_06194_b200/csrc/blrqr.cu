@@ -403,6 +403,7 @@ struct DagDev {
   int* ctr;  // [2c] head / [2c+1] tail of ring c, [2*DAG_RINGS] done
   long long* trace;  // optional: per task (start ns, end ns, sm id)
   TeamCtx* team;     // optional: CTA teams for large Jacobi cores (team.cuh)
+  int reserve;       // the last `reserve` CTAs only help priority team jobs
   unsigned long long* ptrace;  // optional: per task PH_COUNT phase cycle counters
 };
 
@@ -425,24 +426,25 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM) k_tiled_dag(DagDev d, blrqr_g
                                                      long long timeout_cycles) {
   Ctx cx = make_ctx(ws, wsp, status, flops);
   cx.team = d.team;
+  const bool reserved = d.team && (int)blockIdx.x >= (int)gridDim.x - d.reserve;
   __shared__ int s_task, s_member;
   while (true) {
     if (threadIdx.x == 0) {
       int t = -1;
       const long long t0 = sm_clock();
-      if (d.team) atomicAdd(d.team->tk + 2, 1);  // polling
+      if (d.team) team_polling(d.team, 1, reserved);
       while (true) {
         bool got = false;
         if (d.team) {  // help a running team job first: it is on the critical path
           int member;
-          const int slot = team_try_join(d.team, &member);
+          const int slot = team_try_join(d.team, &member, reserved);
           if (slot >= 0) {
             t = -2 - slot;
             s_member = member;
             break;
           }
         }
-        for (int c = 0; c < DAG_RINGS && !got; ++c) {
+        for (int c = 0; c < DAG_RINGS && !got && !reserved; ++c) {
           const int h = ld_volatile(d.ctr + 2 * c);
           const int tl = ld_volatile(d.ctr + 2 * c + 1);
           if (h < tl && atomicCAS(d.ctr + 2 * c, h, h + 1) == h) {
@@ -461,7 +463,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM) k_tiled_dag(DagDev d, blrqr_g
         }
         __nanosleep(64);
       }
-      if (d.team) atomicSub(d.team->tk + 2, 1);
+      if (d.team) team_polling(d.team, -1, reserved);
       __threadfence();
       s_task = t;
     }
@@ -478,6 +480,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM) k_tiled_dag(DagDev d, blrqr_g
     }
     const blrqr_task tk = d.tasks[t];
     cx.team = (d.prio[t] & 2) ? d.team : nullptr;  // only near-critical tasks recruit helpers
+    cx.team_hi = d.prio[t] & 1;                    // critical chains use the priority ring
     if (d.trace && threadIdx.x == 0) d.trace[3 * (long long)t] = global_ns();
     cx.tph = d.ptrace ? d.ptrace + 16LL * t : nullptr;
     PhaseTimer tt;
@@ -597,6 +600,7 @@ static void init_kernels() {
 #define INIT_KERNELS() init_kernels()
 
 static int g_teams_enabled = 1;
+static int g_team_reserve = 16;  // dynamic scheduler: CTAs that only help critical-chain team jobs
 static int g_dag_rings = DAG_RINGS;  // 2: the kind-based two-ring policy
 static int g_team_slack = 1 << 20;  // DAG tasks with unit-weight slack <= this may form teams (all by default: measured best)
 
@@ -614,22 +618,24 @@ static int team_for_launch(cudaStream_t st, TeamCtx** team, int** ctr) {
   int dev = 0;
   cudaGetDevice(&dev);
   const size_t jobs_b = sizeof(TeamJob) * TEAM_JOBS, tick_b = sizeof(int) * (size_t)TEAM_TICKETS;
+  // layout: [256 B header] jobs | tickets | tickets_hi | tk (256 B)
   Buf* b;
   {
     std::lock_guard<std::mutex> lk(mu);
     b = &bufs[{dev, st}];
     if (!b->p) {
-      CK(cudaMalloc(&b->p, 256 + jobs_b + tick_b + 256));
+      CK(cudaMalloc(&b->p, 256 + jobs_b + 2 * tick_b + 256));
       b->h.jobs = reinterpret_cast<TeamJob*>(b->p + 256);
       b->h.tickets = reinterpret_cast<int*>(b->p + 256 + jobs_b);
-      b->h.tk = reinterpret_cast<int*>(b->p + 256 + jobs_b + tick_b);
+      b->h.tickets_hi = reinterpret_cast<int*>(b->p + 256 + jobs_b + tick_b);
+      b->h.tk = reinterpret_cast<int*>(b->p + 256 + jobs_b + 2 * tick_b);
       b->h.tk_cap = TEAM_TICKETS;
       CK(cudaMemcpy(b->p, &b->h, sizeof(TeamCtx), cudaMemcpyHostToDevice));
     }
   }
   if (g_teams_enabled) {
     CK(cudaMemsetAsync(b->h.jobs, 0, jobs_b, st));
-    CK(cudaMemsetAsync(b->h.tickets, 0xFF, tick_b, st));
+    CK(cudaMemsetAsync(b->h.tickets, 0xFF, 2 * tick_b, st));
   }
   CK(cudaMemsetAsync(b->h.tk, 0, 256, st));  // ring head/tail + task counters
   if (ctr) *ctr = b->h.tk + 16;
@@ -924,6 +930,7 @@ void blrqr_set_teams(int enable) {
   if (enable > 1) g_team_slack = enable - 2;  // tuning: enable = 2 + max slack (1 << 20: every task)
 }
 void blrqr_set_dag_rings(int policy) { g_dag_rings = policy == 2 ? 2 : DAG_RINGS; }
+void blrqr_set_team_reserve(int nctas) { g_team_reserve = std::max(0, nctas); }
 int blrqr_set_qrcp_tol(double tol) {
   if (!(tol >= 1.0 && tol < 1e8)) return -1;
   CK(cudaMemcpyToSymbol(g_qrcp_tol, &tol, sizeof(double)));
@@ -968,7 +975,7 @@ int blrqr_tiled_dag(int p, int q, blrqr_task* tasks_host, int* indeg_host, int64
   // by bottom level (longest remaining chain first, DAG_RINGS classes)
   for (int t = 0; t < n; ++t) {
     const int slack = cp - top[t] - bot[t];
-    const bool hi = tasks[t].kind == 0 || tasks[t].kind == 2 || ((tasks[t].kind == 4 || tasks[t].kind == 6) && tasks[t].j == tasks[t].k + 1);
+    const bool hi = tasks[t].kind == 0 || tasks[t].kind == 2 || (tasks[t].kind >= 4 && tasks[t].j == tasks[t].k + 1);
     int ring;
     if (g_dag_rings == 2) ring = hi ? 0 : 1;
     else ring = std::min(DAG_RINGS - 1, (cp - bot[t]) * DAG_RINGS / (cp + 1));
@@ -999,6 +1006,7 @@ int blrqr_tiled_run_dag(const blrqr_grid* g, const blrqr_refl* rf, int ntasks, c
   int dev = 0, clk_khz = 1965000;
   cudaGetDevice(&dev);
   if (int e = team_for_launch(st, &d.team, nullptr)) return e;
+  d.reserve = d.team ? std::min(g_team_reserve, nctas / 4) : 0;
   CK(cudaMemcpyAsync(d.indeg, indeg0_dev, sizeof(int) * ntasks, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemsetAsync(d.q[0], 0xFF, sizeof(int) * DAG_RINGS * (size_t)ntasks, st));
   CK(cudaMemsetAsync(d.ctr, 0, sizeof(int) * (2 * DAG_RINGS + 1), st));

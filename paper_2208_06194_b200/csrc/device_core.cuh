@@ -50,6 +50,7 @@ struct Ctx {
   int* status;             // global status word
   unsigned long long* flops;  // FK_COUNT counters (global)
   TeamCtx* team;           // CTA teams (dynamic scheduler only), else nullptr
+  int team_hi;             // this task is on a critical chain: post team jobs to the priority ring
   unsigned long long* tph;  // debug: this task's PH_COUNT phase cycle row, else nullptr
 };
 

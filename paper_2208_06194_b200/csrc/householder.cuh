@@ -470,88 +470,90 @@ __device__ __noinline__ void tpqrt(Ctx& cx, int n, int k, double* R, int ldr, do
 // O(n^3) forward recurrence.  Same reflectors as LAPACK dtpqrt (l = 0).
 // B is read / written transposed: element (a, l) at Bt[l + a*ldbt].
 // ---------------------------------------------------------------------------
-template <int KM>
+template <int KM, int CPT = 2>
 __device__ __noinline__ void tpqrt_small(Ctx& cx, int n, int k, double* R, int ldr, double* Bt, int ldbt, double* T,
                                          int ldt) {
+  // CPT columns per thread (n <= CPT * NT); CPT = 1 halves the register
+  // state so KM = 32 stays spill-free
+  static_assert(CPT == 1 || CPT == 2, "columns per thread");
   __shared__ double s_v[2][KM];
   __shared__ double s_tau[2];
   const Mark mk = mark(cx);
   double* taus = alloc_fast(cx, n);
   if (!taus) return;
-  const int l0 = threadIdx.x, l1 = threadIdx.x + NT;
-  double b0[KM], b1[KM];
+  double bb[CPT][KM];
+  int ll[CPT];
 #pragma unroll
-  for (int a = 0; a < KM; ++a) {
-    b0[a] = (a < k && l0 < n) ? Bt[l0 + (long long)a * ldbt] : 0.0;
-    b1[a] = (a < k && l1 < n) ? Bt[l1 + (long long)a * ldbt] : 0.0;
+  for (int c = 0; c < CPT; ++c) {
+    ll[c] = threadIdx.x + c * NT;
+#pragma unroll
+    for (int a = 0; a < KM; ++a) bb[c][a] = (a < k && ll[c] < n) ? Bt[ll[c] + (long long)a * ldbt] : 0.0;
   }
+  // R(j, l) of the next step, prefetched one step ahead (step j writes row j only)
+  double rn[CPT];
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) rn[c] = ll[c] < n ? R[(long long)ll[c] * ldr] : 0.0;
   for (int j = 0; j < n; ++j) {
     const int buf = j & 1;
-    if (threadIdx.x == (j % NT)) {
-      const bool hi = j >= NT;
-      double xn2 = 0.0;
+    double rcur[CPT];
 #pragma unroll
-      for (int a = 0; a < KM; ++a) {
-        const double x = hi ? b1[a] : b0[a];
-        xn2 = fma(x, x, xn2);
-      }
-      double* rjj = R + j + (long long)j * ldr;
-      const double alpha = *rjj;
-      double tau = 0.0, beta = alpha;
-      if (xn2 != 0.0) {
-        const double mu = sqrt(alpha * alpha + xn2);
-        beta = alpha >= 0.0 ? -mu : mu;
-        tau = (beta - alpha) / beta;
-        const double scal = 1.0 / (alpha - beta);
+    for (int c = 0; c < CPT; ++c) {
+      rcur[c] = rn[c];
+      if (j + 1 < n && ll[c] < n && ll[c] > j) rn[c] = R[j + 1 + (long long)ll[c] * ldr];
+    }
 #pragma unroll
-        for (int a = 0; a < KM; ++a) {
-          if (hi) b1[a] *= scal;
-          else b0[a] *= scal;
+    for (int c = 0; c < CPT; ++c) {
+      if (ll[c] == j) {  // owner of column j: reflector
+        double xn2 = 0.0;
+#pragma unroll
+        for (int a = 0; a < KM; ++a) xn2 = fma(bb[c][a], bb[c][a], xn2);
+        double* rjj = R + j + (long long)j * ldr;
+        const double alpha = rcur[c];
+        double tau = 0.0, beta = alpha;
+        if (xn2 != 0.0) {
+          const double mu = sqrt(alpha * alpha + xn2);
+          beta = alpha >= 0.0 ? -mu : mu;
+          tau = (beta - alpha) / beta;
+          const double scal = 1.0 / (alpha - beta);
+#pragma unroll
+          for (int a = 0; a < KM; ++a) bb[c][a] *= scal;
         }
-      }
 #pragma unroll
-      for (int a = 0; a < KM; ++a) s_v[buf][a] = hi ? b1[a] : b0[a];
-      s_tau[buf] = tau;
-      taus[j] = tau;
-      *rjj = beta;
+        for (int a = 0; a < KM; ++a) s_v[buf][a] = bb[c][a];
+        s_tau[buf] = tau;
+        taus[j] = tau;
+        *rjj = beta;
+      }
     }
     __syncthreads();
     const double tau = s_tau[buf];
     if (tau != 0.0) {
-      if (l0 < n && l0 > j) {
-        double* r = R + j + (long long)l0 * ldr;
-        double d = *r;
 #pragma unroll
-        for (int a = 0; a < KM; ++a) d = fma(s_v[buf][a], b0[a], d);
-        d *= tau;
-        *r -= d;
+      for (int c = 0; c < CPT; ++c) {
+        if (ll[c] < n && ll[c] > j) {
+          double d = rcur[c];
 #pragma unroll
-        for (int a = 0; a < KM; ++a) b0[a] = fma(-d, s_v[buf][a], b0[a]);
-      }
-      if (l1 < n && l1 > j) {
-        double* r = R + j + (long long)l1 * ldr;
-        double d = *r;
+          for (int a = 0; a < KM; ++a) d = fma(s_v[buf][a], bb[c][a], d);
+          d *= tau;
+          R[j + (long long)ll[c] * ldr] = rcur[c] - d;
 #pragma unroll
-        for (int a = 0; a < KM; ++a) d = fma(s_v[buf][a], b1[a], d);
-        d *= tau;
-        *r -= d;
-#pragma unroll
-        for (int a = 0; a < KM; ++a) b1[a] = fma(-d, s_v[buf][a], b1[a]);
+          for (int a = 0; a < KM; ++a) bb[c][a] = fma(-d, s_v[buf][a], bb[c][a]);
+        }
       }
     }
   }
 #pragma unroll
-  for (int a = 0; a < KM; ++a) {
-    if (a < k && l0 < n) Bt[l0 + (long long)a * ldbt] = b0[a];
-    if (a < k && l1 < n) Bt[l1 + (long long)a * ldbt] = b1[a];
-  }
+  for (int c = 0; c < CPT; ++c)
+#pragma unroll
+    for (int a = 0; a < KM; ++a)
+      if (a < k && ll[c] < n) Bt[ll[c] + (long long)a * ldbt] = bb[c][a];
   __syncthreads();
   // Y (k x n) for the T build: shared memory when it fits
   double* Ys = salloc(cx, (long long)KM * n);
   if (Ys) {
     for (int l = threadIdx.x; l < n; l += NT)
 #pragma unroll
-      for (int a = 0; a < KM; ++a) Ys[a + KM * l] = a < k ? Bt[l + (long long)a * ldbt] : 0.0;
+      for (int a = 0; a < KM; ++a) Ys[l + n * a] = a < k ? Bt[l + (long long)a * ldbt] : 0.0;
     __syncthreads();
   }
   for (int i = threadIdx.x; i < n; i += NT) {
@@ -561,18 +563,18 @@ __device__ __noinline__ void tpqrt_small(Ctx& cx, int n, int k, double* R, int l
     T[i + (long long)i * ldt] = ti;
 #pragma unroll
     for (int a = 0; a < KM; ++a)
-      z[a] = ti * (Ys ? Ys[a + KM * i] : (a < k ? Bt[i + (long long)a * ldbt] : 0.0));
+      z[a] = ti * (Ys ? Ys[i + n * a] : (a < k ? Bt[i + (long long)a * ldbt] : 0.0));
     for (int j = i + 1; j < n; ++j) {
-      double y[KM];
-#pragma unroll
-      for (int a = 0; a < KM; ++a) y[a] = Ys ? Ys[a + KM * j] : (a < k ? Bt[j + (long long)a * ldbt] : 0.0);
+      // y_j read twice (dot, then update) so only z stays live in registers
       double dot = 0.0;
 #pragma unroll
-      for (int a = 0; a < KM; ++a) dot = fma(z[a], y[a], dot);
+      for (int a = 0; a < KM; ++a)
+        dot = fma(z[a], Ys ? Ys[j + n * a] : (a < k ? Bt[j + (long long)a * ldbt] : 0.0), dot);
       const double t = -taus[j] * dot;
       T[i + (long long)j * ldt] = t;
 #pragma unroll
-      for (int a = 0; a < KM; ++a) z[a] = fma(t, y[a], z[a]);
+      for (int a = 0; a < KM; ++a)
+        z[a] = fma(t, Ys ? Ys[j + n * a] : (a < k ? Bt[j + (long long)a * ldbt] : 0.0), z[a]);
     }
   }
   __syncthreads();

@@ -31,6 +31,7 @@ __device__ __forceinline__ Ctx make_ctx(double* ws, long long ws_per_cta, int* s
   c.status = status;
   c.flops = flops;
   c.team = nullptr;
+  c.team_hi = 0;
   c.tph = nullptr;
   return c;
 }
@@ -144,13 +145,16 @@ __device__ void tiled_update(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf,
   PhaseTimer pt;
   if (x.lr) {
     const int r = *x.rank;
+    if (cx.tph && threadIdx.x == 0) cx.tph[15] = (unsigned long long)r;  // debug trace: bottom rows
     if (r == 0) {  // tp_qr with an empty bottom: identity reflector (kernels.py:146-147)
       zero_mat(b, b, T, b);
     } else {
-      if (r <= 16 && b <= 2 * NT) {
-        tpqrt_small<16>(cx, b, r, rk.u, rk.ld, x.v, x.ld, T, b);  // B^T = V in place -> Y^T
-      } else if (r <= 32 && b <= 2 * NT) {
-        tpqrt_small<32>(cx, b, r, rk.u, rk.ld, x.v, x.ld, T, b);
+      if (r <= 16 && b <= NT) {
+        tpqrt_small<16, 1>(cx, b, r, rk.u, rk.ld, x.v, x.ld, T, b);  // B^T = V in place -> Y^T
+      } else if (r <= 16 && b <= 2 * NT) {
+        tpqrt_small<16, 2>(cx, b, r, rk.u, rk.ld, x.v, x.ld, T, b);
+      } else if (r <= 32 && b <= NT) {
+        tpqrt_small<32, 1>(cx, b, r, rk.u, rk.ld, x.v, x.ld, T, b);
       } else {
         double* B = alloc(cx, (long long)r * b);
         double* S = alloc(cx, (long long)b * b);

@@ -64,10 +64,16 @@ struct __align__(128) TeamJob {
   double dv[4];
 };
 
+// Two ticket rings: the priority ring carries the jobs of critical-chain
+// tasks (Ctx::team_hi) and is also served by the dynamic scheduler's
+// reserved helper CTAs, which never take tasks of their own.
 struct TeamCtx {
-  TeamJob* jobs;  // TEAM_JOBS
-  int* tickets;   // ring of slot << 16 | (gen & 0x7fff), -1 = not yet written
-  int* tk;        // [0] head, [1] tail, [2] CTAs currently polling, [16..17] task counters
+  TeamJob* jobs;    // TEAM_JOBS
+  int* tickets;     // normal ring of slot << 16 | (gen & 0x7fff), -1 = not yet written
+  int* tickets_hi;  // priority ring (same encoding)
+  int* tk;  // [0] head, [1] tail, [2] CTAs polling that accept normal jobs,
+            // [3] head_hi, [4] tail_hi, [5] CTAs polling that accept priority jobs,
+            // [16..17] task counters
   int tk_cap;
 };
 
@@ -123,13 +129,16 @@ __device__ int team_launch(Ctx& cx, TeamJob* job, int want) {
     job->rot[0] = job->rot[1] = job->rot[2] = 0;
     job->done = 0;
     // only ask for as many helpers as there are CTAs polling right now
-    want = min(want, 1 + max(0, vload(tc->tk + 2)));
+    const bool hi = cx.team_hi != 0;
+    want = min(want, 1 + max(0, vload(tc->tk + (hi ? 5 : 2))));
     __threadfence();
     atomicExch(&job->join, gen << 16);  // open
     const int ticket = (slot << 16) | gen;
+    int* ring = hi ? tc->tickets_hi : tc->tickets;
+    int* tail = tc->tk + (hi ? 4 : 1);
     for (int h = 1; h < want; ++h) {
-      const int idx = atomicAdd(tc->tk + 1, 1);
-      if (idx < tc->tk_cap) atomicExch(tc->tickets + idx, ticket);
+      const int idx = atomicAdd(tail, 1);
+      if (idx < tc->tk_cap) atomicExch(ring + idx, ticket);
     }
     const long long t0 = sm_clock();
     while (want > 1 && (vload(&job->join) & 0x7fff) < want - 1 && sm_clock() - t0 < TEAM_WAIT_CYCLES)
@@ -471,13 +480,13 @@ __device__ void tpqrt_team(Ctx& cx, int n, int k, double* R, int ldr, double* B,
 // ---- helper side -------------------------------------------------------------
 // thread 0 of an idle CTA: claim a ticket and join its job.
 // Returns the job slot (>= 0) with *member set, or -1.
-__device__ int team_try_join(TeamCtx* tc, int* member) {
-  const int h = vload(tc->tk);
-  const int tl = vload(tc->tk + 1);
+__device__ int team_try_join_ring(TeamCtx* tc, int* tickets, int* head, const int* tail, int* member) {
+  const int h = vload(head);
+  const int tl = vload(tail);
   if (h >= tl || h >= tc->tk_cap) return -1;
-  if (atomicCAS(tc->tk, h, h + 1) != h) return -1;
+  if (atomicCAS(head, h, h + 1) != h) return -1;
   int tk;
-  while ((tk = vload(tc->tickets + h)) < 0) __nanosleep(32);
+  while ((tk = vload(tickets + h)) < 0) __nanosleep(32);
   const int slot = tk >> 16, gen = tk & 0x7fff;
   TeamJob* job = tc->jobs + slot;
   int w = vload(&job->join);
@@ -494,6 +503,19 @@ __device__ int team_try_join(TeamCtx* tc, int* member) {
   return slot;
 }
 
+// priority ring first; the normal ring unless `hi_only` (reserved helpers)
+__device__ int team_try_join(TeamCtx* tc, int* member, bool hi_only = false) {
+  const int s = team_try_join_ring(tc, tc->tickets_hi, tc->tk + 3, tc->tk + 4, member);
+  if (s >= 0 || hi_only) return s;
+  return team_try_join_ring(tc, tc->tickets, tc->tk, tc->tk + 1, member);
+}
+
+// polling registration: ordinary idle CTAs accept both rings
+__device__ __forceinline__ void team_polling(TeamCtx* tc, int delta, bool hi_only = false) {
+  if (!hi_only) atomicAdd(tc->tk + 2, delta);
+  atomicAdd(tc->tk + 5, delta);
+}
+
 __device__ void team_help(Ctx& cx, TeamCtx* tc, int slot, int member);
 
 // Persistent task loop for a flat batch of n independent tasks (batched
@@ -508,7 +530,7 @@ __device__ void team_task_loop(Ctx& cx, long long n, int* ctr, F run) {
   while (true) {
     if (threadIdx.x == 0) {
       long long t = -1;
-      if (cx.team) atomicAdd(cx.team->tk + 2, 1);  // polling
+      if (cx.team) team_polling(cx.team, 1);
       while (true) {
         if (cx.team) {
           int member;
@@ -530,7 +552,7 @@ __device__ void team_task_loop(Ctx& cx, long long n, int* ctr, F run) {
         if (vload(ctr + 1) >= n) break;
         __nanosleep(64);
       }
-      if (cx.team) atomicSub(cx.team->tk + 2, 1);
+      if (cx.team) team_polling(cx.team, -1);
       s_t = t;
     }
     __syncthreads();

@@ -75,4 +75,5 @@ print(json.dumps({"wall_s": wall, "makespan_s": (en.max() - t0g) / 1e9, "sum_tas
 if len(sys.argv) > 2:  # full path, one task per line: kind k i j seconds
     with open(sys.argv[2], "w") as fh:
         for t in path:
-            fh.write(f"{kinds[tasks[t, 0]]} {int(tasks[t, 1])} {int(tasks[t, 2])} {int(tasks[t, 3])} {dur[t]:.5f}\n")
+            extra = f" r={int(ph[t, 15] * 1.965e9)}" if tasks[t, 0] == 2 else ""
+            fh.write(f"{kinds[tasks[t, 0]]} {int(tasks[t, 1])} {int(tasks[t, 2])} {int(tasks[t, 3])} {dur[t]:.5f}{extra}\n")

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--no-teams", action="store_true")
     ap.add_argument("--team-slack", type=int, default=None)
     ap.add_argument("--rings", type=int, default=None)
+    ap.add_argument("--reserve", type=int, default=None, help="reserved team-helper CTAs of the DAG kernel")
     args = ap.parse_args()
     ge.build()
     from paper_2208_06194_b200 import _lib, configs, flops
@@ -41,6 +42,8 @@ def main():
         _lib.runtime().lib.blrqr_set_teams(0)
     elif args.team_slack is not None:
         _lib.runtime().lib.blrqr_set_teams(2 + args.team_slack)
+    if args.reserve is not None:
+        _lib.runtime().lib.blrqr_set_team_reserve(args.reserve)
     if args.rings is not None:
         _lib.runtime().lib.blrqr_set_dag_rings(args.rings)
     cfg = configs.CONFIGS[args.config]
