@@ -433,6 +433,60 @@ __device__ __noinline__ void jacobi_smem(const Ctx& cx, int rows, int ncols, dou
   __syncthreads();
 }
 
+// Deferred-J variant of block_pair_sweep: the pair's rotations are
+// accumulated in a small nc x nc matrix R (shared memory, starts as I; one
+// element per lane per rotation instead of a kp-long J column), and the
+// caller applies J_pair <- J_pair R once per block pair with a GEMM.
+__device__ __noinline__ bool block_pair_sweep_r_off(int xoff, int rows, int roff, int nc, double tol2) {
+  double* Xs = dyn_smem + xoff;
+  double* Rs = dyn_smem + roff;
+  for (int e = threadIdx.x; e < nc * nc; e += NT) Rs[e] = (e % nc == e / nc) ? 1.0 : 0.0;
+  __syncthreads();
+  if (rows <= 64) return block_pair_sweep_t<2>(Xs, rows, Rs, nc, nc, tol2);
+  if (rows <= 128) return block_pair_sweep_t<4>(Xs, rows, Rs, nc, nc, tol2);
+  if (rows <= 256) return block_pair_sweep_t<8>(Xs, rows, Rs, nc, nc, tol2);
+  if (rows <= 384) return block_pair_sweep_t<12>(Xs, rows, Rs, nc, nc, tol2);
+  return block_pair_sweep_t<16>(Xs, rows, Rs, nc, nc, tol2);
+}
+
+// shared-memory doubles one block-pair step needs (X and J staging + R)
+__device__ __forceinline__ long long jac_pair_smem(int jb, int rows, int ncols) {
+  return (long long)2 * jb * (rows + ncols) + 4LL * jb * jb;
+}
+
+// One block pair (bi, bj) of the blocked one-sided Jacobi over X (rows x
+// ncols, ldx) / J (ncols x ncols, ldj) in global memory: stage the pair's X
+// columns, run the inner sweep with deferred rotations, write X back, then
+// J(:, pair) <- J(:, pair) R.  st: jac_pair_smem(jb, ...) doubles of the
+// shared arena.  Returns true (in every thread) if any pair rotated.
+__device__ bool jacobi_block_pair(double* X, int ldx, double* J, int ldj, int rows, int ncols, int jb, int bi, int bj,
+                                  double* st, double tol2) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ni = min(jb, ncols - bi * jb), nj = min(jb, ncols - bj * jb);
+  const int nc = ni + nj;
+  double* Xs = st;
+  double* Js = st + 2 * jb * rows;
+  double* Rs = Js + 2 * jb * ncols;
+  for (int c = warp; c < nc; c += NWARP) {
+    const int gc = c < ni ? bi * jb + c : bj * jb + (c - ni);
+    warp_ld_cg(Xs + c * rows, X + (long long)gc * ldx, rows, lane);
+    warp_ld_cg(Js + c * ncols, J + (long long)gc * ldj, ncols, lane);
+  }
+  __syncthreads();
+  const bool rot = block_pair_sweep_r_off((int)(Xs - dyn_smem), rows, (int)(Rs - dyn_smem), nc, tol2);
+  for (int c = warp; c < nc; c += NWARP) {
+    const int gc = c < ni ? bi * jb + c : bj * jb + (c - ni);
+    warp_st_cg(X + (long long)gc * ldx, Xs + c * rows, rows, lane);
+  }
+  if (rot) {  // uniform: J(:, pair) <- J(:, pair) R, straight into the two global column blocks
+    gemm(false, false, ncols, ni, nc, 1.0, Js, ncols, Rs, nc, 0.0, J + (long long)bi * jb * ldj, ldj);
+    gemm(false, false, ncols, nj, nc, 1.0, Js, ncols, Rs + (long long)ni * nc, nc, 0.0,
+         J + (long long)bj * jb * ldj, ldj);
+  }
+  __syncthreads();
+  return rot;
+}
+
 // Blocked one-sided Jacobi for column sets that do not fit in shared memory
 // (X k x kp and J kp x kp in L2).  Columns are grouped in blocks of jb; each
 // outer round pairs blocks round-robin and, per block pair, the CTA stages
@@ -447,12 +501,10 @@ __device__ __noinline__ bool jacobi_blocked(Ctx& cx, int rows, int ncols, double
   __shared__ int s_rot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int jb = 16;
-  while (jb > 2 && 2 * jb * (rows + ncols) > cx.scap - cx.stop) jb >>= 1;
-  if (2 * jb * (rows + ncols) > cx.scap - cx.stop) return false;
+  while (jb > 2 && jac_pair_smem(jb, rows, ncols) > cx.scap - cx.stop) jb >>= 1;
+  if (jac_pair_smem(jb, rows, ncols) > cx.scap - cx.stop) return false;
   const Mark mk = mark(cx);
-  double* st = salloc(cx, (long long)2 * jb * (rows + ncols));
-  double* Xs = as_smem(cx, st);
-  double* Js = Xs + 2 * jb * rows;
+  double* st = as_smem(cx, salloc(cx, jac_pair_smem(jb, rows, ncols)));
   for (int j = warp; j < ncols; j += NWARP)
     for (int i = lane; i < ncols; i += 32) J[i + (long long)j * ldj] = (i == j) ? 1.0 : 0.0;
   __syncthreads();
@@ -468,26 +520,7 @@ __device__ __noinline__ bool jacobi_blocked(Ctx& cx, int rows, int ncols, double
         int bi, bj;
         rr_pair(bp, rnd, nbe, bi, bj);
         if (bj >= nb) continue;  // dummy block (uniform across the CTA)
-        const int ni = min(jb, ncols - bi * jb), nj = min(jb, ncols - bj * jb);
-        const int nc = ni + nj;
-        // stage in: local column c -> global column
-        for (int c = warp; c < nc; c += NWARP) {
-          const int gc = c < ni ? bi * jb + c : bj * jb + (c - ni);
-          const double* xg = X + (long long)gc * ldx;
-          const double* jg = J + (long long)gc * ldj;
-          warp_ld_cg(Xs + c * rows, xg, rows, lane);
-          warp_ld_cg(Js + c * ncols, jg, ncols, lane);
-        }
-        __syncthreads();
-        if (block_pair_sweep(Xs, rows, Js, ncols, nc, tol2) && threadIdx.x == 0) s_rot = 1;
-        for (int c = warp; c < nc; c += NWARP) {
-          const int gc = c < ni ? bi * jb + c : bj * jb + (c - ni);
-          double* xg = X + (long long)gc * ldx;
-          double* jg = J + (long long)gc * ldj;
-          warp_st_cg(xg, Xs + c * rows, rows, lane);
-          warp_st_cg(jg, Js + c * ncols, ncols, lane);
-        }
-        __syncthreads();
+        if (jacobi_block_pair(X, ldx, J, ldj, rows, ncols, jb, bi, bj, st, tol2) && threadIdx.x == 0) s_rot = 1;
       }
     }
     const int rot = s_rot;
@@ -616,23 +649,90 @@ __device__ __noinline__ int pivoted_qr(int m, int n, double* A, int lda, double 
 
 // Apply the first nref reflectors of a pivoted_qr factorization (vectors
 // below the diagonal of A, taus) to Z (m x nz): Z <- H_0 ... H_{nref-1} Z.
+// Register form: a warp owns whole columns of Z (RPL rows per lane, m <= 32
+// RPL), applies all nref reflectors to them with no CTA barrier (columns are
+// independent), and prefetches the next reflector while reducing the current
+// one.  Same per-column arithmetic as the plain loop below.
+template <int RPL>
+__device__ __noinline__ void apply_reflectors_reg(int m, int nref, const double* A, int lda, const double* taus, double* Z, int ldz,
+                                     int nz) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int c = warp; c < nz; c += NWARP) {
+    double* zc = Z + (long long)c * ldz;
+    double z[RPL];
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) z[r] = lane + 32 * r < m ? zc[lane + 32 * r] : 0.0;
+    constexpr bool PF = RPL <= 12;  // prefetch the next reflector (register budget)
+    double vn[PF ? RPL : 1];
+    int k = nref - 1;
+    if (PF && k >= 0) {
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        const int i = lane + 32 * r;
+        vn[PF ? r : 0] = (i > k && i < m) ? A[i + (long long)k * lda] : 0.0;
+      }
+    }
+    for (; k >= 0; --k) {
+      double v[RPL];
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        const int i = lane + 32 * r;
+        v[r] = PF ? vn[PF ? r : 0] : ((i > k && i < m) ? A[i + (long long)k * lda] : 0.0);
+      }
+      const double tau = taus[k];
+      if (PF && k > 0) {  // prefetch reflector k - 1
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) {
+          const int i = lane + 32 * r;
+          vn[PF ? r : 0] = (i > k - 1 && i < m) ? A[i + (long long)(k - 1) * lda] : 0.0;
+        }
+      }
+      if (tau == 0.0) continue;
+      double d = 0.0, zk = 0.0;
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        d = fma(v[r], z[r], d);
+        if (lane + 32 * r == k) zk = z[r];
+      }
+      d = (warp_sum(d) + __shfl_sync(0xffffffffu, zk, k & 31)) * tau;
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        z[r] = fma(-d, v[r], z[r]);
+        if (lane + 32 * r == k) z[r] -= d;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RPL; ++r)
+      if (lane + 32 * r < m) zc[lane + 32 * r] = z[r];
+  }
+  __syncthreads();
+}
+
+// Apply the first nref reflectors of a pivoted_qr factorization (vectors
+// below the diagonal of A, taus) to Z (m x nz): Z <- H_0 ... H_{nref-1} Z.
 __device__ __noinline__ void apply_reflectors(int m, int nref, const double* A, int lda, const double* taus, double* Z,
                                               int ldz, int nz) {
+  if (m <= 128) return apply_reflectors_reg<4>(m, nref, A, lda, taus, Z, ldz, nz);
+  if (m <= 256) return apply_reflectors_reg<8>(m, nref, A, lda, taus, Z, ldz, nz);
+  if (m <= 384) return apply_reflectors_reg<12>(m, nref, A, lda, taus, Z, ldz, nz);
+  if (m <= 512) return apply_reflectors_reg<16>(m, nref, A, lda, taus, Z, ldz, nz);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int k = nref - 1; k >= 0; --k) {
-    const double tau = taus[k];
-    if (tau == 0.0) continue;
-    const double* vk = A + (long long)k * lda;
-    for (int c = warp; c < nz; c += NWARP) {
-      double* zc = Z + (long long)c * ldz;
+  for (int c = warp; c < nz; c += NWARP) {  // columns are independent: no CTA barrier per reflector
+    double* zc = Z + (long long)c * ldz;
+    for (int k = nref - 1; k >= 0; --k) {
+      const double tau = taus[k];
+      if (tau == 0.0) continue;
+      const double* vk = A + (long long)k * lda;
       double d = 0.0;
       for (int i = k + 1 + lane; i < m; i += 32) d = fma(vk[i], zc[i], d);
       d = (warp_sum(d) + zc[k]) * tau;
+      __syncwarp();
       if (lane == 0) zc[k] -= d;
       for (int i = k + 1 + lane; i < m; i += 32) zc[i] = fma(-d, vk[i], zc[i]);
+      __syncwarp();
     }
-    __syncthreads();
   }
+  __syncthreads();
 }
 
 // ---------------------------------------------------------------------------

@@ -199,13 +199,12 @@ __device__ void team_jacobi_member(Ctx& cx, TeamJob* job, int t, int team) {
   double* X = job->pv[0];
   double* J = job->pv[1];
   const Mark mk = mark(cx);
-  double* st = salloc(cx, (long long)2 * jb * (rows + ncols));
+  double* st = salloc(cx, jac_pair_smem(jb, rows, ncols));
   if (!st) {  // the leader sized jb for its own (fuller) arena; cannot happen
     if (threadIdx.x == 0) atomicOr(cx.status, ST_ARENA_OVERFLOW);
     st = cx.sbase;
   }
-  double* Xs = as_smem(cx, st);
-  double* Js = Xs + 2 * jb * rows;
+  st = as_smem(cx, st);
   const double tol = 2.220446049250313e-16 * (double)max(rows, 1);
   const double tol2 = tol * tol;
   const int nb = (ncols + jb - 1) / jb;
@@ -217,25 +216,7 @@ __device__ void team_jacobi_member(Ctx& cx, TeamJob* job, int t, int team) {
         int bi, bj;
         rr_pair(bp, rnd, nbe, bi, bj);
         if (bj >= nb) continue;
-        const int ni = min(jb, ncols - bi * jb), nj = min(jb, ncols - bj * jb);
-        const int nc = ni + nj;
-        for (int c = warp; c < nc; c += NWARP) {
-          const int gc = c < ni ? bi * jb + c : bj * jb + (c - ni);
-          const double* xg = X + (long long)gc * ldx;
-          const double* jg = J + (long long)gc * ldj;
-          warp_ld_cg(Xs + c * rows, xg, rows, lane);
-          warp_ld_cg(Js + c * ncols, jg, ncols, lane);
-        }
-        __syncthreads();
-        if (block_pair_sweep(Xs, rows, Js, ncols, nc, tol2) && threadIdx.x == 0) s_rot = 1;
-        for (int c = warp; c < nc; c += NWARP) {
-          const int gc = c < ni ? bi * jb + c : bj * jb + (c - ni);
-          double* xg = X + (long long)gc * ldx;
-          double* jg = J + (long long)gc * ldj;
-          warp_st_cg(xg, Xs + c * rows, rows, lane);
-          warp_st_cg(jg, Js + c * ncols, ncols, lane);
-        }
-        __syncthreads();
+        if (jacobi_block_pair(X, ldx, J, ldj, rows, ncols, jb, bi, bj, st, tol2) && threadIdx.x == 0) s_rot = 1;
       }
       team_barrier(cx, job, team);
       // every member has passed this sweep's first barrier, so all have read
@@ -261,8 +242,8 @@ __device__ bool team_jacobi_lead(Ctx& cx, int rows, int ncols, double* X, int ld
   if (!cx.team || in_smem(cx, X) || in_smem(cx, J)) return false;  // other CTAs need global addresses
   // jacobi_blocked's block size for this arena state
   int jb = 16;
-  while (jb > 2 && 2 * jb * (rows + ncols) > cx.scap - cx.stop) jb >>= 1;
-  if (2 * jb * (rows + ncols) > cx.scap - cx.stop) return false;
+  while (jb > 2 && jac_pair_smem(jb, rows, ncols) > cx.scap - cx.stop) jb >>= 1;
+  if (jac_pair_smem(jb, rows, ncols) > cx.scap - cx.stop) return false;
   const int nb = (ncols + jb - 1) / jb;
   const int want = min(TEAM_MAX, ((nb + 1) & ~1) / 2);
   if (want < 2) return false;
