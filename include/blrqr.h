@@ -175,7 +175,7 @@ int blrqr_tiled_run(const blrqr_grid* g, const blrqr_refl* rf, const blrqr_task*
  * bit 1: the task may recruit a CTA team; bits 2+: ready ring 0..7 from the
  * task's bottom level on the DAG, longest remaining chain served first).
  * blrqr_tiled_run_dag runs the whole factorization with one persistent CTA
- * per SM pulling ready tasks; work_dev is 9*ntasks + 32 ints of scratch. */
+ * per SM pulling ready tasks; work_dev is blrqr_dag_work_ints(ntasks) ints of scratch. */
 int64_t blrqr_tiled_dag_size(int p, int q, int64_t* nedges);
 /* Debug: record (start ns, end ns, SM id) per task of subsequent dynamic runs
  * into a device buffer of 3*ntasks int64 (NULL disables). */
@@ -206,6 +206,8 @@ void blrqr_set_team_reserve(int nctas);
  * 2 CTA team over nctas CTAs.  sigma (ncols), perm (ncols) outputs. */
 int blrqr_debug_jacobi(int rows, int ncols, double* X, double* J, double* sigma, int* perm, int mode, double* ws,
                        int64_t ws_per_cta, int nctas, int* status, unsigned long long* flops, void* stream);
+/* Scratch ints blrqr_tiled_run_dag needs for ntasks tasks (ready rings, counters). */
+int64_t blrqr_dag_work_ints(int ntasks);
 /* Debug: `ctas` CTAs each run `reps` CTA-level GEMMs C = op(A) op(B) (+ C). */
 int blrqr_debug_gemm(int ta, int tb, int M, int N, int K, const double* A, int lda, const double* B, int ldb,
                      double* C, int ldc, int reps, int ctas, void* stream);

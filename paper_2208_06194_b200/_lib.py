@@ -72,6 +72,7 @@ _SIGS = {
     "blrqr_set_dag_rings": ([_I], None),
     "blrqr_set_qrcp_tol": ([_D], _I),
     "blrqr_set_team_reserve": ([_I], None),
+    "blrqr_dag_work_ints": ([_I], _L),
     "blrqr_debug_phase_trace": ([_P], None),
     "blrqr_apply_q": ([C.POINTER(Grid), C.POINTER(Refl), _I, _P, _L, _I, _I, _P, _L, _I, _P, _P, _P], _I),
     "blrqr_blr_to_dense": ([C.POINTER(Grid), _P, _L, _P], _I),

@@ -390,7 +390,10 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM) k_mgs_update(blrqr_grid a, bl
 // acquires then __threadfence + __syncthreads before the CTA reads.
 // ready rings, ring 0 served first; a task's ring is prio >> 2 (host-assigned
 // from its bottom level on the DAG, longest remaining chain first)
-constexpr int DAG_RINGS = 8;
+#ifndef BLR_DAG_RINGS
+#define BLR_DAG_RINGS 8
+#endif
+constexpr int DAG_RINGS = BLR_DAG_RINGS;
 
 struct DagDev {
   int n;
@@ -938,6 +941,11 @@ int blrqr_set_qrcp_tol(double tol) {
 }
 
 
+
+int64_t blrqr_dag_work_ints(int ntasks) {
+  if (ntasks < 0) return -1;
+  return (int64_t)(DAG_RINGS + 1) * ntasks + 2 * DAG_RINGS + 1 + 32;
+}
 
 int64_t blrqr_tiled_dag_size(int p, int q, int64_t* nedges) {
   if (q < 1 || p < q) return -1;

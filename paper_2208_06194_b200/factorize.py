@@ -140,7 +140,8 @@ class DeviceFactorization:
                         "off": torch.from_numpy(off).to(dev), "succ": torch.from_numpy(succ).to(dev),
                         "prio": torch.from_numpy(prio).to(dev)}
                 self.dag = dict(self.rt.dag_cache[key])
-                self.dag["work"] = torch.empty(9 * self.dag["n"] + 32, dtype=torch.int32, device=dev)
+                nwork = int(self.rt.lib.blrqr_dag_work_ints(self.dag["n"]))
+                self.dag["work"] = torch.empty(nwork, dtype=torch.int32, device=dev)
         elif method == "blocked-hh":
             g = self.g
             self.rf = DeviceRefl(self.g)
