@@ -153,6 +153,19 @@ __device__ __forceinline__ bool jac_angle(double a, double b, double g, double t
 // cancels (new value < a quarter of the old), so the caller recomputes.
 constexpr int JAC_SMEM_MAXC = 160;  // jacobi_smem column limit (tracked-norm slots)
 
+// Early stop: the largest squared cosine g^2/(ab) among the pairs a sweep
+// rotated (CTA-wide, as ordered bits of a non-negative double).  Jacobi
+// converges quadratically, so when every rotation of a sweep had
+// cos^2 <= JAC_STOP_COS2 (cos <= 1e-8) the next sweep's cosines are ~1e-16
+// relative, at the rotation threshold rows*eps: that confirmation sweep is
+// skipped.
+__shared__ unsigned long long s_jac_cos2;
+constexpr double JAC_STOP_COS2 = 1e-16;
+__device__ __forceinline__ void jac_note_cos2(double a, double b, double g, int lane) {
+  if (lane == 0) atomicMax(&s_jac_cos2, (unsigned long long)__double_as_longlong((g * g) / (a * b)));
+}
+__device__ __forceinline__ double jac_cos2() { return __longlong_as_double((long long)s_jac_cos2); }
+
 __device__ __forceinline__ bool jac_norm_update(double& a, double& b, double t, double g) {
   const double tg = t * g;
   const double a2 = a - tg, b2 = b + tg;
@@ -203,6 +216,7 @@ __device__ __forceinline__ bool jac_pair_reg(double* xp, double* xq, int rows, d
   for (int o = 16; o > 0; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
   double c, s, t;
   if (!jac_angle_t(a, b, g, tol2, c, s, t)) return false;
+  jac_note_cos2(a, b, g, lane);
 #pragma unroll
   for (int r = 0; r < RPL; ++r) {
     const double x = c * xr[r] - s * yr[r];
@@ -341,7 +355,7 @@ __device__ __noinline__ void jacobi_smem(const Ctx& cx, int rows, int ncols, dou
   const int kk = (ncols + 1) & ~1;
   const int npairs = kk / 2;
   for (int sweep = 0; sweep < 40 && ncols > 1; ++sweep) {
-    if (threadIdx.x == 0) s_rot = 0;
+    if (threadIdx.x == 0) { s_rot = 0; s_jac_cos2 = 0ull; }
     stage_norms(X, rows, ncols, s_jn);  // fresh norms every sweep (bounded drift)
     for (int rnd = 0; rnd < kk - 1; ++rnd) {
       for (int pi = warp; pi < npairs; pi += 2 * NWARP) {
@@ -377,6 +391,8 @@ __device__ __noinline__ void jacobi_smem(const Ctx& cx, int rows, int ncols, dou
         double c0, s0, t0, c1, s1, t1;
         const bool r0 = v0 && jac_angle_t(a0, b0, g0, tol2, c0, s0, t0);
         const bool r1 = v1 && jac_angle_t(a1, b1, g1, tol2, c1, s1, t1);
+        if (r0) jac_note_cos2(a0, b0, g0, lane);
+        if (r1) jac_note_cos2(a1, b1, g1, lane);
         if (r0) {
           jac_rotate(X + p0 * rows, X + q0 * rows, rows, lane, c0, s0);
           jac_rotate(J + p0 * ncols, J + q0 * ncols, ncols, lane, c0, s0);
@@ -408,9 +424,10 @@ __device__ __noinline__ void jacobi_smem(const Ctx& cx, int rows, int ncols, dou
       __syncthreads();
     }
     const int rot = s_rot;
+    const double cos2 = jac_cos2();  // read before the barrier: thread 0 resets it next sweep
     __syncthreads();
     if (prof && threadIdx.x == 0) atomicAdd(prof + PROF_BASE + PH_JSWEEPS, 1ull);
-    if (!rot) break;
+    if (!rot || cos2 <= JAC_STOP_COS2) break;
   }
   if (prof && threadIdx.x == 0) atomicAdd(prof + PROF_BASE + PH_JCALLS, 1ull);
   for (int c = warp; c < ncols; c += NWARP) {
@@ -494,7 +511,7 @@ __device__ __noinline__ bool jacobi_blocked(Ctx& cx, int rows, int ncols, double
   const int nb = (ncols + jb - 1) / jb;
   const int nbe = (nb + 1) & ~1;
   for (int sweep = 0; sweep < 40 && ncols > 1; ++sweep) {
-    if (threadIdx.x == 0) s_rot = 0;
+    if (threadIdx.x == 0) { s_rot = 0; s_jac_cos2 = 0ull; }
     __syncthreads();
     for (int rnd = 0; rnd < nbe - 1; ++rnd) {
       for (int bp = 0; bp < nbe / 2; ++bp) {
@@ -505,9 +522,10 @@ __device__ __noinline__ bool jacobi_blocked(Ctx& cx, int rows, int ncols, double
       }
     }
     const int rot = s_rot;
+    const double cos2 = jac_cos2();  // read before the barrier: thread 0 resets it next sweep
     __syncthreads();
     if (prof && threadIdx.x == 0) atomicAdd(prof + PROF_BASE + PH_JSWEEPS, 1ull);
-    if (!rot) break;
+    if (!rot || cos2 <= JAC_STOP_COS2) break;
   }
   if (prof && threadIdx.x == 0) atomicAdd(prof + PROF_BASE + PH_JCALLS, 1ull);
   release(cx, mk);

@@ -57,6 +57,7 @@ struct __align__(128) TeamJob {
   int bar_count;
   int bar_gen;
   int rot[3];
+  unsigned long long cos2[3];  // per-sweep max rotated cos^2 (Jacobi early stop), recycled like rot
   int done;
   int kind;
   int iv[12];
@@ -127,6 +128,7 @@ __device__ int team_launch(Ctx& cx, TeamJob* job, int want) {
     job->team = 0;
     job->bar_count = 0;
     job->rot[0] = job->rot[1] = job->rot[2] = 0;
+    job->cos2[0] = job->cos2[1] = job->cos2[2] = 0ull;
     job->done = 0;
     // only ask for as many helpers as there are CTAs polling right now
     const bool hi = cx.team_hi != 0;
@@ -210,7 +212,8 @@ __device__ void team_jacobi_member(Ctx& cx, TeamJob* job, int t, int team) {
   const int nb = (ncols + jb - 1) / jb;
   const int nbe = (nb + 1) & ~1;
   for (int sweep = 0; sweep < 40; ++sweep) {
-    if (threadIdx.x == 0) s_rot = 0;
+    if (threadIdx.x == 0) { s_rot = 0; s_jac_cos2 = 0ull; }
+    __syncthreads();
     for (int rnd = 0; rnd < nbe - 1; ++rnd) {
       for (int bp = t; bp < nbe / 2; bp += team) {
         int bi, bj;
@@ -221,12 +224,21 @@ __device__ void team_jacobi_member(Ctx& cx, TeamJob* job, int t, int team) {
       team_barrier(cx, job, team);
       // every member has passed this sweep's first barrier, so all have read
       // the flag of the previous sweep: recycle the one of the sweep after next
-      if (rnd == 0 && t == 0 && threadIdx.x == 0) job->rot[(sweep + 2) % 3] = 0;
+      if (rnd == 0 && t == 0 && threadIdx.x == 0) {
+        job->rot[(sweep + 2) % 3] = 0;
+        job->cos2[(sweep + 2) % 3] = 0ull;
+      }
     }
     // publish this member's rotations, then agree on convergence
-    if (threadIdx.x == 0 && s_rot) atomicOr(&job->rot[sweep % 3], 1);
+    if (threadIdx.x == 0 && s_rot) {
+      atomicOr(&job->rot[sweep % 3], 1);
+      atomicMax(&job->cos2[sweep % 3], s_jac_cos2);
+    }
     team_barrier(cx, job, team);
-    if (threadIdx.x == 0) s_conv = (vload(&job->rot[sweep % 3]) == 0);
+    if (threadIdx.x == 0) {
+      const unsigned long long c2 = *reinterpret_cast<volatile unsigned long long*>(&job->cos2[sweep % 3]);
+      s_conv = (vload(&job->rot[sweep % 3]) == 0) || __longlong_as_double((long long)c2) <= JAC_STOP_COS2;
+    }
     __syncthreads();
     if (t == 0 && threadIdx.x == 0 && cx.flops) atomicAdd(cx.flops + PROF_BASE + PH_JSWEEPS, 1ull);
     if (s_conv) break;
