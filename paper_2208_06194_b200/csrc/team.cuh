@@ -43,7 +43,10 @@ constexpr int TEAM_TICKETS = 1 << 22;
 constexpr int TEAM_CLOSED = 0x8000;
 constexpr long long TEAM_WAIT_CYCLES = 40000;           // leader's wait for helpers (~20 us)
 constexpr long long TEAM_SPIN_TIMEOUT = 20000000000LL;  // ~10 s of spinning -> abort
-constexpr int BACK_CW = 32;                              // back-transform column chunk
+#ifndef BLR_BACK_CW
+#define BLR_BACK_CW 32
+#endif
+constexpr int BACK_CW = BLR_BACK_CW;                              // back-transform column chunk
 constexpr int TEAM_BACK_MIN = 64;  // Q_U width from which the back-transform splits
 constexpr int TEAM_QRCP_MIN = 128;  // core order from which the pivoted QR splits
 
