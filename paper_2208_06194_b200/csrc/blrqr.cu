@@ -295,14 +295,6 @@ __global__ void __launch_bounds__(NT) k_lr_product(int op, int m, int k, int n, 
 
 #include "tasks_blocked_mgs.cuh"
 
-// ---- blocked Householder step kernels ------------------------------------
-__global__ void __launch_bounds__(NT, CTAS_PER_SM) k_blocked_panel(blrqr_grid g, blrqr_refl rf, int k, double* P, double* Yp,
-                                                         double* ws, long long wsp, int* status,
-                                                         unsigned long long* flops) {
-  Ctx cx = make_ctx(ws, wsp, status, flops);
-  blocked_panel(cx, g, rf, k, P, Yp);
-}
-
 // Column ownership for the block-cyclic multi-GPU drivers: this launch
 // touches only the update columns j with j mod world == rank (world = 1: all).
 __device__ __forceinline__ int owned_col(int first, int world, int rank, int idx) {
@@ -314,70 +306,56 @@ __host__ __device__ __forceinline__ int owned_count(int first, int end, int worl
   return j0 >= end ? 0 : (end - j0 + world - 1) / world;
 }
 
-__global__ void __launch_bounds__(NT, CTAS_PER_SM) k_blocked_chain(blrqr_grid g, blrqr_refl rf, int k, double eps, double* zbuf,
-                                                         int* zrank, double* ws, long long wsp, int* status,
-                                                         unsigned long long* flops, int world, int rank) {
-  Ctx cx = make_ctx(ws, wsp, status, flops);
-  const long long bb = (long long)g.b * g.b;
-  const int nj = owned_count(k + 1, g.q, world, rank);
-  for (int jj = blockIdx.x; jj < nj; jj += gridDim.x) {
-    const int j = owned_col(k + 1, world, rank, jj);
-    blocked_chain(cx, g, rf, eps, k, j, zbuf + 2 * bb * j, zbuf + 2 * bb * j + bb, zrank + j);
-    cx.top = 0;
-    cx.stop = 0;
-    __syncthreads();
-  }
-}
+// ---- blocked Householder / blocked MGS step kernels -----------------------
+// Each step's independent tasks (one panel; one chain per column j; one
+// update per (i, j)) run through team_task_loop on the full grid: CTAs
+// without a task of their own join the team jobs (QR, Jacobi, back-transform,
+// GEQRT, T build) of the running ones -- the panel and the long ascending-i
+// chains are the critical path of these methods.  Teams do not change any
+// result bit (team.cuh).
+constexpr int BSTEP_PANEL = 0, BSTEP_CHAIN = 1, BSTEP_UPDATE = 2;
 
-__global__ void __launch_bounds__(NT, CTAS_PER_SM) k_blocked_update(blrqr_grid g, blrqr_refl rf, int k, double eps,
-                                                          double* zbuf, const int* zrank, double* ws, long long wsp,
-                                                          int* status, unsigned long long* flops, int world, int rank) {
+__global__ void __launch_bounds__(NT, CTAS_PER_SM) k_blocked_stage(int stage, blrqr_grid g, blrqr_refl rf, int k,
+                                                                   double eps, double* P, double* Yp, double* zbuf,
+                                                                   int* zrank, double* ws, long long wsp, int* status,
+                                                                   unsigned long long* flops, int world, int rank,
+                                                                   TeamCtx* team, int* ctr) {
   Ctx cx = make_ctx(ws, wsp, status, flops);
+  cx.team = team;
   const long long bb = (long long)g.b * g.b;
   const int ni = g.p - k, nj = owned_count(k + 1, g.q, world, rank);
-  for (int t = blockIdx.x; t < ni * nj; t += gridDim.x) {
-    const int i = k + t % ni, j = owned_col(k + 1, world, rank, t / ni);
-    blocked_update(cx, g, rf, eps, k, i, j, zbuf + 2 * bb * j, zbuf + 2 * bb * j + bb, zrank + j);
-    cx.top = 0;
-    cx.stop = 0;
-    __syncthreads();
-  }
+  const long long n = stage == BSTEP_PANEL ? 1 : (stage == BSTEP_CHAIN ? nj : (long long)ni * nj);
+  team_task_loop(cx, n, ctr, [&](long long t) {
+    if (stage == BSTEP_PANEL) {
+      blocked_panel(cx, g, rf, k, P, Yp);
+    } else if (stage == BSTEP_CHAIN) {
+      const int j = owned_col(k + 1, world, rank, (int)t);
+      blocked_chain(cx, g, rf, eps, k, j, zbuf + 2 * bb * j, zbuf + 2 * bb * j + bb, zrank + j);
+    } else {
+      const int i = k + (int)(t % ni), j = owned_col(k + 1, world, rank, (int)(t / ni));
+      blocked_update(cx, g, rf, eps, k, i, j, zbuf + 2 * bb * j, zbuf + 2 * bb * j + bb, zrank + j);
+    }
+  });
 }
 
-// ---- blocked MGS step kernels ---------------------------------------------
-__global__ void __launch_bounds__(NT, CTAS_PER_SM) k_mgs_panel_task(blrqr_grid a, blrqr_grid qg, blrqr_grid rg, int j,
-                                                          double* P, double* ws, long long wsp, int* status,
-                                                          unsigned long long* flops) {
+__global__ void __launch_bounds__(NT, CTAS_PER_SM) k_mgs_stage(int stage, blrqr_grid a, blrqr_grid qg, blrqr_grid rg,
+                                                               int j, double eps, double* P, double* ws, long long wsp,
+                                                               int* status, unsigned long long* flops, int world,
+                                                               int rank, TeamCtx* team, int* ctr) {
   Ctx cx = make_ctx(ws, wsp, status, flops);
-  mgs_panel_task(cx, a, qg, rg, j, P);
-}
-
-__global__ void __launch_bounds__(NT, CTAS_PER_SM) k_mgs_project(blrqr_grid a, blrqr_grid qg, blrqr_grid rg, int j, double eps,
-                                                       double* ws, long long wsp, int* status,
-                                                       unsigned long long* flops, int world, int rank) {
-  Ctx cx = make_ctx(ws, wsp, status, flops);
+  cx.team = team;
   const int nk = owned_count(j + 1, a.q, world, rank);
-  for (int kk = blockIdx.x; kk < nk; kk += gridDim.x) {
-    const int k = owned_col(j + 1, world, rank, kk);
-    mgs_project(cx, a, qg, rg, eps, j, k);
-    cx.top = 0;
-    cx.stop = 0;
-    __syncthreads();
-  }
-}
-
-__global__ void __launch_bounds__(NT, CTAS_PER_SM) k_mgs_update(blrqr_grid a, blrqr_grid qg, blrqr_grid rg, int j, double eps,
-                                                      double* ws, long long wsp, int* status,
-                                                      unsigned long long* flops, int world, int rank) {
-  Ctx cx = make_ctx(ws, wsp, status, flops);
-  const int nk = owned_count(j + 1, a.q, world, rank);
-  for (int t = blockIdx.x; t < nk * a.p; t += gridDim.x) {
-    const int i = t % a.p, k = owned_col(j + 1, world, rank, t / a.p);
-    mgs_update(cx, a, qg, rg, eps, j, i, k);
-    cx.top = 0;
-    cx.stop = 0;
-    __syncthreads();
-  }
+  const long long n = stage == BSTEP_PANEL ? 1 : (stage == BSTEP_CHAIN ? nk : (long long)nk * a.p);
+  team_task_loop(cx, n, ctr, [&](long long t) {
+    if (stage == BSTEP_PANEL) {
+      mgs_panel_task(cx, a, qg, rg, j, P);
+    } else if (stage == BSTEP_CHAIN) {
+      mgs_project(cx, a, qg, rg, eps, j, owned_col(j + 1, world, rank, (int)t));
+    } else {
+      const int i = (int)(t % a.p), k = owned_col(j + 1, world, rank, (int)(t / a.p));
+      mgs_update(cx, a, qg, rg, eps, j, i, k);
+    }
+  });
 }
 
 // ---- dynamic (dependency-counter) tiled scheduler ---------------------------
@@ -592,12 +570,8 @@ static void init_kernels() {
     smem_optin(k_lr_product);
     smem_optin(k_tiled);
     smem_optin(k_tiled_dag);
-    smem_optin(k_blocked_panel);
-    smem_optin(k_blocked_chain);
-    smem_optin(k_blocked_update);
-    smem_optin(k_mgs_panel_task);
-    smem_optin(k_mgs_project);
-    smem_optin(k_mgs_update);
+    smem_optin(k_blocked_stage);
+    smem_optin(k_mgs_stage);
   });
 }
 #define INIT_KERNELS() init_kernels()
@@ -1065,21 +1039,24 @@ int blrqr_blocked_step_dist(const blrqr_grid* g, const blrqr_refl* rf, int k, do
   if (world < 1 || rank < 0 || rank >= world) return -5;
   INIT_KERNELS();
   cudaStream_t st = as_stream(stream);
-  if (phases & 1) {
+  auto launch = [&](int stage, int64_t ntask) -> int {
+    int* ctr = nullptr;
+    TeamCtx* team = nullptr;
+    if (int e = team_for_launch(st, &team, &ctr)) return e;
+    const int grid = (int)std::max<int64_t>(1, team ? nctas : std::min<int64_t>(ntask, nctas));
     double* P = panel_ws;
     double* Yp = panel_ws + (int64_t)g->p * g->b * g->b;
-    k_blocked_panel<<<1, NT, SMEM_BYTES, st>>>(*g, *rf, k, P, Yp, ws, ws_per_cta, status, flops);
+    k_blocked_stage<<<grid, NT, SMEM_BYTES, st>>>(stage, *g, *rf, k, eps, P, Yp, zbuf, zrank, ws, ws_per_cta, status,
+                                                   flops, world, rank, team, ctr);
     CK(cudaGetLastError());
-  }
+    return 0;
+  };
+  if (phases & 1)
+    if (int e = launch(BSTEP_PANEL, 1)) return e;
   const int nj = owned_count(k + 1, g->q, world, rank);
   if ((phases & 2) && nj > 0) {
-    k_blocked_chain<<<std::min(nj, nctas), NT, SMEM_BYTES, st>>>(*g, *rf, k, eps, zbuf, zrank, ws, ws_per_cta,
-                                                                 status, flops, world, rank);
-    CK(cudaGetLastError());
-    const int nt = (g->p - k) * nj;
-    k_blocked_update<<<std::min(nt, nctas), NT, SMEM_BYTES, st>>>(*g, *rf, k, eps, zbuf, zrank, ws, ws_per_cta,
-                                                                  status, flops, world, rank);
-    CK(cudaGetLastError());
+    if (int e = launch(BSTEP_CHAIN, nj)) return e;
+    if (int e = launch(BSTEP_UPDATE, (int64_t)(g->p - k) * nj)) return e;
   }
   return 0;
 }
@@ -1101,18 +1078,22 @@ int blrqr_mgs_step_dist(const blrqr_grid* a, const blrqr_grid* qg, const blrqr_g
   if (world < 1 || rank < 0 || rank >= world) return -5;
   INIT_KERNELS();
   cudaStream_t st = as_stream(stream);
-  if (phases & 1) {
-    k_mgs_panel_task<<<1, NT, SMEM_BYTES, st>>>(*a, *qg, *rg, j, panel_ws, ws, ws_per_cta, status, flops);
+  auto launch = [&](int stage, int64_t ntask) -> int {
+    int* ctr = nullptr;
+    TeamCtx* team = nullptr;
+    if (int e = team_for_launch(st, &team, &ctr)) return e;
+    const int grid = (int)std::max<int64_t>(1, team ? nctas : std::min<int64_t>(ntask, nctas));
+    k_mgs_stage<<<grid, NT, SMEM_BYTES, st>>>(stage, *a, *qg, *rg, j, eps, panel_ws, ws, ws_per_cta, status, flops,
+                                               world, rank, team, ctr);
     CK(cudaGetLastError());
-  }
+    return 0;
+  };
+  if (phases & 1)
+    if (int e = launch(BSTEP_PANEL, 1)) return e;
   const int nk = owned_count(j + 1, a->q, world, rank);
   if ((phases & 2) && nk > 0) {
-    k_mgs_project<<<std::min(nk, nctas), NT, SMEM_BYTES, st>>>(*a, *qg, *rg, j, eps, ws, ws_per_cta, status, flops,
-                                                               world, rank);
-    CK(cudaGetLastError());
-    k_mgs_update<<<std::min(nk * a->p, nctas), NT, SMEM_BYTES, st>>>(*a, *qg, *rg, j, eps, ws, ws_per_cta, status,
-                                                                     flops, world, rank);
-    CK(cudaGetLastError());
+    if (int e = launch(BSTEP_CHAIN, nk)) return e;
+    if (int e = launch(BSTEP_UPDATE, (int64_t)nk * a->p)) return e;
   }
   return 0;
 }
