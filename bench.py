@@ -126,6 +126,11 @@ def cpu_reference_sample(cfg_name: str, rows: int, threads: int, grid_host=None)
     grid = oblr.Grid(c.n, c.n, b, lowrank, [[cells.get((i, j)) for j in range(p)] for i in range(p)])
     st = oalg.TiledState(grid, c.eps)  # no clone: the sample owns its cells
     ofl.reset()
+    # single-threaded BLAS under the thread pool, also when numpy was imported
+    # (by torch) before OPENBLAS_NUM_THREADS could be set: oversubscribed
+    # BLAS threads made this sample 6x slower inside the GPU arm
+    from threadpoolctl import threadpool_limits
+    limiter = threadpool_limits(1)
     t0 = time.perf_counter()
     with ThreadPoolExecutor(max_workers=threads) as pool:
         st.diag_qr(0)
@@ -134,6 +139,7 @@ def cpu_reference_sample(cfg_name: str, rows: int, threads: int, grid_host=None)
             st.update_qr(0, i)
             list(pool.map(lambda j, i=i: st.apply_trap(0, i, j), range(1, p)))
     dt = time.perf_counter() - t0
+    limiter.restore_original_limits()
     fl = ofl.total()
     sample = (f"{cfg_name} tiled-hh sweep k=0, block rows 1..{rows} of {p - 1}: DiagQR(0), {p - 1} ApplyBlock, "
               f"{rows} UpdateQR, {rows * (p - 1)} ApplyTrap; fork-join pool of {threads} threads over j")
