@@ -305,7 +305,7 @@ __device__ Blk blk_mul(Ctx& cx, const Blk& x, const Blk& y) {
   }
   if (y.lr) {
     double* u = alloc(cx, (long long)x.rows * max(y.rank, 1));
-    gemm(false, false, x.rows, y.rank, x.cols, 1.0, x.u, x.ldu, y.u, y.ldu, 0.0, u, x.rows);
+    team_gemm(cx, false, false, x.rows, y.rank, x.cols, 1.0, x.u, x.ldu, y.u, y.ldu, 0.0, u, x.rows);
     add_flops(cx, FK_LR_MUL, mm_cost(x.rows, x.cols, y.rank));
     return make_lr(x.rows, y.cols, y.rank, u, x.rows, y.v, y.ldv, s);
   }
@@ -334,7 +334,7 @@ __device__ Blk blk_mul_t(Ctx& cx, const Blk& x, const Blk& y) {
   }
   if (y.lr) {
     double* u = alloc(cx, (long long)x.cols * max(y.rank, 1));
-    gemm(true, false, x.cols, y.rank, x.rows, 1.0, x.u, x.ldu, y.u, y.ldu, 0.0, u, x.cols);
+    team_gemm(cx, true, false, x.cols, y.rank, x.rows, 1.0, x.u, x.ldu, y.u, y.ldu, 0.0, u, x.cols);
     add_flops(cx, FK_LR_MUL, mm_cost(x.cols, x.rows, y.rank));
     return make_lr(x.cols, y.cols, y.rank, u, x.cols, y.v, y.ldv, s);
   }
@@ -348,12 +348,12 @@ __device__ Blk blk_mul_t(Ctx& cx, const Blk& x, const Blk& y) {
 __device__ Blk blk_dense_times(Ctx& cx, const double* t, int ldt, bool trans, const Blk& x) {
   if (x.lr) {
     double* u = alloc(cx, (long long)x.rows * max(x.rank, 1));
-    gemm(trans, false, x.rows, x.rank, x.rows, 1.0, t, ldt, x.u, x.ldu, 0.0, u, x.rows);
+    team_gemm(cx, trans, false, x.rows, x.rank, x.rows, 1.0, t, ldt, x.u, x.ldu, 0.0, u, x.rows);
     add_flops(cx, FK_LR_MUL, mm_cost(x.rows, x.rows, x.rank));
     return make_lr(x.rows, x.cols, x.rank, u, x.rows, x.v, x.ldv, x.s);
   }
   double* d = alloc(cx, (long long)x.rows * x.cols);
-  gemm(trans, false, x.rows, x.cols, x.rows, 1.0, t, ldt, x.u, x.ldu, 0.0, d, x.rows);
+  team_gemm(cx, trans, false, x.rows, x.cols, x.rows, 1.0, t, ldt, x.u, x.ldu, 0.0, d, x.rows);
   add_flops(cx, FK_GEMM, mm_cost(x.rows, x.rows, x.cols));
   return make_dense(x.rows, x.cols, d, x.rows, x.s);
 }
@@ -362,7 +362,7 @@ __device__ Blk blk_dense_times(Ctx& cx, const double* t, int ldt, bool trans, co
 __device__ void expand_add(Ctx& cx, const Blk& d, const Blk& l, double* dst, int ldd) {
   copy_mat(d.rows, d.cols, d.u, d.ldu, dst, ldd, d.s);
   if (l.rank > 0) {
-    gemm(false, true, l.rows, l.cols, l.rank, l.s, l.u, l.ldu, l.v, l.ldv, 1.0, dst, ldd);
+    team_gemm(cx, false, true, l.rows, l.cols, l.rank, l.s, l.u, l.ldu, l.v, l.ldv, 1.0, dst, ldd);
     add_flops(cx, FK_EXPAND, mm_cost(l.rows, l.rank, l.cols));
   }
 }
@@ -442,7 +442,7 @@ __device__ __noinline__ void sub_into_cell(Ctx& cx, const Cell& c, const Blk& te
   } else {
     if (term.lr) {
       if (term.rank > 0) {
-        gemm(false, true, c.b, c.b, term.rank, -term.s, term.u, term.ldu, term.v, term.ldv, 1.0, c.u, c.ld);
+        team_gemm(cx, false, true, c.b, c.b, term.rank, -term.s, term.u, term.ldu, term.v, term.ldv, 1.0, c.u, c.ld);
         add_flops(cx, FK_EXPAND, mm_cost(c.b, term.rank, c.b));
       }
     } else {

@@ -20,7 +20,9 @@
 //   TK_TPQRT  UpdateQR's triangular-pentagonal QR: panels as TK_QRB, then
 //             the T build as TK_TBUILD, with the same team;
 //   TK_BACK   the back-transform U_C = Q_U [Q1 J_r; 0], V_C = Q_V [Q2 W_r; 0]
-//             in fixed 32-column chunks, chunk c on member c mod T.
+//             in fixed 32-column chunks, chunk c on member c mod T;
+//   TK_GEMM   the block products of the ApplyTrap updates (T_ik^T ssum.u,
+//             dense x low-rank, expansions): fixed 64-column chunks of C.
 // Every kind performs exactly the single-CTA operation sequence on the same
 // data partition (jacobi_blocked's rounds, the same column chunks), so the
 // results are bitwise independent of how many helpers turned up, and equal
@@ -50,7 +52,7 @@ constexpr int BACK_CW = BLR_BACK_CW;                              // back-transf
 constexpr int TEAM_BACK_MIN = 64;  // Q_U width from which the back-transform splits
 constexpr int TEAM_QRCP_MIN = 128;  // core order from which the pivoted QR splits
 
-enum TeamKind : int { TK_JACOBI = 1, TK_BACK = 2, TK_QRB = 3, TK_QRCP = 4, TK_TBUILD = 5, TK_TPQRT = 6 };
+enum TeamKind : int { TK_JACOBI = 1, TK_BACK = 2, TK_QRB = 3, TK_QRCP = 4, TK_TBUILD = 5, TK_TPQRT = 6, TK_GEMM = 7 };
 
 struct __align__(128) TeamJob {
   int state;  // 0 free, 9 being set up, 2 running (team size published)
@@ -437,6 +439,51 @@ __device__ void build_t_team(Ctx& cx, int n, int m, const double* Y, int ldy, bo
   }
 }
 
+// ---- TK_GEMM -----------------------------------------------------------------
+// C = alpha op(A) op(B) + beta C in fixed GEMM_CW-column chunks of C; a lone
+// CTA runs the same chunks, so results do not depend on the team size.
+// iv: ta, tb, M, N, K, lda, ldb, ldc; dv: alpha, beta; pv: A, B, C
+constexpr int GEMM_CW = 64;
+constexpr int TEAM_GEMM_MIN_MNK = 1 << 22;  // M*N*K from which helpers are recruited
+
+__device__ __forceinline__ void gemm_chunk(int ch, bool ta, bool tb, int M, int N, int K, double alpha, const double* A,
+                                           int lda, const double* B, int ldb, double beta, double* C, int ldc) {
+  const int c0 = ch * GEMM_CW, nc = min(GEMM_CW, N - c0);
+  gemm(ta, tb, M, nc, K, alpha, A, lda, tb ? B + c0 : B + (long long)c0 * ldb, ldb, beta, C + (long long)c0 * ldc,
+       ldc);
+}
+
+__device__ void team_gemm_member(Ctx& cx, TeamJob* job, int t, int team) {
+  const int* iv = job->iv;
+  const int nch = (iv[3] + GEMM_CW - 1) / GEMM_CW;
+  for (int ch = t; ch < nch; ch += team)
+    gemm_chunk(ch, iv[0] != 0, iv[1] != 0, iv[2], iv[3], iv[4], job->dv[0], job->pv[0], iv[5], job->pv[1], iv[6],
+               job->dv[1], job->pv[2], iv[7]);
+}
+
+__device__ void team_gemm(Ctx& cx, bool ta, bool tb, int M, int N, int K, double alpha, const double* A, int lda,
+                          const double* B, int ldb, double beta, double* C, int ldc) {
+  const int nch = (N + GEMM_CW - 1) / GEMM_CW;
+  const bool global = !in_smem(cx, A) && !in_smem(cx, B) && !in_smem(cx, C);
+  TeamJob* job = (nch >= 2 && global && (long long)M * N * K >= TEAM_GEMM_MIN_MNK) ? team_reserve(cx) : nullptr;
+  int team = 1;
+  if (job) {
+    if (threadIdx.x == 0) {
+      job->kind = TK_GEMM;
+      const int iv[8] = {ta ? 1 : 0, tb ? 1 : 0, M, N, K, lda, ldb, ldc};
+      for (int i = 0; i < 8; ++i) job->iv[i] = iv[i];
+      job->dv[0] = alpha;
+      job->dv[1] = beta;
+      job->pv[0] = const_cast<double*>(A);
+      job->pv[1] = const_cast<double*>(B);
+      job->pv[2] = C;
+    }
+    team = team_launch(cx, job, min(TEAM_MAX, nch));
+  }
+  for (int ch = 0; ch < nch; ch += team) gemm_chunk(ch, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  if (team > 1) team_finish(cx, job, team);
+}
+
 // ---- TK_TPQRT ----------------------------------------------------------------
 // iv: n, k, ldr, ldb, ldt; pv: R, B, T, S, tau
 __device__ void team_tpqrt_member(Ctx& cx, TeamJob* job, int t, int team) {
@@ -578,6 +625,7 @@ __device__ void team_help(Ctx& cx, TeamCtx* tc, int slot, int member) {
     case TK_QRCP: team_qrcp_member(cx, job, member, team); break;
     case TK_TBUILD: team_tbuild_member(cx, job, member, team); break;
     case TK_TPQRT: team_tpqrt_member(cx, job, member, team); break;
+    case TK_GEMM: team_gemm_member(cx, job, member, team); break;
     default: break;
   }
   __syncthreads();
