@@ -219,10 +219,11 @@ int blrqr_tiled_run_dag(const blrqr_grid* g, const blrqr_refl* rf, int ntasks, c
                         double timeout_s, int* status, unsigned long long* flops, void* stream);
 
 /* Blocked Householder (factorize.py:187-292), one step k: panel GEQRT of
- * block column k (triangularize_block_column, :187-229; one CTA), then for
+ * block column k (triangularize_block_column, :187-229; one task), then for
  * every j > k the ascending-i accumulation chain z_j = T_k^T sum_i Y_ik^T A_ij
- * (one CTA per j) and the independent updates A_ij -= Y_ik z_j (one CTA per
- * (i, j)) (apply_block_column_reflector, :232-262).
+ * (one task per j) and the independent updates A_ij -= Y_ik z_j (one task per
+ * (i, j)) (apply_block_column_reflector, :232-262).  Each stage is one launch
+ * on nctas CTAs; CTAs without a task join the running tasks' CTA teams.
  * zbuf: q * 2 * b * b doubles (z_j factors), zrank: q ints.
  * panel_ws: >= 2 * p * b * b doubles (stacked panel + explicit Y). */
 int blrqr_blocked_step(const blrqr_grid* g, const blrqr_refl* rf, int k, double eps, double* zbuf, int* zrank,
@@ -231,8 +232,9 @@ int blrqr_blocked_step(const blrqr_grid* g, const blrqr_refl* rf, int k, double 
 
 /* Blocked MGS (factorize.py:576-671), one step j: panel MGS of block column j
  * into the explicit Q grid qg (same kind map as a) and R_jj (rg, q x q),
- * projections R_jk (one CTA per k > j, ascending-i chain) and updates
- * A_ik -= Q_ij R_jk (one CTA per (i, k)).  panel_ws >= p * b * b doubles. */
+ * projections R_jk (one task per k > j, ascending-i chain) and updates
+ * A_ik -= Q_ij R_jk (one task per (i, k)); stages launched as for the blocked
+ * step.  panel_ws >= p * b * b doubles. */
 int blrqr_mgs_step(const blrqr_grid* a, const blrqr_grid* qg, const blrqr_grid* rg, int j, double eps,
                    double* panel_ws, int64_t panel_doubles, double* ws, int64_t ws_per_cta, int nctas, int* status,
                    unsigned long long* flops, void* stream);
