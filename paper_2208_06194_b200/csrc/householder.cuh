@@ -125,7 +125,6 @@ __device__ __noinline__ void build_t_full(Ctx& cx, int n, const double* S, int l
     // zero T(J, 0:j0) (strict lower blocks left of the diagonal block)
     for (int c = threadIdx.x >> 5; c < j0; c += NWARP)
       for (int a = threadIdx.x & 31; a < w; a += 32) {
-      const long long e = (long long)c * w + a;
       T[(j0 + a) + (long long)c * ldt] = 0.0;
     }
     if (j0 > 0) {

@@ -20,7 +20,6 @@ __device__ __noinline__ void jacobi_cols(int rows, int ncols, double* X, int ldx
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int j = threadIdx.x >> 5; j < ncols; j += NWARP)
     for (int i = threadIdx.x & 31; i < ncols; i += 32) {
-    const long long e = (long long)j * ncols + i;
     J[i + (long long)j * ldj] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
@@ -771,7 +770,6 @@ __device__ __noinline__ int rrqr_trunc(Ctx& cx, int m, int n, double* A, int lda
   // U = Q[:, :rank]: reflectors applied to the identity slab
   for (int c = threadIdx.x >> 5; c < rank; c += NWARP)
     for (int i = threadIdx.x & 31; i < m; i += 32) {
-    const long long e = (long long)c * m + i;
     U[i + (long long)c * ldu] = (i == c) ? 1.0 : 0.0;
   }
   __syncthreads();
@@ -779,7 +777,6 @@ __device__ __noinline__ int rrqr_trunc(Ctx& cx, int m, int n, double* A, int lda
   // V[piv[c], r] = R[r, c] (R upper: zero for c < r)
   for (int r = threadIdx.x >> 5; r < rank; r += NWARP)
     for (int c = threadIdx.x & 31; c < n; c += 32) {
-    const long long e = (long long)r * n + c;
     V[piv[c] + (long long)r * ldv] = (c >= r) ? A[r + (long long)c * lda] : 0.0;
   }
   __syncthreads();

@@ -201,7 +201,6 @@ __device__ void team_barrier(Ctx& cx, TeamJob* job, int team) {
 // iv: rows, ncols, ldx, ldj, jb; pv: X, J
 __device__ void team_jacobi_member(Ctx& cx, TeamJob* job, int t, int team) {
   __shared__ int s_rot, s_conv;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rows = job->iv[0], ncols = job->iv[1], ldx = job->iv[2], ldj = job->iv[3], jb = job->iv[4];
   double* X = job->pv[0];
   double* J = job->pv[1];
