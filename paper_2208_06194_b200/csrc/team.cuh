@@ -43,14 +43,23 @@ constexpr int TEAM_MAX = 16;  // members including the leader
 constexpr int TEAM_JOBS = 128;
 constexpr int TEAM_TICKETS = 1 << 22;
 constexpr int TEAM_CLOSED = 0x8000;
-constexpr long long TEAM_WAIT_CYCLES = 40000;           // leader's wait for helpers (~20 us)
+#ifndef BLR_TEAM_WAIT
+#define BLR_TEAM_WAIT 40000
+#endif
+constexpr long long TEAM_WAIT_CYCLES = BLR_TEAM_WAIT;           // leader's wait for helpers (~20 us)
 constexpr long long TEAM_SPIN_TIMEOUT = 20000000000LL;  // ~10 s of spinning -> abort
 #ifndef BLR_BACK_CW
 #define BLR_BACK_CW 32
 #endif
 constexpr int BACK_CW = BLR_BACK_CW;                              // back-transform column chunk
-constexpr int TEAM_BACK_MIN = 64;  // Q_U width from which the back-transform splits
-constexpr int TEAM_QRCP_MIN = 128;  // core order from which the pivoted QR splits
+#ifndef BLR_TEAM_BACK_MIN
+#define BLR_TEAM_BACK_MIN 64
+#endif
+constexpr int TEAM_BACK_MIN = BLR_TEAM_BACK_MIN;  // Q_U width from which the back-transform splits
+#ifndef BLR_TEAM_QRCP_MIN
+#define BLR_TEAM_QRCP_MIN 128
+#endif
+constexpr int TEAM_QRCP_MIN = BLR_TEAM_QRCP_MIN;  // core order from which the pivoted QR splits
 
 enum TeamKind : int { TK_JACOBI = 1, TK_BACK = 2, TK_QRB = 3, TK_QRCP = 4, TK_TBUILD = 5, TK_TPQRT = 6, TK_GEMM = 7 };
 
