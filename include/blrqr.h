@@ -131,6 +131,15 @@ int blrqr_apply_wy(int m, int n, int nc, const double* y, const double* t, doubl
                    int64_t ws_doubles, int* status, unsigned long long* flops, void* stream);
 /* tp_qr (kernels.py:131-155): r_top (n x n upper) and a_bot (k x n) ->
  * r_new, y (k x n), t (n x n).  Inputs are not modified. */
+/* GEQRT (op 0; kernels.py:87-103: a m x n -> y m x n, t n x n, r n x n) or
+ * TPQRT (op 1; kernels.py:131-155: top n x n upper over an m x n bottom a2
+ * -> o1 = r_new n x n, o2 = y m x n, o3 = t n x n) as one task of an
+ * nctas-CTA launch whose other CTAs join the task's CTA-team jobs -- the
+ * same device routines the tiled DiagQR / UpdateQR tasks run.  ws: nctas
+ * per-CTA workspaces of ws_per_cta doubles.  Results do not depend on nctas. */
+int blrqr_panel_team(int op, int m, int n, const double* a, const double* a2, double* o1, double* o2, double* o3,
+                     double* ws, int64_t ws_per_cta, int nctas, int* status, unsigned long long* flops,
+                     void* stream);
 int blrqr_tpqrt(int n, int k, const double* r_top, const double* a_bot, double* r_new, double* y, double* t,
                 double* ws, int64_t ws_doubles, int* status, unsigned long long* flops, void* stream);
 /* apply_tp(_transpose) (kernels.py:158-186): in place on c_top (n x nc), c_bot (k x nc) */
@@ -211,6 +220,19 @@ int64_t blrqr_dag_work_ints(int ntasks);
 /* Debug: `ctas` CTAs each run `reps` CTA-level GEMMs C = op(A) op(B) (+ C). */
 int blrqr_debug_gemm(int ta, int tb, int M, int N, int K, const double* A, int lda, const double* B, int ldb,
                      double* C, int ldc, int reps, int ctas, void* stream);
+/* Debug: select the device GEMM implementation for subsequent launches --
+ * 0 default dispatch (DMMA FP64 tensor-core tiles where they apply), 1 DFMA
+ * tiles only, 2 DMMA wherever a DMMA tile shape exists (A/B runs). */
+int blrqr_debug_gemm_impl(int impl);
+/* The reference's tiled task DAG (scheduler.py:173-201: nodes in sweep order
+ * tiled_sequential_tasks :127-138, edges last writer -> any later touch and
+ * readers since the last write -> the next writer over the read/write sets of
+ * _tiled_access :109-124).  tasks_host: blrqr_tiled_task_count(p, q) tasks
+ * (kind 0 DiagQR, 1 ApplyBlock, 2 UpdateQR, 3 ApplyTrap); successor CSR in
+ * succ_off_host / succ_host.  Returns the edge count (call with
+ * tasks_host = NULL to size), -1 bad shape, -2 max_edges too small. */
+int64_t blrqr_tiled_ref_dag(int p, int q, blrqr_task* tasks_host, int64_t* succ_off_host, int* succ_host,
+                            int64_t max_edges);
 int blrqr_tiled_dag(int p, int q, blrqr_task* tasks_host, int* indeg_host, int64_t* succ_off_host,
                     int* succ_host, int* prio_host);
 int blrqr_tiled_run_dag(const blrqr_grid* g, const blrqr_refl* rf, int ntasks, const blrqr_task* tasks_dev,

@@ -39,6 +39,10 @@ CONFIGS = {
     "C3": Config("C3", "expcov", 32768, 512, 1e-8, ("tiled-hh",)),
     "C4": Config("C4", "invpoisson", 16384, 256, 1e-10, ("mgs", "blocked-hh", "tiled-hh")),
     "C5": Config("C5", "laplace", 65536, 1024, 1e-8, ("tiled-hh",)),
+    # C5 at reduced n: same family, b = 1024 and eps as C5, a 16 x 16 grid the
+    # unmodified reference factorizes in minutes (parity pin for the b = 1024
+    # code paths: 1024^2 GEQRT, b = 1024 TPQRT / RRQR, cap < b slabs)
+    "C5s": Config("C5s", "laplace", 16384, 1024, 1e-8, ("tiled-hh",)),
 }
 
 

@@ -80,7 +80,10 @@ _SIGS = {
                            _P, _P], _I),
     "blrqr_debug_jacobi": ([_I, _I, _P, _P, _P, _P, _I, _P, _L, _I, _P, _P, _P], _I),
     "blrqr_debug_gemm": ([_I, _I, _I, _I, _I, _P, _I, _P, _I, _P, _I, _I, _I, _P], _I),
+    "blrqr_debug_gemm_impl": ([_I], _I),
+    "blrqr_panel_team": ([_I, _I, _I, _P, _P, _P, _P, _P, _P, _L, _I, _P, _P, _P], _I),
     "blrqr_tiled_dag": ([_I, _I, _P, _P, _P, _P, _P], _I),
+    "blrqr_tiled_ref_dag": ([_I, _I, _P, _P, _P, _L], _L),
     "blrqr_tiled_run_dag": ([C.POINTER(Grid), C.POINTER(Refl), _I, _P, _P, _P, _P, _P, _P, _D, _P, _L, _I, _D, _P,
                              _P, _P], _I),
     "blrqr_blocked_step": ([C.POINTER(Grid), C.POINTER(Refl), _I, _D, _P, _P, _P, _L, _P, _L, _I, _P, _P, _P], _I),
@@ -204,6 +207,10 @@ class Runtime:
             raise RuntimeError("dynamic scheduler timed out (no ready task); results are invalid")
         if st & ST_BAD_KIND:
             raise ValueError("diagonal blocks must be dense")
+        if st & ST_BAD_ARG:
+            raise RuntimeError("device invariant check failed (ST_BAD_ARG); results are invalid")
+        if st & ST_NONFINITE:
+            raise FloatingPointError("non-finite value produced on the device")
         if st & ST_MGS_COLLAPSE and warn_mgs:
             import warnings
             from .kernels import RankDeficiencyWarning

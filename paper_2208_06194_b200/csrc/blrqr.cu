@@ -148,14 +148,60 @@ __global__ void __launch_bounds__(NT) k_tpqrt(int n, int k, const double* rt, co
     zero_mat(n, n, t, n);
     return;
   }
-  copy_mat(k, n, ab, k, y, k);
-  tpqrt(cx, n, k, rn, n, y, k, t, n);
+  // the factorization's UpdateQR dispatch (tasks.cuh:tp_update_lr) on V = B^T
+  double* V = alloc(cx, (long long)n * k);
+  if (!V) return;
+  transpose_mat(k, n, ab, k, V, n);
+  tp_update_lr(cx, n, k, rn, n, V, n, t);
+  transpose_mat(n, k, V, n, y, k);
   for (int j = threadIdx.x >> 5; j < n; j += NWARP)
     for (int i = threadIdx.x & 31; i < n; i += 32) {
     const long long e = (long long)j * n + i;
     if (i > j) rn[e] = 0.0;
   }
   add_flops(cx, FK_UPDATE_QR, qr_cost(n + k, n) + tgen_cost(n + k, n));
+}
+
+// GEQRT (op 0: m x n a -> y, t, r) or TPQRT (op 1: n x n r_top over a k x n
+// bottom -> r_new, y, t) as ONE task of a multi-CTA launch: the CTA that
+// takes it runs the factorization's own device routine (geqrt_inplace /
+// tp_update_lr, i.e. what DiagQR / UpdateQR run inside the DAG) and every
+// other CTA of the launch joins its team jobs (trailing-update chunks, T
+// builds), so the API call runs at the speed the factorization's critical
+// chain sees.  Results are bitwise independent of the launch size.
+__global__ void __launch_bounds__(NT, CTAS_PER_SM) k_panel_team(int op, int m, int n, const double* a,
+                                                                const double* a2, double* o1, double* o2, double* o3,
+                                                                double* ws, long long wsp, int* status,
+                                                                unsigned long long* flops, TeamCtx* team, int* ctr) {
+  Ctx cx = make_ctx(ws, wsp, status, flops);
+  cx.team = team;
+  team_task_loop(cx, 1, ctr, [&](long long) {
+    if (op == 0) {  // y (m x n), t (n x n), r (n x n)
+      double* A = alloc(cx, (long long)m * n);
+      if (!A) return;
+      copy_mat(m, n, a, m, A, m);
+      geqrt_inplace(cx, m, n, A, m, o1, m, o2, n);
+      for (int j = threadIdx.x >> 5; j < n; j += NWARP)
+        for (int i = threadIdx.x & 31; i < n; i += 32) o3[(long long)j * n + i] = i <= j ? A[i + (long long)j * m] : 0.0;
+      __syncthreads();
+    } else {  // n = top order, m = bottom rows: o1 = r_new, o2 = y (m x n), o3 = t
+      const int k = m;
+      copy_mat(n, n, a, n, o1, n);
+      if (k == 0) {
+        zero_mat(n, n, o3, n);
+        return;
+      }
+      double* V = alloc(cx, (long long)n * k);
+      if (!V) return;
+      transpose_mat(k, n, a2, k, V, n);
+      tp_update_lr(cx, n, k, o1, n, V, n, o3);
+      transpose_mat(n, k, V, n, o2, k);
+      for (int j = threadIdx.x >> 5; j < n; j += NWARP)
+        for (int i = (threadIdx.x & 31) + j + 1; i < n; i += 32) o1[(long long)j * n + i] = 0.0;
+      add_flops(cx, FK_UPDATE_QR, qr_cost(n + k, n) + tgen_cost(n + k, n));
+      __syncthreads();
+    }
+  });
 }
 
 // apply_tp: w = op(T)(c_top + Y^T c_bot); c_top -= w; c_bot -= Y w
@@ -563,6 +609,7 @@ static void init_kernels() {
     smem_optin(k_compress);
     smem_optin(k_dense_to_blr);
     smem_optin(k_geqrt);
+    smem_optin(k_panel_team);
     smem_optin(k_apply_wy);
     smem_optin(k_tpqrt);
     smem_optin(k_apply_tp);
@@ -685,6 +732,23 @@ int blrqr_geqrt(int m, int n, const double* a, double* y, double* t, double* r, 
   if (m < n || n <= 0) return -1;
   INIT_KERNELS();
   k_geqrt<<<1, NT, SMEM_BYTES, as_stream(stream)>>>(m, n, a, y, t, r, ws, ws_doubles, status, flops);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int blrqr_panel_team(int op, int m, int n, const double* a, const double* a2, double* o1, double* o2, double* o3,
+                     double* ws, int64_t ws_per_cta, int nctas, int* status, unsigned long long* flops,
+                     void* stream) {
+  if (op == 0 && (m < n || n <= 0)) return -2;
+  if (op == 1 && (n <= 0 || m < 0)) return -2;
+  if (op != 0 && op != 1) return -1;
+  if (nctas <= 0) return -11;
+  INIT_KERNELS();
+  int* ctr = nullptr;
+  TeamCtx* team = nullptr;
+  if (int e = team_for_launch(as_stream(stream), &team, &ctr)) return e;
+  k_panel_team<<<team ? nctas : 1, NT, SMEM_BYTES, as_stream(stream)>>>(op, m, n, a, a2, o1, o2, o3, ws, ws_per_cta,
+                                                                      status, flops, team, ctr);
   CK(cudaGetLastError());
   return 0;
 }
@@ -841,8 +905,11 @@ int blrqr_tiled_schedule(int p, int q, blrqr_task* tasks_host, int64_t* level_st
 
 // canonical-order task list + successor CSR of the tiled DAG
 // (scheduler.py:173-201 edges: last writer -> any touch, readers -> writer)
+// split = false: the reference's own task set (one ApplyTrap per (k, i, j)),
+// the DAG build_tiled_dag returns; split = true: the device scheduler's DAG
+// with ApplyTrap split three ways over double-buffered w slots.
 static void tiled_dag_host(int p, int q, std::vector<blrqr_task>& tasks, std::vector<int>& indeg,
-                           std::vector<int64_t>& off, std::vector<int>& succ) {
+                           std::vector<int64_t>& off, std::vector<int>& succ, bool split = true) {
   tasks.clear();
   for (int k = 0; k < q; ++k) {
     tasks.push_back({0, k, -1, -1});
@@ -850,6 +917,10 @@ static void tiled_dag_host(int p, int q, std::vector<blrqr_task>& tasks, std::ve
     for (int i = k + 1; i < p; ++i) {
       tasks.push_back({2, k, i, -1});
       for (int j = k + 1; j < q; ++j) {
+        if (!split) {
+          tasks.push_back({3, k, i, j});
+          continue;
+        }
         tasks.push_back({4, k, i, j});  // split ApplyTrap: w
         tasks.push_back({6, k, i, j});  //                   R_kj -= w
         tasks.push_back({5, k, i, j});  //                   A_ij -= Ytilde w
@@ -929,6 +1000,22 @@ int64_t blrqr_tiled_dag_size(int p, int q, int64_t* nedges) {
   tiled_dag_host(p, q, tasks, indeg, off, succ);
   if (nedges) *nedges = (int64_t)succ.size();
   return (int64_t)tasks.size();
+}
+
+int64_t blrqr_tiled_ref_dag(int p, int q, blrqr_task* tasks_host, int64_t* succ_off_host, int* succ_host,
+                            int64_t max_edges) {
+  if (q < 1 || p < q) return -1;
+  std::vector<blrqr_task> tasks;
+  std::vector<int> indeg, succ;
+  std::vector<int64_t> off;
+  tiled_dag_host(p, q, tasks, indeg, off, succ, false);
+  if (tasks_host) {
+    if ((int64_t)succ.size() > max_edges) return -2;
+    std::copy(tasks.begin(), tasks.end(), tasks_host);
+    std::copy(off.begin(), off.end(), succ_off_host);
+    std::copy(succ.begin(), succ.end(), succ_host);
+  }
+  return (int64_t)succ.size();
 }
 
 int blrqr_tiled_dag(int p, int q, blrqr_task* tasks_host, int* indeg_host, int64_t* succ_off_host,
@@ -1157,6 +1244,11 @@ extern "C" int blrqr_debug_jacobi(int rows, int ncols, double* X, double* J, dou
   k_jacobi_probe<<<mode == 2 ? nctas : 1, NT, SMEM_BYTES, as_stream(stream)>>>(rows, ncols, X, J, sigma, perm, mode, ws,
                                                                             ws_per_cta, status, flops, team, ctr);
   CK(cudaGetLastError());
+  return 0;
+}
+
+extern "C" int blrqr_debug_gemm_impl(int impl) {
+  CK(cudaMemcpyToSymbol(g_gemm_impl, &impl, sizeof(int)));
   return 0;
 }
 

@@ -250,9 +250,19 @@ __device__ void zero_mat(int m, int n, double* A, int lda) {
   __syncthreads();
 }
 
+// Static shared scratch of the CTA-level GEMMs (all tile shapes, DMMA double
+// buffers) and of transpose_mat's staging tile: every user is a complete
+// CTA-synchronised call, so they never hold it at the same time.
+constexpr int GEMM_SMEM = 4608;  // doubles (36 KB next to the 180 KB dynamic arena)
+__device__ __forceinline__ double* gemm_smem() {
+  __shared__ __align__(16) double buf[GEMM_SMEM];
+  return buf;
+}
+
 // B = A^T (A is m x n); 32x32 tiles through shared memory
 __device__ void transpose_mat(int m, int n, const double* A, int lda, double* B, int ldb) {
-  __shared__ double tile[32][33];
+  double (*tile)[33] = reinterpret_cast<double (*)[33]>(gemm_smem());
+  __syncthreads();  // the scratch may have just been read by a GEMM's last stage
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int i0 = 0; i0 < m; i0 += 32)
     for (int j0 = 0; j0 < n; j0 += 32) {
@@ -271,11 +281,6 @@ __device__ void transpose_mat(int m, int n, const double* A, int lda, double* B,
 // Shared-memory tiled DFMA; tile shape chosen from N.
 // ---------------------------------------------------------------------------
 
-constexpr int GEMM_SMEM = 2600;  // doubles of shared scratch shared by all GEMM tile shapes
-__device__ __forceinline__ double* gemm_smem() {
-  __shared__ __align__(16) double buf[GEMM_SMEM];
-  return buf;
-}
 
 template <int BM, int BN, int BK, int TY>
 __device__ __noinline__ void gemm_tiled(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, int lda,
@@ -452,8 +457,45 @@ __device__ __noinline__ void gemm_rows(bool ta, bool tb, int M, int N, int K, do
   __syncthreads();
 }
 
+}  // namespace blr
+#include "dmma.cuh"
+namespace blr {
+
+// GEMM implementation selector (debug / A-B runs: blrqr_debug_gemm_impl):
+// 0 = default dispatch, 1 = DFMA paths only (round-1 dispatch), 2 = DMMA
+// wherever a DMMA tile shape applies
+__device__ int g_gemm_impl = 0;
+
+// DMMA tile choice for an M x N output; false when no DMMA shape fits well
+// (N <= 16 with a transposed A: its [m][k] staging does not fit GEMM_SMEM)
+__device__ __forceinline__ bool gemm_dmma_dispatch(bool ta, bool tb, int M, int N, int K, double alpha,
+                                                   const double* A, int lda, const double* B, int ldb, double beta,
+                                                   double* C, int ldc) {
+  if (M >= 96 && N >= 48)
+    gemm_dmma<128, 64, 8, 4>(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else if (M >= 96 && N > 16)
+    gemm_dmma<128, 32, 8, 8>(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else if (M >= 96)
+    gemm_dmma<128, 16, 8, 16>(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else if (M <= 16 && N >= 48)
+    gemm_dmma<16, 128, 8, 1>(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else if (M <= 32 && N >= 48)
+    gemm_dmma<32, 128, 8, 2>(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else
+    gemm_dmma<64, 64, 8, 4>(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  return true;
+}
+
 __device__ __noinline__ void gemm(bool ta, bool tb, int M, int N, int K, double alpha, const double* A, int lda,
                      const double* B, int ldb, double beta, double* C, int ldc) {
+  const int impl = g_gemm_impl;
+  if (impl != 1 && M >= 8 && N >= 8 && K >= 4) {
+    // FP64 tensor cores for everything but the long-K / few-output inner
+    // products (gemm_tn_dot keeps all 16 warps busy on those)
+    const bool dot = ta && !tb && K >= 64 && (long long)M * N <= 4096;
+    if (impl == 2 || (!dot && (long long)M * N * K >= 8192))
+      if (gemm_dmma_dispatch(ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc)) return;
+  }
   if (ta && !tb && M > 0 && N > 0 && K >= 64 && (long long)M * N <= 4096) {
     gemm_tn_dot(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
     return;

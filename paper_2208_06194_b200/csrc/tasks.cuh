@@ -135,6 +135,32 @@ __device__ void tiled_block(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, 
   tiled_block_op(cx, g, rf, g, k, j, true);
 }
 
+// TPQRT of [R; V^T] with the bottom given transposed (V: b x r, ldv) -- the
+// low-rank UpdateQR (factorize.py:398-411 -> kernels.py:131-155).  On exit R
+// holds R_new, V holds Y^T and T the full b x b T.  The same dispatch serves
+// the DAG task and the blrqr_tpqrt API entry, so the API parity tests run the
+// exact device code the factorization runs (register variants for short
+// bottoms, the team-capable panel TPQRT otherwise).
+__device__ void tp_update_lr(Ctx& cx, int b, int r, double* R, int ldr, double* V, int ldv, double* T) {
+  if (r <= 16 && b <= NT) {
+    tpqrt_small<16, 1>(cx, b, r, R, ldr, V, ldv, T, b);  // B^T = V in place -> Y^T
+  } else if (r <= 16 && b <= 2 * NT) {
+    tpqrt_small<16, 2>(cx, b, r, R, ldr, V, ldv, T, b);
+  } else if (r <= 32 && b <= NT) {
+    tpqrt_small<32, 1>(cx, b, r, R, ldr, V, ldv, T, b);
+  } else {
+    const long long mark = cx.top;
+    double* B = alloc(cx, (long long)r * b);
+    double* S = alloc(cx, (long long)b * b);
+    double* tau = alloc(cx, b);
+    if (!B || !S || !tau) return;
+    transpose_mat(b, r, V, ldv, B, r);          // B = V^T (r x b)
+    tpqrt_team(cx, b, r, R, ldr, B, r, T, b, S, tau);
+    transpose_mat(r, b, B, r, V, ldv);          // Y^T back into the V slab
+    cx.top = mark;
+  }
+}
+
 __device__ void tiled_update(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf, int k, int i) {
   const int b = g.b;
   Cell rk = grid_cell(g, k, k);
@@ -149,21 +175,7 @@ __device__ void tiled_update(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf,
     if (r == 0) {  // tp_qr with an empty bottom: identity reflector (kernels.py:146-147)
       zero_mat(b, b, T, b);
     } else {
-      if (r <= 16 && b <= NT) {
-        tpqrt_small<16, 1>(cx, b, r, rk.u, rk.ld, x.v, x.ld, T, b);  // B^T = V in place -> Y^T
-      } else if (r <= 16 && b <= 2 * NT) {
-        tpqrt_small<16, 2>(cx, b, r, rk.u, rk.ld, x.v, x.ld, T, b);
-      } else if (r <= 32 && b <= NT) {
-        tpqrt_small<32, 1>(cx, b, r, rk.u, rk.ld, x.v, x.ld, T, b);
-      } else {
-        double* B = alloc(cx, (long long)r * b);
-        double* S = alloc(cx, (long long)b * b);
-        double* tau = alloc(cx, b);
-        if (!B || !S || !tau) return;
-        transpose_mat(b, r, x.v, x.ld, B, r);          // B = V_ik^T (r x b)
-        tpqrt_team(cx, b, r, rk.u, rk.ld, B, r, T, b, S, tau);
-        transpose_mat(r, b, B, r, x.v, x.ld);          // Ytilde.v = Y^T stored in the V slab
-      }
+      tp_update_lr(cx, b, r, rk.u, rk.ld, x.v, x.ld, T);
       add_flops(cx, FK_UPDATE_QR, qr_cost(b + r, b) + tgen_cost(b + r, b));
     }
     if (threadIdx.x == 0) { rf.yrank[c] = r; *x.rank = 0; }
@@ -243,13 +255,19 @@ __device__ void tiled_trap_a1(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf
   double* wu = rf.wpool + cw * rf.wslot;
   double* wv = wu + rf.wslot / 2;
   if (w.lr) {
-    if ((long long)b * w.rank > rf.wslot / 2) set_status(cx, ST_RANK_OVERFLOW);
-    copy_mat(b, w.rank, w.u, w.ldu, wu, b);
-    copy_mat(b, w.rank, w.v, w.ldv, wv, b);
-    if (threadIdx.x == 0) rf.wrank[cw] = w.rank;
+    // never write past the slot: an overflowing rank is flagged (harvest
+    // raises) and the copy is clamped to what the slot holds
+    const int fit = (int)min((long long)w.rank, (long long)(rf.wslot / 2 / b));
+    if (fit < w.rank) set_status(cx, ST_RANK_OVERFLOW);
+    copy_mat(b, fit, w.u, w.ldu, wu, b);
+    copy_mat(b, fit, w.v, w.ldv, wv, b);
+    if (threadIdx.x == 0) rf.wrank[cw] = fit;
   } else {
-    if ((long long)b * b > rf.wslot) set_status(cx, ST_RANK_OVERFLOW);
-    copy_mat(b, b, w.u, w.ldu, wu, b);
+    if ((long long)b * b > rf.wslot) {
+      set_status(cx, ST_RANK_OVERFLOW);
+    } else {
+      copy_mat(b, b, w.u, w.ldu, wu, b);
+    }
     if (threadIdx.x == 0) rf.wrank[cw] = -1;
   }
   if (w.s != 1.0) set_status(cx, ST_BAD_ARG);  // w inherits ssum's unit scale

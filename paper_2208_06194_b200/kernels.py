@@ -75,10 +75,12 @@ def qr_compact_wy(a: np.ndarray):
         raise ValueError(f"panel must be tall: got {m} x {n}")
     rt = _lib.runtime()
     y, t, r = _buf(m * n), _buf(n * n), _buf(n * n)
-    ws, per, _ = rt.workspace(max(m, 64), n, m)
+    ws, per, nct = rt.workspace(max(m, 64), n, m)
     ad = _dev(a)  # keep operands alive until the (async) launch has consumed them
-    _lib.check(rt.lib.blrqr_geqrt(m, n, ad.data_ptr(), y.data_ptr(), t.data_ptr(), r.data_ptr(), ws, per,
-                                  rt.status.data_ptr(), rt.flops.data_ptr(), _lib.stream_ptr()), "geqrt")
+    # the tiled DiagQR routine on a CTA team (blrqr_panel_team op 0)
+    _lib.check(rt.lib.blrqr_panel_team(0, m, n, ad.data_ptr(), None, y.data_ptr(), t.data_ptr(), r.data_ptr(), ws,
+                                       per, nct, rt.status.data_ptr(), rt.flops.data_ptr(), _lib.stream_ptr()),
+               "geqrt")
     rt.harvest()
     return WYReflector(_host(y, m, n), _host(t, n, n)), _host(r, n, n)
 
@@ -125,11 +127,12 @@ def tp_qr(r_top: np.ndarray, a_bot: np.ndarray):
         return TPReflector(np.zeros((0, n)), np.zeros((n, n))), r_top.copy()
     rt = _lib.runtime()
     rn, y, t = _buf(n * n), _buf(k * n), _buf(n * n)
-    ws, per, _ = rt.workspace(max(n, k, 64), n, n + k)
+    ws, per, nct = rt.workspace(max(n, k, 64), n, n + k)
     rtd, abd = _dev(r_top), _dev(a_bot)
-    _lib.check(rt.lib.blrqr_tpqrt(n, k, rtd.data_ptr(), abd.data_ptr(), rn.data_ptr(),
-                                  y.data_ptr(), t.data_ptr(), ws, per, rt.status.data_ptr(), rt.flops.data_ptr(),
-                                  _lib.stream_ptr()), "tpqrt")
+    # the tiled UpdateQR routine on a CTA team (blrqr_panel_team op 1)
+    _lib.check(rt.lib.blrqr_panel_team(1, k, n, rtd.data_ptr(), abd.data_ptr(), rn.data_ptr(), y.data_ptr(),
+                                       t.data_ptr(), ws, per, nct, rt.status.data_ptr(), rt.flops.data_ptr(),
+                                       _lib.stream_ptr()), "tpqrt")
     rt.harvest()
     return TPReflector(_host(y, k, n), _host(t, n, n)), _host(rn, n, n)
 

@@ -85,7 +85,8 @@ def res_orth_device(f, a_dense: torch.Tensor, chunk: int = 8192) -> tuple[float,
     for c0 in range(0, n, chunk):
         c1 = min(n, c0 + chunk)
         # columns c0:c1 of Q R are rows c0:c1 of (Q R)^T = R^T[c0:c1] @ Q^T
-        qr_t = rt_[c0:c1] @ qt
+        # R^T is n x m for a tall grid (m > n): only its first n columns meet Q^T
+        qr_t = rt_[c0:c1, :n] @ qt
         num += torch.sum((qr_t - a_dense[:, c0:c1].T) ** 2)
         g = qt[c0:c1] @ qt.T
         g[:, c0:c1].diagonal().sub_(1.0)

@@ -9,10 +9,11 @@ identical factorizations, exactly like the reference's bitwise guarantee
 (scheduler.py:1-11).  ``threads`` is accepted for API compatibility and
 ignored; ``BLRQR_THREADS`` likewise.
 
-The tiled DAG itself (``build_tiled_dag``, scheduler.py:173-201) is built
-here on the host with the reference's read/write sets so callers can inspect
-it; the device path uses the C++ level scheduler of libblrqr.so, which
-derives levels from the same sets.
+The tiled DAG itself (``build_tiled_dag``, scheduler.py:173-201) comes from
+libblrqr.so (``blrqr_tiled_ref_dag``): the C++ builder that also derives the
+device schedules, run on the reference's task set; this module only wraps
+its CSR arrays in the reference's ``Task`` / ``TaskDag`` containers so
+callers can inspect it (DOT output, levels, edge sets).
 """
 
 from __future__ import annotations
@@ -20,6 +21,8 @@ from __future__ import annotations
 import enum
 import os
 from dataclasses import dataclass, field
+
+import numpy as np
 
 from .core import BlrMatrix
 from .factorize import FactorizationResult, _host_entry
@@ -73,28 +76,34 @@ class Task:
         return f"{self.kind.value}({','.join(str(c) for c in (self.k, self.i, self.j) if c >= 0)})"
 
 
-def _access(t: Task):
-    k, i, j = t.k, t.i, t.j
-    if t.kind is TaskKind.DIAG_QR:
-        return [("A", k, k)], [("A", k, k), ("D", k, k)]
-    if t.kind is TaskKind.APPLY_BLOCK_REFLECTOR:
-        return [("D", k, k), ("A", k, j)], [("A", k, j)]
-    if t.kind is TaskKind.UPDATE_QR:
-        return [("A", k, k), ("A", i, k)], [("A", k, k), ("A", i, k), ("U", i, k)]
-    if t.kind is TaskKind.APPLY_TRAP_REFLECTOR:
-        return [("U", i, k), ("A", k, j), ("A", i, j)], [("A", k, j), ("A", i, j)]
-    raise ValueError(f"not a tiled task: {t}")
+_KINDS = (TaskKind.DIAG_QR, TaskKind.APPLY_BLOCK_REFLECTOR, TaskKind.UPDATE_QR, TaskKind.APPLY_TRAP_REFLECTOR)
+
+
+def _ref_dag_arrays(p: int, q: int):
+    """(tasks[n, 4] int32 (kind, k, i, j), succ_off[n + 1], succ[e]) from libblrqr."""
+    from . import _lib
+    lib = _lib.load()
+    n = int(lib.blrqr_tiled_task_count(p, q))
+    if n < 0:
+        raise ValueError("need p >= q >= 1")
+    ne = int(lib.blrqr_tiled_ref_dag(p, q, None, None, None, 0))
+    tasks = np.zeros((n, 4), dtype=np.int32)
+    off = np.zeros(n + 1, dtype=np.int64)
+    succ = np.zeros(max(ne, 1), dtype=np.int32)
+    rc = lib.blrqr_tiled_ref_dag(p, q, tasks.ctypes.data, off.ctypes.data, succ.ctypes.data, ne)
+    if rc != ne:
+        raise RuntimeError("tiled DAG build failed")
+    return tasks, off, succ[:ne]
+
+
+def _task(row) -> Task:
+    kind, k, i, j = (int(x) for x in row)
+    return Task(_KINDS[kind], k=k, i=i, j=j)
 
 
 def tiled_sequential_tasks(p: int, q: int) -> list[Task]:
-    out = []
-    for k in range(q):
-        out.append(Task(TaskKind.DIAG_QR, k=k))
-        out += [Task(TaskKind.APPLY_BLOCK_REFLECTOR, k=k, j=j) for j in range(k + 1, q)]
-        for i in range(k + 1, p):
-            out.append(Task(TaskKind.UPDATE_QR, k=k, i=i))
-            out += [Task(TaskKind.APPLY_TRAP_REFLECTOR, k=k, i=i, j=j) for j in range(k + 1, q)]
-    return out
+    """Sweep order of the tiled method (scheduler.py:127-138)."""
+    return [_task(r) for r in _ref_dag_arrays(p, q)[0]]
 
 
 @dataclass
@@ -134,26 +143,14 @@ class TaskDag:
 
 
 def build_tiled_dag(p: int, q: int) -> TaskDag:
-    """Edges from last-writer / readers-since conflicts in sweep order."""
+    """scheduler.py:173-201: edges from last-writer / readers-since conflicts in
+    sweep order, built by libblrqr's C++ DAG builder."""
     if not 1 <= q <= p:
         raise ValueError("need p >= q >= 1")
-    nodes = tiled_sequential_tasks(p, q)
-    edges = set()
-    writer, readers = {}, {}
-    for t, task in enumerate(nodes):
-        rd, wr = _access(task)
-        for cell in set(rd) | set(wr):
-            w = writer.get(cell)
-            if w is not None and w != t:
-                edges.add((w, t))
-        for cell in wr:
-            edges.update((r, t) for r in readers.get(cell, ()) if r != t)
-        for cell in wr:
-            writer[cell] = t
-            readers[cell] = []
-        for cell in rd:
-            if cell not in wr:
-                readers.setdefault(cell, []).append(t)
+    tasks, off, succ = _ref_dag_arrays(p, q)
+    nodes = [_task(r) for r in tasks]
+    src = np.repeat(np.arange(len(nodes), dtype=np.int64), np.diff(off))
+    edges = set(zip(src.tolist(), succ.astype(np.int64).tolist()))
     return TaskDag(nodes, edges)
 
 

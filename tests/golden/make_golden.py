@@ -332,15 +332,23 @@ def run_full(name, methods=None):
         g = np.random.default_rng(5).standard_normal((n, 8))
         sk = np.zeros((n, 8))
         fro = np.zeros((p, p))
+        sig3 = np.full((p, p, 3), np.nan)  # smallest 3 singular values of each LR block (tie proofs)
         for i in range(p):
             for j in range(p):
-                d = rcore.block_to_dense(res.r.blocks[i][j])
+                blk = res.r.blocks[i][j]
+                d = rcore.block_to_dense(blk)
                 sk[i * b:(i + 1) * b] += d @ g[j * b:(j + 1) * b]
                 fro[i, j] = np.linalg.norm(d)
+                if rcore.is_lowrank(blk) and blk.rank:
+                    ru = np.linalg.qr(blk.u)[1]
+                    rv = np.linalg.qr(blk.v)[1]
+                    s = np.linalg.svd(ru @ rv.T, compute_uv=False)[::-1][:3]
+                    sig3[i, j, :len(s)] = s
         out[f"{m}_ranks"] = np.array([[blk.rank if rcore.is_lowrank(blk) else -1
                                        for blk in row] for row in res.r.blocks])
         out[f"{m}_sketch"] = sk
         out[f"{m}_fro"] = fro
+        out[f"{m}_sig3"] = sig3
         out[f"{m}_radd_hist"] = np.array([[k[0], k[1], v] for k, v in sorted(hist.items())])
         summary["methods"][m] = {"factorize_s": tf, "flops": fl,
                                  "flops_total": int(sum(fl.values()))}

@@ -68,3 +68,18 @@ def test_no_cpu_fallback_without_gpu(lib):
     with pytest.raises(RuntimeError):
         pk.rounded_add(pk.LowRankBlock(np.eye(4)[:, :1], np.ones((4, 1))),
                        pk.LowRankBlock(np.eye(4)[:, :1], np.ones((4, 1))), pk.ToleranceConfig(1e-8))
+
+
+@pytest.mark.parametrize("pq", ["1x1", "2x2", "3x3", "4x4", "6x4"])
+def test_build_tiled_dag_matches_reference(lib, pq):
+    """scheduler.build_tiled_dag (a wrapper over libblrqr's C++ builder) gives
+    exactly the reference's nodes and edges (kat.json, written by the
+    unmodified reference's build_tiled_dag, scheduler.py:173-201)."""
+    import json
+    from conftest import GOLDEN
+    from paper_2208_06194_b200.scheduler import build_tiled_dag
+    kat = json.load(open(os.path.join(GOLDEN, "kat.json")))[f"dag_{pq}"]
+    p, q = (int(x) for x in pq.split("x"))
+    dag = build_tiled_dag(p, q)
+    assert [str(t) for t in dag.nodes] == kat["nodes"]
+    assert sorted([list(e) for e in dag.edges]) == kat["edges"]

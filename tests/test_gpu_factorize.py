@@ -370,3 +370,34 @@ def test_edge_cases_match_reference(pk, case, method):
     assert np.abs(gr - z[f"{case}_{method}_ranks"]).max() <= 1
     ft = int(z[f"{case}_{method}_flops"])
     assert abs(pflops.total() - ft) <= 0.01 * ft
+
+
+@pytest.mark.parametrize("method", ["mgs", "blocked-hh", "tiled-hh"])
+def test_metrics_tall_grid(pk, method):
+    """compute_metrics on a tall grid (p > q): the GPU Res/Orth equal a host
+    evaluation of the reference formulas (metrics.py:69-109 uses
+    blr_to_dense(result.r)[:n, :]) on the same factorization."""
+    from paper_2208_06194_b200 import metrics as pm
+    from paper_2208_06194_b200.scheduler import execute_sequential
+    z = np.load(os.path.join(GOLDEN, "edge_cases.npz"))
+    eps = float(z["eps"])
+    m, n, b = (int(x) for x in z["tall_shape"])
+    pre = "tall_a_"
+    ranks = z[pre + "ranks"]
+    blocks = [[pk.LowRankBlock(z[f"{pre}u_{i}_{j}"], z[f"{pre}v_{i}_{j}"]) if ranks[i, j] >= 0
+               else z[f"{pre}d_{i}_{j}"] for j in range(n // b)] for i in range(m // b)]
+    a = pk.BlrMatrix(pk.BlrStructure(m, n, b, z[pre + "adm"].copy()), blocks)
+    dense = pk.blr_to_dense(a)
+    res = execute_sequential(method, a, pk.ToleranceConfig(eps))
+    rep = pm.compute_metrics(dense, res, eps)
+    r = pk.blr_to_dense(res.r)[:n, :]
+    if method == "mgs":
+        q = pk.blr_to_dense(res.q_explicit)[:, :n]
+    else:
+        fn = pk.factorize.tiled_apply_q if method == "tiled-hh" else pk.factorize.blocked_apply_q
+        q = fn(res, np.eye(m)[:, :n], False)
+    hres = np.linalg.norm(q @ r - dense) / np.linalg.norm(dense)
+    horth = np.linalg.norm(q.T @ q - np.eye(n)) / np.sqrt(n)
+    assert abs(rep.res - hres) <= 1e-3 * hres + 1e-15, (rep.res, hres)
+    assert abs(rep.orth - horth) <= 1e-3 * horth + 1e-15, (rep.orth, horth)
+    assert rep.res <= 10 * eps
