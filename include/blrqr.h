@@ -231,6 +231,10 @@ int blrqr_debug_gemm_impl(int impl);
  * (kind 0 DiagQR, 1 ApplyBlock, 2 UpdateQR, 3 ApplyTrap); successor CSR in
  * succ_off_host / succ_host.  Returns the edge count (call with
  * tasks_host = NULL to size), -1 bad shape, -2 max_edges too small. */
+/* Identifier of the knobs blrqr_tiled_dag bakes into its prio array
+ * (blrqr_set_dag_rings policy, blrqr_set_teams slack); cache DAG arrays on
+ * (p, q, this value). */
+int64_t blrqr_dag_policy(void);
 int64_t blrqr_tiled_ref_dag(int p, int q, blrqr_task* tasks_host, int64_t* succ_off_host, int* succ_host,
                             int64_t max_edges);
 int blrqr_tiled_dag(int p, int q, blrqr_task* tasks_host, int* indeg_host, int64_t* succ_off_host,

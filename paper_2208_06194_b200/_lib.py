@@ -84,6 +84,7 @@ _SIGS = {
     "blrqr_panel_team": ([_I, _I, _I, _P, _P, _P, _P, _P, _P, _L, _I, _P, _P, _P], _I),
     "blrqr_tiled_dag": ([_I, _I, _P, _P, _P, _P, _P], _I),
     "blrqr_tiled_ref_dag": ([_I, _I, _P, _P, _P, _L], _L),
+    "blrqr_dag_policy": ([], _L),
     "blrqr_tiled_run_dag": ([C.POINTER(Grid), C.POINTER(Refl), _I, _P, _P, _P, _P, _P, _P, _D, _P, _L, _I, _D, _P,
                              _P, _P], _I),
     "blrqr_blocked_step": ([C.POINTER(Grid), C.POINTER(Refl), _I, _D, _P, _P, _P, _L, _P, _L, _I, _P, _P, _P], _I),
@@ -139,7 +140,12 @@ def stream_ptr() -> int:
 
 
 class Runtime:
-    """Per-process device state: workspace arena, status word, flop counters."""
+    """Per-process device state: workspace arena, status word, flop counters.
+
+    One stream at a time: the per-CTA workspace, the status word and the flop
+    counters are process-wide, so two factorizations must not run
+    concurrently on different streams (the CTA-team tables inside libblrqr
+    are per (device, stream), but these buffers are not)."""
 
     def __init__(self):
         self.dev = require_cuda()

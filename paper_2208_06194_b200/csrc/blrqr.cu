@@ -629,7 +629,9 @@ static int g_dag_rings = DAG_RINGS;  // 2: the kind-based two-ring policy
 static int g_team_slack = 1 << 20;  // DAG tasks with unit-weight slack <= this may form teams (all by default: measured best)
 
 // Team-job table + ticket ring + two task counters, one per (device, stream)
-// so concurrent launches on different streams never share them; allocated
+// so concurrent launches on different streams never share them (the host
+// Runtime's per-CTA workspace / status / flop buffers are process-wide, so
+// the Python layer runs one stream at a time); allocated
 // once, reset (stream-ordered) before every launch that uses them.  Returns
 // the TeamCtx (nullptr when teams are disabled) and the counter pair.
 static int team_for_launch(cudaStream_t st, TeamCtx** team, int** ctr) {
@@ -978,6 +980,9 @@ void blrqr_set_teams(int enable) {
   if (enable > 1) g_team_slack = enable - 2;  // tuning: enable = 2 + max slack (1 << 20: every task)
 }
 void blrqr_set_dag_rings(int policy) { g_dag_rings = policy == 2 ? 2 : DAG_RINGS; }
+// the knobs blrqr_tiled_dag bakes into the prio array (ready-ring policy and
+// team-eligibility slack): callers caching DAG arrays key them on this
+int64_t blrqr_dag_policy(void) { return ((int64_t)g_dag_rings << 32) | (int64_t)(uint32_t)g_team_slack; }
 void blrqr_set_team_reserve(int nctas) { g_team_reserve = std::max(0, nctas); }
 int blrqr_set_qrcp_tol(double tol) {
   if (!(tol >= 1.0 && tol < 1e8)) return -1;
@@ -1083,8 +1088,14 @@ int blrqr_tiled_run_dag(const blrqr_grid* g, const blrqr_refl* rf, int ntasks, c
   CK(cudaGetLastError());
   cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev);
   const long long timeout_cycles = (long long)(timeout_s * clk_khz * 1e3);
-  k_tiled_dag<<<nctas, NT, SMEM_BYTES, st>>>(d, *g, *rf, eps, ws, ws_per_cta, status, flops, timeout_cycles);
-  CK(cudaGetLastError());
+  // The persistent scheduler spins on work released by other CTAs, so all
+  // nctas CTAs must be co-resident: a cooperative launch guarantees it (or
+  // fails with cudaErrorCooperativeLaunchTooLarge instead of deadlocking).
+  double* ws_arg = ws;
+  int64_t wsp_arg = ws_per_cta;
+  void* args[] = {&d, const_cast<blrqr_grid*>(g), const_cast<blrqr_refl*>(rf), &eps, &ws_arg, &wsp_arg, &status,
+                  &flops, const_cast<long long*>(&timeout_cycles)};
+  CK(cudaLaunchCooperativeKernel((const void*)k_tiled_dag, dim3(nctas), dim3(NT), args, SMEM_BYTES, st));
   return 0;
 }
 

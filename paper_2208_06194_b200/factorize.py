@@ -64,8 +64,9 @@ class FactorizationResult:
 
 
 @lru_cache(maxsize=16)
-def tiled_dag_arrays(p: int, q: int):
-    """(tasks[n,4], indeg[n], succ_off[n+1], succ[e], prio[n]) of the tiled DAG
+def tiled_dag_arrays(p: int, q: int, policy: int = 0):
+    """(tasks[n,4], indeg[n], succ_off[n+1], succ[e], prio[n]) of the tiled DAG (policy =
+    blrqr_dag_policy(): part of the cache key because prio depends on the knobs)
     (same read/write-set edges as scheduler.py:173-201), from libblrqr."""
     lib = _lib.load()
     ne = C.c_int64(0)
@@ -131,7 +132,8 @@ class DeviceFactorization:
             self.nlevels = len(self.levels) - 1
             if scheduler == "dag":
                 self.rf.enable_split_traps()
-                key = (self.g.p, self.g.q)
+                # prio bakes in the ring / team knobs: key the cache on them too
+                key = (self.g.p, self.g.q, int(self.rt.lib.blrqr_dag_policy()))
                 dev = self.rt.dev
                 if key not in self.rt.dag_cache:  # read-only device copy of the DAG, once per shape
                     dt, ind, off, succ, prio = tiled_dag_arrays(*key)

@@ -401,3 +401,54 @@ def test_metrics_tall_grid(pk, method):
     assert abs(rep.res - hres) <= 1e-3 * hres + 1e-15, (rep.res, hres)
     assert abs(rep.orth - horth) <= 1e-3 * horth + 1e-15, (rep.orth, horth)
     assert rep.res <= 10 * eps
+
+
+def test_foreign_containers_duck_typed(pk):
+    """A BlrMatrix built from another package's block class (the reference's
+    LowRankBlock is such a class: core.py:31-66; is_lowrank there is an
+    isinstance check) factorizes unchanged: DeviceGrid.from_host duck-types
+    u / v factors, and the result is bitwise the one from this package's
+    containers."""
+    from dataclasses import dataclass
+    from paper_2208_06194_b200.scheduler import execute_sequential
+
+    @dataclass
+    class ForeignLR:
+        u: np.ndarray
+        v: np.ndarray
+
+        @property
+        def rank(self):
+            return self.u.shape[1]
+
+        @property
+        def rows(self):
+            return self.u.shape[0]
+
+        @property
+        def cols(self):
+            return self.v.shape[0]
+
+    @dataclass
+    class ForeignMatrix:
+        structure: object
+        blocks: list
+
+        @property
+        def p(self):
+            return self.structure.p
+
+        @property
+        def q(self):
+            return self.structure.q
+
+    z, meta, dense = _input("lap512")
+    n, b, eps = meta["n"], meta["b"], meta["eps"]
+    g = schedule.dense_to_blr(dense, b, oblr.weak_map(n // b, n // b), eps)
+    ours = _to_pkg(pk, g)
+    foreign = ForeignMatrix(ours.structure, [[ForeignLR(x.u, x.v) if pk.is_lowrank(x) else x for x in row]
+                                             for row in ours.blocks])
+    cfg = pk.ToleranceConfig(eps)
+    r1 = pk.blr_to_dense(execute_sequential("tiled-hh", ours, cfg).r)
+    r2 = pk.blr_to_dense(execute_sequential("tiled-hh", foreign, cfg).r)
+    assert np.array_equal(r1, r2)
