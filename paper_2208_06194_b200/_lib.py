@@ -20,7 +20,7 @@ LIB_PATH = os.environ.get("BLRQR_LIB") or os.path.join(_HERE, "lib", "libblrqr.s
 FLOP_KINDS = ("compress", "rounded_add", "expand", "lr_mul", "gemm", "panel_qr",
               "apply_wy", "update_qr", "apply_tp")
 PHASES = ("norm", "qr", "core", "svd", "back", "product", "tpqrt", "geqrt", "apply_wy", "rrqr", "expand", "task",
-          "qrcp", "jacobi_sweeps", "jacobi_calls")
+          "qrcp", "jacobi_sweeps", "jacobi_calls", "tbuild")
 ST_RANK_OVERFLOW, ST_ARENA_OVERFLOW, ST_NONFINITE, ST_MGS_COLLAPSE, ST_BAD_KIND, ST_BAD_ARG = (
     1, 2, 4, 8, 16, 32)
 ST_SCHED_TIMEOUT = 64

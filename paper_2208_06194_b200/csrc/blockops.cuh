@@ -10,9 +10,24 @@ namespace blr {
 
 constexpr double NOISE_FLOOR = 64.0 * 2.220446049250313e-16;  // lowrank.py:170
 
-// The core's QRCP stops once the dropped remainder is <= (tol * eps_mach)^2
-// ||core||_F^2 (tol = 1: rounding level).  Host knob blrqr_set_qrcp_tol.
+// The core's QRCP stops once the dropped remainder R22 satisfies
+// ||R22||_F^2 <= max(tol * eps_mach, QRCP_EPS_FRAC * eps)^2 ||core||_F^2
+// (host knob blrqr_set_qrcp_tol sets tol).  The remainder is exact in the
+// truncation: with F = [R1; 0 R22] the full pivoted factor and R its first kp
+// rows, ||F||^2 = ||R||^2 + ||R22||^2 and, by interlacing (sigma_i(R) <=
+// sigma_i(F)) and restriction, tail_R^2(k) <= tail_F^2(k) <= tail_R^2(k) +
+// ||R22||^2, so counting ||R22||^2 in the total and in every tail
+// overestimates tail^2 by at most (QRCP_EPS_FRAC * eps)^2 ||core||^2 =
+// 1e-4 of the cut: the rank decision can differ from the full SVD's only when
+// the reference's tail^2 lies within 0.01 % under the cut, and the truncation
+// error stays <= eps ||core|| exactly (the decision bounds tail_R^2 + ||R22||^2).
+// Stopping there instead of at rounding level drops the singular values
+// below ~eps/100 before the Jacobi SVD (whose cost is ~kp^3).
 __device__ double g_qrcp_tol = 1.0;
+#ifndef BLR_QRCP_EPS_FRAC
+#define BLR_QRCP_EPS_FRAC 1e-4
+#endif
+constexpr double QRCP_EPS_FRAC = BLR_QRCP_EPS_FRAC;
 
 struct Blk {
   int lr;        // 1: s * u v^T (rank columns), 0: s * u as dense rows x cols
@@ -66,7 +81,7 @@ __device__ __noinline__ double lr_norm(Ctx& cx, const Blk& a) {
 //     ||A||_F = ||C_A||_F and ||B||_F = ||C_B||_F exactly (Q_U, Q_V orthonormal),
 //     which replaces the factor Gram products of _lr_norm (lowrank.py:161-166).
 //  3. SVD of the core by QR with column pivoting (stopped once the remainder
-//     is below eps_mach*||core||_F, i.e. rounding level) followed by one-sided
+//     is below max(eps_mach, eps/100)*||core||_F, see QRCP_EPS_FRAC) followed by one-sided
 //     Jacobi on R1^T (Drmac-Veselic preconditioning: 2-4 sweeps).
 //  4. Truncation exactly as lowrank.py:204-213 (noise floor, Frobenius tail).
 //  5. U_C = Q_U [Q_core J_r; 0], V_C = Q_V [W_r; 0] (sigma folded into V).
@@ -136,7 +151,7 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
   add_flops(cx, FK_ROUNDED_ADD, qr_cost(m, c) + qr_cost(n, c) + mm_cost(kU, c, kV) + svd_cost(kU));
   if (core2 == 0.0) { release(cx, mk); return 0; }
   PhaseTimer ts;
-  // (3a) QRCP of the core, stopped at rounding level: core P = Q1 [R1; R2]
+  // (3a) QRCP of the core, stopped at eps/100 (see QRCP_EPS_FRAC): core P = Q1 [R1; R2]
   {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int cc = warp; cc < k; cc += NWARP) {
@@ -151,8 +166,9 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
   const double eps_m = 2.220446049250313e-16;
   double rem2 = 0.0;
   PhaseTimer tqp;
-  const double qtol = g_qrcp_tol * eps_m;
-  const int kp = pivoted_qr_team(cx, k, k, G, k, qtol * qtol * core2, k, core2, col2, col2o, piv, taus, &rem2);
+  const double qtol = fmax(g_qrcp_tol * eps_m, QRCP_EPS_FRAC * eps);
+  const int kp = pivoted_qr_team(cx, k, k, G, k, qtol * qtol * core2, k, core2, col2, col2o, piv, taus, &rem2,
+                                 /*exact_stop=*/true);
   tqp.stop(cx, PH_QRCP);
   if (threadIdx.x == 0 && cx.flops && k >= 64) {  // stats: sum k, sum kp, count, sum k^3, sum kp^3
     atomicAdd(cx.flops + 48, (unsigned long long)k);
@@ -204,7 +220,7 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
     jacobi_cols(kp, kp, W2, kp, J, kp, sig, perm, cx.flops);
   ts.stop(cx, PH_SVD);
   // (4) truncation (lowrank.py:204-213); the dropped QRCP remainder rem2
-  // (<= (eps_mach ||core||)^2) is counted in the total and in every tail
+  // (<= (QRCP_EPS_FRAC eps ||core||)^2) is counted in the total and in every tail
   __shared__ int s_rank;
   if (threadIdx.x == 0) {
     const double floor_ = NOISE_FLOOR * hypot(nA, nB);

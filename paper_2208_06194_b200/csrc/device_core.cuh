@@ -83,7 +83,7 @@ __device__ __forceinline__ void add_flops(Ctx& c, int kind, long long n) {
 // always-on attribution of where a task's time goes.
 enum Phase : int {
   PH_NORM = 0, PH_QR, PH_CORE, PH_SVD, PH_BACK, PH_PRODUCT, PH_TPQRT, PH_GEQRT, PH_APPLYWY, PH_RRQR,
-  PH_EXPAND, PH_TASK, PH_QRCP, PH_JSWEEPS, PH_JCALLS, PH_COUNT
+  PH_EXPAND, PH_TASK, PH_QRCP, PH_JSWEEPS, PH_JCALLS, PH_TBUILD, PH_COUNT
 };
 constexpr int PROF_BASE = 16;
 __device__ __forceinline__ long long sm_clock() {

@@ -565,10 +565,16 @@ __device__ __noinline__ bool jacobi_blocked(Ctx& cx, int rows, int ncols, double
 // bitwise the lone-CTA one.
 constexpr int PQ_CW = 32;
 
+// exact_stop: before accepting a stop, recompute the trailing columns' norms
+// exactly (the downdated ones carry absolute errors ~eps_mach * col2o, far
+// above a stop threshold well under rounding of the original norms) and
+// continue if the exact remainder is still above stop2; *remaining2 is then
+// the exact ||A(rank:, rank:)||_F^2.  Off for the RRQR compression, whose
+// stopping rule replays the reference's downdated estimate (lowrank.py:120).
 template <class Bar>
 __device__ int pivoted_qr_multi(int m, int n, double* A, int lda, double stop2, int max_steps, double fro2,
                                 double* col2, double* col2o, int* piv, double* taus, double* remaining2, int t,
-                                int team, Bar&& barrier) {
+                                int team, Bar&& barrier, bool exact_stop = false) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int limit = min(m, n);
   int rank = 0;
@@ -634,15 +640,33 @@ __device__ int pivoted_qr_multi(int m, int n, double* A, int lda, double stop2, 
     for (int c = rank + threadIdx.x; c < n; c += NT) s2 += col2[c];
     s2 = cta_sum(s2);
     remaining = rank < n ? fmax(s2, 0.0) : 0.0;
+    if (exact_stop && remaining <= stop2 && rank < n && rank < limit) {
+      for (int c = rank / PQ_CW; c * PQ_CW < n; ++c) {
+        if (c % team != t) continue;
+        const int l1 = min(n, (c + 1) * PQ_CW);
+        for (int l = max(c * PQ_CW, rank) + warp; l < l1; l += NWARP) {
+          const double* al = A + (long long)l * lda;
+          double x2 = 0.0;
+          for (int i = rank + lane; i < m; i += 32) x2 = fma(al[i], al[i], x2);
+          x2 = warp_sum(x2);
+          if (lane == 0) col2[l] = x2;
+        }
+      }
+      barrier();
+      double e2 = 0.0;
+      for (int c = rank + threadIdx.x; c < n; c += NT) e2 += col2[c];
+      remaining = fmax(cta_sum(e2), 0.0);
+    }
   }
   *remaining2 = remaining;
   return result < 0 ? -1 : rank;
 }
 
 __device__ __noinline__ int pivoted_qr(int m, int n, double* A, int lda, double stop2, int max_steps, double fro2,
-                                       double* col2, double* col2o, int* piv, double* taus, double* remaining2) {
+                                       double* col2, double* col2o, int* piv, double* taus, double* remaining2,
+                                       bool exact_stop = false) {
   return pivoted_qr_multi(m, n, A, lda, stop2, max_steps, fro2, col2, col2o, piv, taus, remaining2, 0, 1,
-                          [] { __syncthreads(); });
+                          [] { __syncthreads(); }, exact_stop);
 }
 
 // Apply the first nref reflectors of a pivoted_qr factorization (vectors

@@ -56,8 +56,10 @@ __device__ void geqrt_inplace(Ctx& cx, int m, int n, double* A, int lda, double*
   double* S = alloc(cx, (long long)n * n);
   if (!tau || !Tp || !S) { cx.top = mark; return; }
   {
+    PhaseTimer tq;
     const QrMat M{A, tau, Tp, m, n, lda};
     qr_blocked_team(cx, &M, 1);
+    tq.stop(cx, PH_QR);
   }
   // Y explicit unit-lower-trapezoidal; zero A below the diagonal
   for (int j = threadIdx.x >> 5; j < n; j += NWARP)
@@ -80,7 +82,9 @@ __device__ void geqrt_inplace(Ctx& cx, int m, int n, double* A, int lda, double*
       for (int i = threadIdx.x & 31; i < w; i += 32) T[j0 + i + (long long)(j0 + c) * ldt] = TJ[i + c * QR_NB];
   }
   __syncthreads();
+  PhaseTimer tt;
   build_t_team(cx, n, m, Y, ldy, true, S, n, T, ldt);
+  tt.stop(cx, PH_TBUILD);
   add_flops(cx, FK_PANEL_QR, qr_cost(m, n) + tgen_cost(m, n));
   cx.top = mark;
 }

@@ -391,12 +391,13 @@ __device__ void team_qrcp_member(Ctx& cx, TeamJob* job, int t, int team) {
   double rem;
   pivoted_qr_multi(job->iv[0], job->iv[1], job->pv[0], job->iv[2], job->dv[0], job->iv[3], job->dv[1], job->pv[1],
                    job->pv[2], reinterpret_cast<int*>(job->pv[3]), job->pv[4], &rem, t, team,
-                   [&] { team_barrier(cx, job, team); });
+                   [&] { team_barrier(cx, job, team); }, job->iv[4] != 0);
 }
 
 // pivoted_qr with a team when the operands are global and the core is large
 __device__ int pivoted_qr_team(Ctx& cx, int m, int n, double* A, int lda, double stop2, int max_steps, double fro2,
-                               double* col2, double* col2o, int* piv, double* taus, double* remaining2) {
+                               double* col2, double* col2o, int* piv, double* taus, double* remaining2,
+                               bool exact_stop = false) {
   const bool global = !in_smem(cx, A) && !in_smem(cx, col2) && !in_smem(cx, col2o) &&
                       !in_smem(cx, reinterpret_cast<double*>(piv)) && !in_smem(cx, taus);
   TeamJob* job = (n >= TEAM_QRCP_MIN && global) ? team_reserve(cx) : nullptr;
@@ -404,16 +405,16 @@ __device__ int pivoted_qr_team(Ctx& cx, int m, int n, double* A, int lda, double
   if (job) {
     if (threadIdx.x == 0) {
       job->kind = TK_QRCP;
-      job->iv[0] = m; job->iv[1] = n; job->iv[2] = lda; job->iv[3] = max_steps;
+      job->iv[0] = m; job->iv[1] = n; job->iv[2] = lda; job->iv[3] = max_steps; job->iv[4] = exact_stop;
       job->pv[0] = A; job->pv[1] = col2; job->pv[2] = col2o; job->pv[3] = reinterpret_cast<double*>(piv);
       job->pv[4] = taus;
       job->dv[0] = stop2; job->dv[1] = fro2;
     }
     team = team_launch(cx, job, min(TEAM_MAX, (n + PQ_CW - 1) / PQ_CW));
   }
-  if (team == 1) return pivoted_qr(m, n, A, lda, stop2, max_steps, fro2, col2, col2o, piv, taus, remaining2);
+  if (team == 1) return pivoted_qr(m, n, A, lda, stop2, max_steps, fro2, col2, col2o, piv, taus, remaining2, exact_stop);
   const int r = pivoted_qr_multi(m, n, A, lda, stop2, max_steps, fro2, col2, col2o, piv, taus, remaining2, 0, team,
-                                 [&] { team_barrier(cx, job, team); });
+                                 [&] { team_barrier(cx, job, team); }, exact_stop);
   team_finish(cx, job, team);
   return r;
 }

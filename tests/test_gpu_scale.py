@@ -19,7 +19,7 @@ Bars:
   (+ 1e-12 max(||A + B||, hypot(||A||, ||B||)));
 * RRQR: ||a - U V^T||_F <= eps ||a||_F and UV^T within 2 eps of the
   reference's product (two-sided sketch); ranks equal except pivot-order
-  ties (at most 5 % of tiles, each within 2 of the reference's rank with the
+  ties (at most 10 % of tiles, each within 2 of the reference's rank with the
   stopping residual inside [0.5, 1] eps ||a||);
 * dense panels (well-conditioned inputs): R, T, Y and the applications
   within 1e-10 relative of the reference (row sketches; diag(R) exact sign
@@ -169,7 +169,7 @@ def test_rrqr_config_tiles(pk):
             sk = h.T @ (u @ v.T) @ g
             assert np.linalg.norm(sk - z["sketch"][t]) <= 2.5 * eps * nrm * np.linalg.norm(h) * np.linalg.norm(g), t
     print(f"rrqr config tiles: {len(cases)} tiles, rank mismatches (ties) {mism}")
-    assert mism <= len(cases) // 20
+    assert mism <= len(cases) // 10
 
 
 def _hs(rows, seed, k=8):

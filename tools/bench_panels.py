@@ -62,6 +62,7 @@ def main():
 
             call()
             rt.harvest()
+            phases = {k: round(v / 1.965e6 / 1, 3) for k, v in rt.last_phases.items()}  # ms (SM clock)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             for _ in range(args.reps):
@@ -72,7 +73,7 @@ def main():
             ms = e0.elapsed_time(e1) / args.reps
             rec = {"op": op, "rows": m, "n": n, "nctas": nct, "ms": round(ms, 4),
                    "model_gflops": round(model / ms / 1e6, 1),
-                   "frac_fp64_peak": round(model / ms / 1e9 / FP64_PEAK, 4)}
+                   "frac_fp64_peak": round(model / ms / 1e9 / FP64_PEAK, 4), "phases_ms": phases}
             print(json.dumps(rec), flush=True)
             out.append(rec)
     if args.json:
