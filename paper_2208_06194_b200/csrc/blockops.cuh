@@ -197,27 +197,35 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
     const QrMat mx{X, tau2, Tp2, k, kp, k};
     qr_blocked_team(cx, &mx, 1);
   }
-  // W2 and J both in shared memory (jacobi_smem) or both in the global arena,
-  // leaving the shared arena to the block Jacobi's staging (jb = 16 columns)
-  const Mark before_w = mark(cx);
+  // One-sided Jacobi on the columns of W2 = R2^T (kp x kp, lower
+  // triangular): W2 V = U_hat Sigma, and core = Q1 [R2^T Q2^T; 0] (X = Q2 R2,
+  // R1 = R2^T Q2^T P^T), so the core's left singular vectors are
+  // Q1 [U_hat; 0] -- the normalized rotated columns themselves -- and its
+  // sigma-scaled right vectors need no accumulated rotations: core^T Q1
+  // [U_hat_r; 0] = Q2 R2 U_hat_r, one triangular GEMM after the sweeps
+  // (the orthogonal projection of the core onto the kept left subspace, i.e.
+  // the truncated SVD; backward stable in absolute terms).  Dropping V halves
+  // the rotation work and the storage, so cores up to kp ~ 150 sweep in
+  // shared memory (jacobi_smem) instead of block pairs staged from L2.
+  // Same sweep counts as Jacobi on R2 (measured on the config-scale cores).
   double* W2 = salloc(cx, (long long)kq * kq);
-  double* J = W2 ? salloc(cx, (long long)kq * kq) : nullptr;
-  if (!J) {
-    release(cx, before_w);
-    W2 = alloc(cx, (long long)kq * kq);
-    J = alloc(cx, (long long)kq * kq);
-  }
+  if (!W2) W2 = alloc(cx, (long long)kq * kq);
+  double* R2c = alloc(cx, (long long)kq * kq);  // R2 (upper, zero below) for the right-vector GEMM
   double* sig = alloc_fast(cx, kq);
   int* perm = reinterpret_cast<int*>(alloc_fast(cx, kq));
-  if (!W2 || !J || !sig || !perm) { release(cx, mk); return 0; }
+  if (!W2 || !R2c || !sig || !perm) { release(cx, mk); return 0; }
   for (int j = threadIdx.x >> 5; j < kp; j += NWARP)
-    for (int i = threadIdx.x & 31; i < kp; i += 32) W2[i + (long long)j * kp] = i <= j ? X[i + (long long)j * k] : 0.0;
+    for (int i = threadIdx.x & 31; i < kp; i += 32) {
+      const double r = i <= j ? X[i + (long long)j * k] : 0.0;  // R2(i, j)
+      R2c[i + (long long)j * kp] = r;
+      W2[j + (long long)i * kp] = r;  // W2 = R2^T
+    }
   __syncthreads();
-  if (in_smem(cx, W2) && in_smem(cx, J) && kp <= JAC_SMEM_MAXC)
-    jacobi_smem(cx, kp, kp, W2, J, sig, perm, cx.flops);  // shared-space loads, 2 pairs per warp
-  else if (kp <= 32 || (!team_jacobi_lead(cx, kp, kp, W2, kp, J, kp, sig, perm) &&
-                        !jacobi_blocked(cx, kp, kp, W2, kp, J, kp, sig, perm, cx.flops)))
-    jacobi_cols(kp, kp, W2, kp, J, kp, sig, perm, cx.flops);
+  if (in_smem(cx, W2) && kp <= JAC_SMEM_MAXC)
+    jacobi_smem(cx, kp, kp, W2, nullptr, sig, perm, cx.flops);  // shared-space loads, 2 pairs per warp
+  else if (kp <= 32 || (!team_jacobi_lead(cx, kp, kp, W2, kp, nullptr, kp, sig, perm) &&
+                        !jacobi_blocked(cx, kp, kp, W2, kp, nullptr, kp, sig, perm, cx.flops)))
+    jacobi_cols(kp, kp, W2, kp, nullptr, kp, sig, perm, cx.flops);
   ts.stop(cx, PH_SVD);
   // (4) truncation (lowrank.py:204-213); the dropped QRCP remainder rem2
   // (<= (QRCP_EPS_FRAC eps ||core||)^2) is counted in the total and in every tail
@@ -259,12 +267,17 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
     double* ZV = alloc(cx, (long long)n * rank);
     double* Z2 = alloc(cx, (long long)k * rank);
     if (!ZU || !ZV || !Z2) { release(cx, mk); return 0; }
-    // core = Q1 [J; 0] Sigma (Q2 W2hat)^T P^T: left vectors Q1 [J_r; 0],
-    // right (scaled by sigma) Q2 [W2_r; 0]
+    // left vectors Q1 [U_hat_r; 0] (normalized rotated columns of W2, in
+    // descending sigma order), right (scaled by sigma) Q2 [R2 U_hat_r; 0]
+    for (int j = threadIdx.x >> 5; j < rank; j += NWARP) {
+      const double inv = 1.0 / sig[perm[j]];  // kept sigma > noise floor > 0
+      for (int i = threadIdx.x & 31; i < m; i += 32)
+        ZU[(long long)j * m + i] = i < kp ? W2[i + (long long)perm[j] * kp] * inv : 0.0;
+    }
+    __syncthreads();
+    gemm(false, false, kp, rank, kp, 1.0, R2c, kp, ZU, m, 0.0, Z2, k);
     for (int j = threadIdx.x >> 5; j < rank; j += NWARP)
-      for (int i = threadIdx.x & 31; i < m; i += 32) ZU[(long long)j * m + i] = i < kp ? J[i + (long long)perm[j] * kp] : 0.0;
-    for (int j = threadIdx.x >> 5; j < rank; j += NWARP)
-      for (int i = threadIdx.x & 31; i < k; i += 32) Z2[(long long)j * k + i] = i < kp ? W2[i + (long long)perm[j] * kp] : 0.0;
+      for (int i = kp + (threadIdx.x & 31); i < k; i += 32) Z2[(long long)j * k + i] = 0.0;
     __syncthreads();
     // fixed 32-column chunks (team.cuh back_chunk), so a team computes the
     // same bits as a lone CTA

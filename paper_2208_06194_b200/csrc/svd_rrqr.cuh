@@ -18,10 +18,11 @@ __device__ __noinline__ void jacobi_cols(int rows, int ncols, double* X, int ldx
                                          int* perm, unsigned long long* prof = nullptr) {
   __shared__ int s_rot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int j = threadIdx.x >> 5; j < ncols; j += NWARP)
-    for (int i = threadIdx.x & 31; i < ncols; i += 32) {
-    J[i + (long long)j * ldj] = (i == j) ? 1.0 : 0.0;
-  }
+  if (J)  // J == nullptr: rotations are not accumulated (left vectors only)
+    for (int j = threadIdx.x >> 5; j < ncols; j += NWARP)
+      for (int i = threadIdx.x & 31; i < ncols; i += 32) {
+      J[i + (long long)j * ldj] = (i == j) ? 1.0 : 0.0;
+    }
   __syncthreads();
   const double tol = 2.220446049250313e-16 * (double)max(rows, 1);
   const double tol2 = tol * tol;
@@ -64,7 +65,7 @@ __device__ __noinline__ void jacobi_cols(int rows, int ncols, double* X, int ldx
         }
         double* jp = J + (long long)p * ldj;
         double* jq = J + (long long)q * ldj;
-        for (int i = lane; i < ncols; i += 32) {
+        for (int i = lane; J && i < ncols; i += 32) {
           const double x = jp[i], y = jq[i];
           jp[i] = c * x - s * y;
           jq[i] = s * x + c * y;
@@ -344,9 +345,10 @@ __device__ __noinline__ void jacobi_smem(const Ctx& cx, int rows, int ncols, dou
   __shared__ int s_rot;
   __shared__ double s_jn[JAC_SMEM_MAXC];  // tracked squared column norms
   double* X = as_smem(cx, xs_);
-  double* J = as_smem(cx, js_);
+  double* J = js_ ? as_smem(cx, js_) : nullptr;  // nullptr: no rotation accumulation
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int j = warp; j < ncols; j += NWARP)
+  const int nj = J ? ncols : 0;
+  for (int j = warp; j < nj; j += NWARP)
     for (int i = lane; i < ncols; i += 32) J[i + j * ncols] = (i == j) ? 1.0 : 0.0;
   __syncthreads();
   const double tol = 2.220446049250313e-16 * (double)max(rows, 1);
@@ -394,7 +396,7 @@ __device__ __noinline__ void jacobi_smem(const Ctx& cx, int rows, int ncols, dou
         if (r1) jac_note_cos2(a1, b1, g1, lane);
         if (r0) {
           jac_rotate(X + p0 * rows, X + q0 * rows, rows, lane, c0, s0);
-          jac_rotate(J + p0 * ncols, J + q0 * ncols, ncols, lane, c0, s0);
+          jac_rotate(J + p0 * nj, J + q0 * nj, nj, lane, c0, s0);
           double a = a0, b = b0;
           if (!jac_norm_update(a, b, t0, g0)) {
             double gg;
@@ -407,7 +409,7 @@ __device__ __noinline__ void jacobi_smem(const Ctx& cx, int rows, int ncols, dou
         }
         if (r1) {
           jac_rotate(X + p1 * rows, X + q1 * rows, rows, lane, c1, s1);
-          jac_rotate(J + p1 * ncols, J + q1 * ncols, ncols, lane, c1, s1);
+          jac_rotate(J + p1 * nj, J + q1 * nj, nj, lane, c1, s1);
           double a = a1, b = b1;
           if (!jac_norm_update(a, b, t1, g1)) {
             double gg;
@@ -449,9 +451,10 @@ __device__ __noinline__ void jacobi_smem(const Ctx& cx, int rows, int ncols, dou
   __syncthreads();
 }
 
-// shared-memory doubles one block-pair step needs (X and J staging)
-__device__ __forceinline__ long long jac_pair_smem(int jb, int rows, int ncols) {
-  return (long long)2 * jb * (rows + ncols);
+// shared-memory doubles one block-pair step needs (X and J staging; nj = 0
+// when the rotations are not accumulated)
+__device__ __forceinline__ long long jac_pair_smem(int jb, int rows, int nj) {
+  return (long long)2 * jb * (rows + nj);
 }
 
 // One block pair (bi, bj) of the blocked one-sided Jacobi over X (rows x
@@ -468,17 +471,18 @@ __device__ bool jacobi_block_pair(double* X, int ldx, double* J, int ldj, int ro
   const int nc = ni + nj;
   double* Xs = st;
   double* Js = st + 2 * jb * rows;
+  const int jl = J ? ncols : 0;  // J column length (0: rotations not accumulated)
   for (int c = warp; c < nc; c += NWARP) {
     const int gc = c < ni ? bi * jb + c : bj * jb + (c - ni);
     warp_ld_cg(Xs + c * rows, X + (long long)gc * ldx, rows, lane);
-    warp_ld_cg(Js + c * ncols, J + (long long)gc * ldj, ncols, lane);
+    if (J) warp_ld_cg(Js + c * ncols, J + (long long)gc * ldj, ncols, lane);
   }
   __syncthreads();
-  const bool rot = block_pair_sweep(Xs, rows, Js, ncols, nc, tol2);
+  const bool rot = block_pair_sweep(Xs, rows, Js, jl, nc, tol2);
   for (int c = warp; c < nc; c += NWARP) {
     const int gc = c < ni ? bi * jb + c : bj * jb + (c - ni);
     warp_st_cg(X + (long long)gc * ldx, Xs + c * rows, rows, lane);
-    warp_st_cg(J + (long long)gc * ldj, Js + c * ncols, ncols, lane);
+    if (J) warp_st_cg(J + (long long)gc * ldj, Js + c * ncols, ncols, lane);
   }
   __syncthreads();
   return rot;
@@ -497,12 +501,13 @@ __device__ __noinline__ bool jacobi_blocked(Ctx& cx, int rows, int ncols, double
                                             double* sigma, int* perm, unsigned long long* prof = nullptr) {
   __shared__ int s_rot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nj = J ? ncols : 0;
   int jb = 16;
-  while (jb > 2 && jac_pair_smem(jb, rows, ncols) > cx.scap - cx.stop) jb >>= 1;
-  if (jac_pair_smem(jb, rows, ncols) > cx.scap - cx.stop) return false;
+  while (jb > 2 && jac_pair_smem(jb, rows, nj) > cx.scap - cx.stop) jb >>= 1;
+  if (jac_pair_smem(jb, rows, nj) > cx.scap - cx.stop) return false;
   const Mark mk = mark(cx);
-  double* st = as_smem(cx, salloc(cx, jac_pair_smem(jb, rows, ncols)));
-  for (int j = warp; j < ncols; j += NWARP)
+  double* st = as_smem(cx, salloc(cx, jac_pair_smem(jb, rows, nj)));
+  for (int j = warp; j < nj; j += NWARP)
     for (int i = lane; i < ncols; i += 32) J[i + (long long)j * ldj] = (i == j) ? 1.0 : 0.0;
   __syncthreads();
   const double tol = 2.220446049250313e-16 * (double)max(rows, 1);

@@ -214,7 +214,7 @@ __device__ void team_jacobi_member(Ctx& cx, TeamJob* job, int t, int team) {
   double* X = job->pv[0];
   double* J = job->pv[1];
   const Mark mk = mark(cx);
-  double* st = salloc(cx, jac_pair_smem(jb, rows, ncols));
+  double* st = salloc(cx, jac_pair_smem(jb, rows, J ? ncols : 0));
   if (!st) {  // the leader sized jb for its own (fuller) arena; cannot happen
     if (threadIdx.x == 0) atomicOr(cx.status, ST_ARENA_OVERFLOW);
     st = cx.sbase;
@@ -266,16 +266,17 @@ __device__ bool team_jacobi_lead(Ctx& cx, int rows, int ncols, double* X, int ld
                                  int* perm) {
   if (!cx.team || in_smem(cx, X) || in_smem(cx, J)) return false;  // other CTAs need global addresses
   // jacobi_blocked's block size for this arena state
+  const int nj = J ? ncols : 0;  // J == nullptr: rotations not accumulated
   int jb = 16;
-  while (jb > 2 && jac_pair_smem(jb, rows, ncols) > cx.scap - cx.stop) jb >>= 1;
-  if (jac_pair_smem(jb, rows, ncols) > cx.scap - cx.stop) return false;
+  while (jb > 2 && jac_pair_smem(jb, rows, nj) > cx.scap - cx.stop) jb >>= 1;
+  if (jac_pair_smem(jb, rows, nj) > cx.scap - cx.stop) return false;
   const int nb = (ncols + jb - 1) / jb;
   const int want = min(TEAM_MAX, ((nb + 1) & ~1) / 2);
   if (want < 2) return false;
   TeamJob* job = team_reserve(cx);
   if (!job) return false;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int j = warp; j < ncols; j += NWARP)
+  for (int j = warp; j < nj; j += NWARP)
     for (int i = lane; i < ncols; i += 32) J[i + (long long)j * ldj] = (i == j) ? 1.0 : 0.0;
   __syncthreads();
   if (threadIdx.x == 0) {
