@@ -33,7 +33,8 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 FP64_PEAK_TFLOPS = 37.07  # measured DMMA m8n8k4 loop on this pool's B200 (profiles/fp64_peaks_r01.txt)
-FP64_PEAK_SRC = "measured: tools/fp64_peak.cu DMMA loop (MEASURED_PEAKS.json has no FP64 entry)"
+FP64_PEAK_SRC = ("measured on this pool: DMMA m8n8k4 loop, tools/fp64_peak.cu -> profiles/fp64_peaks_r01.txt, "
+                 "tools/dmma_probe.cu -> profiles/dmma_probe_r02.txt (MEASURED_PEAKS.json has no FP64 entry)")
 
 
 def _dist():
@@ -237,6 +238,7 @@ def run_ours(args):
         torch.cuda.synchronize()
     barrier()
     counts = f.finish()
+    lr_bytes_step = rt.last_stats[8] / args.steps  # rounded-addition algorithmic bytes (device counter)
     step_ms = [a.elapsed_time(b) for a, b in ev]
     kern_ms = [a.elapsed_time(b) for a, b in kev]
     # harvest() is called once after K steps: counters summed all K steps;
@@ -264,31 +266,50 @@ def run_ours(args):
     if distributed:
         gflops /= ws_  # value below multiplies by ws_ for replicas; F_step is already the whole job
 
-    # ---- e2e: reference-facing path with HOST buffers -----------------------
+    classes = None
+    if not args.no_classes and not distributed:
+        classes = measure_classes(rt, cfg.b)
+
+    # ---- e2e: the drop-in API call with HOST buffers --------------------------
+    # tiled_householder_qr(a, cfg) (factorize.py:447) on the compressed input
+    # as a host BlrMatrix: H2D of the BLR, the factorization, and the whole
+    # FactorizationResult back on the host (R-tilde plus Q-tilde: the T store
+    # and every Ytilde in one D2H each) -- inside the timed region.
     e2e = None
     if args.e2e_steps > 0 and not distributed:
+        from paper_2208_06194_b200 import factorize as pfac
         host = g0.to_host()  # the compressed BLR as the reference's BlrMatrix (numpy)
-        from paper_2208_06194_b200.device import DeviceGrid as DG
-        # pinned staging prepared once (the caller's host buffers)
+        api = {"tiled-hh": pfac.tiled_householder_qr, "blocked-hh": pfac.blocked_householder_qr,
+               "mgs": pfac.blocked_mgs_qr}[method]
+
+        def nbytes(x):
+            return x.u.nbytes + x.v.nbytes if hasattr(x, "u") else x.nbytes
+
+        res_h = api(host, tol)  # untimed warm-up (pinned host buffers, schedule cache)
+        del res_h
         e2e_ms = []
-        h2d = d2h = 0
         for _ in range(args.e2e_steps):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            gd = DG.from_host(host, pinned=True)
-            fe = DeviceFactorization(method, gd, tol, clone=False)
-            fe.run()
-            r_host = fe.g.to_host()
-            fe.finish()
+            res_h = api(host, tol)
             torch.cuda.synchronize()
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
-            h2d = int(sum(x.u.nbytes + x.v.nbytes if hasattr(x, "u") else x.nbytes for row in host.blocks for x in row))
-            d2h = int(sum(x.u.nbytes + x.v.nbytes if hasattr(x, "u") else x.nbytes for row in r_host.blocks for x in row))
+        h2d = int(sum(nbytes(x) for row in host.blocks for x in row))
+        d2h = int(sum(nbytes(x) for row in res_h.r.blocks for x in row))
+        if res_h.q_tiles is not None:
+            d2h += sum(w.y.nbytes + w.t.nbytes for w in res_h.q_tiles.diag.values())
+            d2h += sum(nbytes(y) + t.nbytes for y, t in res_h.q_tiles.updates.values())
+        elif res_h.q_columns is not None:
+            d2h += sum(c.t.nbytes + sum(nbytes(y) for _, y in c.entries) for c in res_h.q_columns)
+        else:
+            d2h += int(sum(nbytes(x) for row in res_h.q_explicit.blocks for x in row))
+        del res_h
         e_ms = sum(e2e_ms) / len(e2e_ms)
         e2e = {"value": F_step / (e_ms * 1e-3) / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": e_ms,
-               "path": "BlrMatrix (host numpy) -> DeviceGrid.from_host (pinned H2D + unpack kernel) -> "
-                       "factorize -> R to host BlrMatrix (pack kernel + D2H)"}
+               "path": f"paper_2208_06194_b200.factorize.{api.__name__}(host BlrMatrix, cfg): pinned H2D + "
+                       "unpack kernel -> factorization -> FactorizationResult on the host (R-tilde pack + D2H, "
+                       "reflector store and Ytilde factors one D2H each)"}
 
     out_ranks = f.g.rank_map()
     res = {
@@ -323,7 +344,9 @@ def run_ours(args):
                      "peak_source": FP64_PEAK_SRC,
                      "note": "achieved = reference flop model per factorization / CUDA-event time of the "
                              "factorization launches on their stream (clone excluded); FP64 has no tcgen05 "
-                             "path, the bound is the FP64 DMMA/DFMA pipe"},
+                             "path, the bound is the FP64 DMMA pipe (mma.sync m8n8k4, used by every CTA GEMM)",
+                     "whole_run": _whole_run(counts, args.steps, lr_bytes_step, k_ms),
+                     "classes": classes},
         "clocks": clk.summary(),
         "e2e": e2e,
         "impl": "ours",
@@ -339,16 +362,172 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
 
 
+HBM_PEAK_GBS = 6544.7  # MEASURED_PEAKS.json hbm_gbs (copy test, burst)
+
+
+def _qr_cost(h, w):
+    return 2 * h * w * w - (2 * w * w * w) // 3
+
+
+def measure_classes(rt, b, reps=3):
+    """Isolated per-class kernels at the metric config's shapes (SURVEY
+    8(d)(i)/(ii)), timed with CUDA events on the launch stream:
+
+    * dense contractions -- DiagQR (GEQRT b x b) and UpdateQR (TPQRT b over a
+      64-row bottom) through blrqr_panel_team (the DAG's own routines on a
+      CTA team), and the tensor-core CTA GEMM alone (148 CTAs, T_ik^T U
+      shapes b x b x 64): TFLOP/s of the reference flop model / executed
+      GEMM flops against the FP64 DMMA peak;
+    * low-rank updates -- one batched rounded-addition launch (10 pairs per
+      SM) at C3's operand ranks, small (c = 8..30) and large (c = 50..340)
+      cores: GB/s of 8 b (2 r_A + 2 r_B + 2 r_C) bytes per addition against
+      the measured HBM copy bandwidth.
+    """
+    import torch
+    from paper_2208_06194_b200 import _lib
+
+    dev = rt.dev
+    g = torch.Generator(device="cpu").manual_seed(7)
+    out = {}
+
+    def timed(fn):
+        fn()
+        rt.harvest()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        st = rt.harvest()
+        return e0.elapsed_time(e1) / reps, rt.last_stats
+
+    # -- dense class ------------------------------------------------------------
+    a = torch.randn(b * b, dtype=torch.float64, generator=g).to(dev)
+    o1, o2, o3 = (torch.empty(b * b, dtype=torch.float64, device=dev) for _ in range(3))
+    ws, per, nct = rt.workspace(b, b, 2 * b)
+
+    def geqrt():
+        _lib.check(rt.lib.blrqr_panel_team(0, b, b, a.data_ptr(), None, o1.data_ptr(), o2.data_ptr(), o3.data_ptr(),
+                                           ws, per, nct, rt.status.data_ptr(), rt.flops.data_ptr(),
+                                           _lib.stream_ptr()), "geqrt")
+
+    ms, _ = timed(geqrt)
+    fl = _qr_cost(b, b) + b ** 3
+    out["geqrt_diagqr"] = {"shape": f"{b}x{b}", "ms": ms, "tflops": fl / ms / 1e9,
+                           "frac_fp64_peak": fl / ms / 1e9 / FP64_PEAK_TFLOPS, "flops": "model qr+tgen"}
+    kb = 64
+    top = (torch.triu(torch.randn(b, b, dtype=torch.float64, generator=g)) + b ** 0.5 * torch.eye(b, dtype=torch.float64))
+    top = top.T.contiguous().reshape(-1).to(dev)
+    bot = torch.randn(kb * b, dtype=torch.float64, generator=g).to(dev)
+    y = torch.empty(kb * b, dtype=torch.float64, device=dev)
+
+    def tpqrt():
+        _lib.check(rt.lib.blrqr_panel_team(1, kb, b, top.data_ptr(), bot.data_ptr(), o1.data_ptr(), y.data_ptr(),
+                                           o3.data_ptr(), ws, per, nct, rt.status.data_ptr(), rt.flops.data_ptr(),
+                                           _lib.stream_ptr()), "tpqrt")
+
+    ms, _ = timed(tpqrt)
+    fl = _qr_cost(b + kb, b) + (b + kb) * b * b
+    out["tpqrt_updateqr"] = {"shape": f"{b} over {kb} rows", "ms": ms, "tflops": fl / ms / 1e9,
+                             "frac_fp64_peak": fl / ms / 1e9 / FP64_PEAK_TFLOPS, "flops": "model qr+tgen"}
+    nc = 64
+    A = torch.randn(b * b, dtype=torch.float64, generator=g).to(dev)
+    B = torch.randn(b * nc, dtype=torch.float64, generator=g).to(dev)
+    C = torch.empty(b * nc, dtype=torch.float64, device=dev)
+    ctas = rt.nctas
+
+    def gemm():
+        rt.lib.blrqr_debug_gemm(1, 0, b, nc, b, A.data_ptr(), b, B.data_ptr(), b, C.data_ptr(), b, 1, ctas,
+                                _lib.stream_ptr())
+
+    ms, _ = timed(gemm)
+    fl = 2.0 * b * nc * b * ctas
+    out["dmma_gemm_TtU"] = {"shape": f"T^T U {b}x{nc}x{b} on each of {ctas} CTAs", "ms": ms, "tflops": fl / ms / 1e9,
+                            "frac_fp64_peak": fl / ms / 1e9 / FP64_PEAK_TFLOPS, "flops": "executed"}
+
+    # -- low-rank class ---------------------------------------------------------
+    def radd_batch(lo, hi, npairs):
+        keep = []
+        ua, va, ub, vb, uo, vo = ([] for _ in range(6))
+        ra, rb = [], []
+        cap = 0
+        for t in range(npairs):
+            c = int(torch.randint(lo, hi + 1, (1,), generator=g))
+            r1 = max(1, int(c * float(torch.rand(1, generator=g)) * 0.8) + c // 10)
+            r1 = min(r1, c - 1)
+            r2 = c - r1
+            for r, us, vs, rr in ((r1, ua, va, ra), (r2, ub, vb, rb)):
+                q = torch.linalg.qr(torch.randn(b, r, dtype=torch.float64, generator=g))[0]
+                s = 10.0 ** (-8.0 * torch.arange(r, dtype=torch.float64) / max(r - 1, 1))
+                v = torch.linalg.qr(torch.randn(b, r, dtype=torch.float64, generator=g))[0] * s
+                us.append(q.T.contiguous().reshape(-1).to(dev))
+                vs.append(v.T.contiguous().reshape(-1).to(dev))
+                rr.append(r)
+            cap = max(cap, c)
+        for _ in range(npairs):
+            uo.append(torch.empty(b * cap, dtype=torch.float64, device=dev))
+            vo.append(torch.empty(b * cap, dtype=torch.float64, device=dev))
+        ptr = [torch.tensor([x.data_ptr() for x in L], dtype=torch.int64, device=dev) for L in (ua, va, ub, vb, uo, vo)]
+        rat = torch.tensor(ra, dtype=torch.int32, device=dev)
+        rbt = torch.tensor(rb, dtype=torch.int32, device=dev)
+        rot = torch.zeros(npairs, dtype=torch.int32, device=dev)
+        keep += [ua, va, ub, vb, uo, vo]
+        wsr, perr, nctr = rt.workspace(b, cap)
+
+        def run():
+            _lib.check(rt.lib.blrqr_rounded_add_batched(
+                npairs, b, b, ptr[0].data_ptr(), ptr[1].data_ptr(), rat.data_ptr(), ptr[2].data_ptr(),
+                ptr[3].data_ptr(), rbt.data_ptr(), ptr[4].data_ptr(), ptr[5].data_ptr(), rot.data_ptr(), cap, 1e-8,
+                wsr, perr, nctr, rt.status.data_ptr(), rt.flops.data_ptr(), _lib.stream_ptr()), "rounded_add")
+
+        ms, stats = timed(run)
+        byts = stats[8] / (reps)  # 8 b (2 r_A + 2 r_B + 2 r_C), summed over the launch
+        return {"pairs": npairs, "core_c": f"{lo}..{hi}", "ms": ms, "GBps": byts / ms / 1e6,
+                "frac_hbm_peak": byts / ms / 1e6 / HBM_PEAK_GBS, "bytes_per_launch": byts,
+                "us_per_addition_per_sm": ms * 1e3 * ctas / npairs}
+
+    out["rounded_add_small_cores"] = radd_batch(8, 30, 10 * ctas)
+    out["rounded_add_large_cores"] = radd_batch(50, 340, 2 * ctas)
+    return out
+
+
+def _whole_run(counts, steps, lr_bytes, k_ms):
+    """max(F_dense / P_fp64, B_lr / BW) / t_factorize, with
+    F_dense = the dense-contraction model flops (panel QR + T generation,
+    W/Y applications, TPQRT, T_ik^T U products) and B_lr = the rounded
+    additions' algorithmic bytes counted on the device."""
+    dense_kinds = ("panel_qr", "apply_wy", "update_qr", "lr_mul")
+    f_dense = sum(v for k, v in counts.items() if k in dense_kinds) / steps
+    t = k_ms * 1e-3
+    td, tb = f_dense / (FP64_PEAK_TFLOPS * 1e12), lr_bytes / (HBM_PEAK_GBS * 1e9)
+    return {"F_dense_flops": f_dense, "B_lowrank_bytes": lr_bytes, "t_dense_bound_s": td, "t_lowrank_bound_s": tb,
+            "frac": max(td, tb) / t, "bound": "tensor" if td >= tb else "hbm",
+            "note": "the run is latency-bound on its critical chain of small sequential factorizations "
+                    "(tools/critical_path.py), so both class bounds sit far below the factorization time"}
+
+
+def _sources_sha():
+    import hashlib
+    h = hashlib.sha256()
+    d = os.path.join(REPO, "paper_2208_06194_b200", "csrc")
+    for f in sorted(os.listdir(d)):
+        h.update(open(os.path.join(d, f), "rb").read())
+    return h.hexdigest()[:16]
+
+
 def _traffic(args, kernel_name):
     """DRAM bytes (read + write) per launch of the dominant kernel, from the
-    committed ncu --set full capture summary (profiles/ncu_traffic.json)."""
+    committed ncu --set full capture summary (profiles/ncu_traffic.json),
+    used only when that capture was taken on the current kernel sources
+    (sha of paper_2208_06194_b200/csrc); otherwise null."""
     if args.traffic is not None:
         return args.traffic
     try:
         with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as fh:
             d = json.load(fh)
         e = d.get(args.config, {})
-        if e.get("kernel") and kernel_name.startswith(e["kernel"]):
+        if e.get("kernel") and kernel_name.startswith(e["kernel"]) and e.get("csrc_sha16") == _sources_sha():
             return e.get("dram_bytes_per_launch")
     except (OSError, ValueError):
         pass
@@ -402,8 +581,9 @@ def main():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--method", default=None)
     ap.add_argument("--e2e-steps", type=int, default=1)
-    ap.add_argument("--cpu-rows", type=int, default=12)
+    ap.add_argument("--cpu-rows", type=int, default=24)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-classes", action="store_true", help="skip the isolated per-class kernel measurements")
     ap.add_argument("--traffic", type=float, default=None,
                     help="DRAM bytes per launch of the dominant kernel from an ncu --set full capture")
     args = ap.parse_args()

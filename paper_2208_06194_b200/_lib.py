@@ -201,7 +201,7 @@ class Runtime:
         self.flops.zero_()
         counts = {k: int(v) for k, v in zip(FLOP_KINDS, fl) if v}
         self.last_phases = {k: int(v) for k, v in zip(PHASES, fl[16:32]) if v}
-        self.last_stats = fl[48:56].tolist()
+        self.last_stats = fl[48:64].tolist()  # [8]: low-rank-class bytes of the rounded additions
         from . import flops as _fl
         for k, v in counts.items():
             _fl.add(k, v)

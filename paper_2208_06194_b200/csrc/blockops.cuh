@@ -261,6 +261,10 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
     set_status(cx, ST_RANK_OVERFLOW);
     rank = cap;
   }
+  // algorithmic bytes of the low-rank class: every input
+  // factor entry read once, every output factor entry written once
+  if (threadIdx.x == 0 && cx.flops)
+    atomicAdd(cx.flops + 56, (unsigned long long)8 * (unsigned long long)(m + n) * (unsigned long long)(c + rank));
   if (rank > 0) {
     PhaseTimer tb;
     double* ZU = alloc(cx, (long long)m * rank);

@@ -310,6 +310,157 @@ __device__ void qr_blocked_multi(Ctx& cx, const QrMat* mats, int nm, int t, int 
   release(cx, mk);
 }
 
+// ---------------------------------------------------------------------------
+// Two-level GEQRT for large panels (the tiled DiagQR at b = 512 / 1024,
+// kernels.py:87-103): outer panels of QR2_NB = 64 columns -- one CTA-team
+// chunk -- factored by their owner with the 16-column inner panels above
+// (updates confined to the outer panel), their forward T written straight
+// into the diagonal 64-block of the full T; the trailing chunks take ONE
+// block-reflector update per outer panel as three DMMA GEMMs (Y^T A,
+// T^T W, A - Y W with K = 64), so the team synchronises 4x less often than
+// with 16-column panels and the trailing work runs on the FP64 tensor cores.
+// The off-diagonal 64-blocks of T follow from
+//   T(R, J) = -(T(R, R:J0) S(R:J0, J)) T_JJ,  S = Y^T Y (rows >= J0),
+// row chunk R by its owner (rows of T depend only on the same rows of
+// earlier column blocks).  Fixed chunk arithmetic: results are bitwise
+// independent of the team size.
+// ---------------------------------------------------------------------------
+constexpr int QR2_NB = 64;
+static_assert(QR2_NB == QR_CW, "outer panel = one team chunk");
+
+// outer panel [c0, c0 + w) by one CTA: inner panels, explicit Y (rows c0..m-1
+// into Yo, ld m - c0), forward T of the panel into T(c0:c0+w, c0:c0+w)
+__device__ void qr2_factor_outer(Ctx& cx, const QrMat& M, int c0, int w, double* Yo, double* T, int ldt) {
+  const int h = M.m - c0;
+  const Mark mk = mark(cx);
+  {
+    // W small in shared memory; Yb global, leaving the shared arena to the
+    // h x 16 panel staging of qr_factor_panel
+    double* W = alloc_fast(cx, (long long)QR_NB * QR2_NB);
+    double* Yb = alloc(cx, (long long)h * QR_NB);
+    if (!W || !Yb) { release(cx, mk); return; }
+    for (int p0 = c0; p0 < c0 + w; p0 += QR_NB) {
+      const int pw = min(QR_NB, c0 + w - p0);
+      qr_factor_panel(cx, M, p0, pw);
+      if (p0 + pw < c0 + w) {
+        extract_y(M.m, p0, pw, M.A, M.lda, Yb, M.m - p0);
+        qr_panel_apply(M, p0, pw, Yb, p0 + pw, c0 + w, W);
+      }
+    }
+    release(cx, mk);
+  }
+  double* S = alloc_fast(cx, (long long)QR2_NB * QR2_NB);
+  double* X = alloc_fast(cx, (long long)QR2_NB * QR_NB);
+  if (!S || !X) { release(cx, mk); return; }
+  extract_y(M.m, c0, w, M.A, M.lda, Yo, h);
+  // T block: inner T's on the diagonal, zeros below, recurrence above
+  double* TJ = T + c0 + (long long)c0 * ldt;
+  for (int c = threadIdx.x >> 5; c < w; c += NWARP)
+    for (int i = threadIdx.x & 31; i < w; i += 32) {
+      const int pb = (c / QR_NB) * QR_NB;
+      double v = 0.0;
+      if (i >= pb && i < pb + QR_NB) v = i <= c ? M.Tp[(i - pb) + (long long)(c0 + c) * QR_NB] : 0.0;
+      TJ[i + (long long)c * ldt] = v;
+    }
+  __syncthreads();
+  gemm(true, false, w, w, h, 1.0, Yo, h, Yo, h, 0.0, S, QR2_NB);  // S = Yo^T Yo (upper part used)
+  for (int j0 = QR_NB; j0 < w; j0 += QR_NB) {
+    const int jw = min(QR_NB, w - j0);
+    gemm(false, false, j0, jw, jw, 1.0, S + (long long)j0 * QR2_NB, QR2_NB, TJ + j0 + (long long)j0 * ldt, ldt, 0.0, X,
+         QR2_NB);
+    gemm(false, false, j0, jw, j0, -1.0, TJ, ldt, X, QR2_NB, 0.0, TJ + (long long)j0 * ldt, ldt);
+  }
+  release(cx, mk);
+}
+
+// A(c0:m, col0:col1) <- (I - Yo T_JJ Yo^T)^T A(c0:m, col0:col1)
+__device__ void qr2_apply_outer(Ctx& cx, const QrMat& M, int c0, int w, const double* Yo, const double* T, int ldt,
+                                int col0, int col1) {
+  const int h = M.m - c0, n2 = col1 - col0;
+  if (n2 <= 0 || w <= 0) return;
+  const Mark mk = mark(cx);
+  double* W = alloc_fast(cx, (long long)QR2_NB * QR2_NB);
+  double* W2 = alloc_fast(cx, (long long)QR2_NB * QR2_NB);
+  if (!W || !W2) { release(cx, mk); return; }
+  double* A2 = M.A + c0 + (long long)col0 * M.lda;
+  gemm(true, false, w, n2, h, 1.0, Yo, h, A2, M.lda, 0.0, W, QR2_NB);
+  gemm(true, false, w, n2, w, 1.0, T + c0 + (long long)c0 * ldt, ldt, W, QR2_NB, 0.0, W2, QR2_NB);
+  gemm(false, false, h, n2, w, -1.0, Yo, h, W2, QR2_NB, 1.0, A2, M.lda);
+  release(cx, mk);
+}
+
+// The whole GEQRT by member t of a team (lone CTA: t = 0, team = 1):
+// R in A's upper triangle, Y (explicit, m x n, ldy) with A zeroed below the
+// diagonal, full forward T (n x n, ldt).  Ybuf: 2 * m * QR2_NB doubles and
+// S: n x n, both visible to the whole team.
+template <class Bar>
+__device__ void geqrt2_multi(Ctx& cx, const QrMat& M, double* T, int ldt, double* Y, int ldy, double* Ybuf, double* S,
+                             int t, int team, Bar&& barrier) {
+  const int k = min(M.m, M.n);
+  const int nP = (k + QR2_NB - 1) / QR2_NB, nch = (M.n + QR2_NB - 1) / QR2_NB;
+  auto owns = [&](int c) { return c % team == t; };
+  auto ybuf = [&](int P) { return Ybuf + (long long)(P & 1) * M.m * QR2_NB; };
+  if (nP > 0 && owns(0)) qr2_factor_outer(cx, M, 0, min(QR2_NB, k), ybuf(0), T, ldt);
+  barrier();
+  for (int P = 0; P < nP; ++P) {
+    const int c0 = P * QR2_NB, w = min(QR2_NB, k - c0);
+    const double* Yo = ybuf(P);
+    int done = -1;
+    if (P + 1 < nP && owns(P + 1)) {  // look-ahead: the next panel's chunk first, then factor it
+      done = P + 1;
+      qr2_apply_outer(cx, M, c0, w, Yo, T, ldt, (P + 1) * QR2_NB, min(M.n, (P + 2) * QR2_NB));
+      qr2_factor_outer(cx, M, (P + 1) * QR2_NB, min(QR2_NB, k - (P + 1) * QR2_NB), ybuf(P + 1), T, ldt);
+    }
+    for (int c = P + 1; c < nch; ++c)
+      if (c != done && owns(c)) qr2_apply_outer(cx, M, c0, w, Yo, T, ldt, c * QR2_NB, min(M.n, (c + 1) * QR2_NB));
+    barrier();
+  }
+  // explicit Y, A zeroed below the diagonal (own chunks)
+  for (int c = t; c < nch; c += team) {
+    const int j1 = min(M.n, (c + 1) * QR2_NB);
+    for (int j = c * QR2_NB + (threadIdx.x >> 5); j < j1; j += NWARP)
+      for (int i = threadIdx.x & 31; i < M.m; i += 32) {
+        double* a = M.A + i + (long long)j * M.lda;
+        double y;
+        if (i < j) y = 0.0;
+        else if (i == j) y = 1.0;
+        else { y = *a; *a = 0.0; }
+        Y[i + (long long)j * ldy] = y;
+      }
+  }
+  __syncthreads();
+  barrier();
+  // off-diagonal T blocks: S(0:J0, J) by owner of J, then rows of T by owner of R
+  for (int J = 1 + t; J < nP; J += team) {
+    const int j0 = J * QR2_NB, jw = min(QR2_NB, k - j0);
+    gemm(true, false, j0, jw, M.m - j0, 1.0, Y + j0, ldy, Y + j0 + (long long)j0 * ldy, ldy, 0.0,
+         S + (long long)j0 * k, k);
+  }
+  for (int R = t; R < nP; R += team) {  // zero T below the diagonal blocks in own row chunk
+    const int r0 = R * QR2_NB, r1 = min(k, r0 + QR2_NB);
+    for (int c = threadIdx.x >> 5; c < r0; c += NWARP)
+      for (int i = r0 + (threadIdx.x & 31); i < r1; i += 32) T[i + (long long)c * ldt] = 0.0;
+  }
+  __syncthreads();
+  barrier();
+  const Mark mk = mark(cx);
+  double* Z = alloc_fast(cx, (long long)QR2_NB * QR2_NB);
+  if (!Z) return;
+  PhaseTimer tb;
+  for (int J = 1; J < nP; ++J) {
+    const int j0 = J * QR2_NB, jw = min(QR2_NB, k - j0);
+    for (int R = t; R < J; R += team) {
+      const int r0 = R * QR2_NB, rw = QR2_NB;
+      gemm(false, false, rw, jw, j0 - r0, 1.0, T + r0 + (long long)r0 * ldt, ldt, S + r0 + (long long)j0 * k, k,
+           0.0, Z, QR2_NB);
+      gemm(false, false, rw, jw, jw, -1.0, Z, QR2_NB, T + j0 + (long long)j0 * ldt, ldt, 0.0,
+           T + r0 + (long long)j0 * ldt, ldt);
+    }
+  }
+  tb.stop(cx, PH_TBUILD);
+  release(cx, mk);
+}
+
 __device__ __noinline__ void qr_blocked(Ctx& cx, int m, int n, double* A, int lda, double* tau, double* Tp) {
   const QrMat M{A, tau, Tp, m, n, lda};
   qr_blocked_multi(cx, &M, 1, 0, 1, [] { __syncthreads(); });

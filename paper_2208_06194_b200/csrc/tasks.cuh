@@ -49,12 +49,30 @@ __device__ __forceinline__ Blk refl_blk(const blrqr_grid& g, const blrqr_refl& r
 // T full (n x n, ldt), R left in the upper triangle of A (below zeroed).
 // kernels.py:87-103 (dgeqrt with nb = n).
 // ---------------------------------------------------------------------------
+// two-level GEQRT from n = 1024 (C5's DiagQR: 16.5 -> 14 ms on a 17-CTA
+// team); at n = 512 the 16-column path is faster (4.0 vs 5.3 ms), its
+// per-panel look-ahead hides more of the panel latency than 64-wide panels
+#ifndef BLR_GEQRT2_MIN
+#define BLR_GEQRT2_MIN 1024
+#endif
 __device__ void geqrt_inplace(Ctx& cx, int m, int n, double* A, int lda, double* Y, int ldy, double* T, int ldt) {
   const long long mark = cx.top;
   double* tau = alloc(cx, n);
   double* Tp = alloc(cx, (long long)QR_NB * n);
   double* S = alloc(cx, (long long)n * n);
   if (!tau || !Tp || !S) { cx.top = mark; return; }
+  if (m >= n && n >= BLR_GEQRT2_MIN) {  // two-level blocking, DMMA trailing updates (householder.cuh)
+    double* Ybuf = alloc(cx, (long long)2 * m * QR2_NB);
+    if (Ybuf) {
+      PhaseTimer tq;
+      const QrMat M{A, tau, Tp, m, n, lda};
+      geqrt2_team(cx, M, T, ldt, Y, ldy, Ybuf, S);
+      tq.stop(cx, PH_QR);
+      add_flops(cx, FK_PANEL_QR, qr_cost(m, n) + tgen_cost(m, n));
+      cx.top = mark;
+      return;
+    }
+  }
   {
     PhaseTimer tq;
     const QrMat M{A, tau, Tp, m, n, lda};

@@ -61,7 +61,8 @@ constexpr int TEAM_BACK_MIN = BLR_TEAM_BACK_MIN;  // Q_U width from which the ba
 #endif
 constexpr int TEAM_QRCP_MIN = BLR_TEAM_QRCP_MIN;  // core order from which the pivoted QR splits
 
-enum TeamKind : int { TK_JACOBI = 1, TK_BACK = 2, TK_QRB = 3, TK_QRCP = 4, TK_TBUILD = 5, TK_TPQRT = 6, TK_GEMM = 7 };
+enum TeamKind : int { TK_JACOBI = 1, TK_BACK = 2, TK_QRB = 3, TK_QRCP = 4, TK_TBUILD = 5, TK_TPQRT = 6, TK_GEMM = 7,
+                      TK_GEQRT = 8 };
 
 struct __align__(128) TeamJob {
   int state;  // 0 free, 9 being set up, 2 running (team size published)
@@ -386,6 +387,39 @@ __device__ void qr_blocked_team(Ctx& cx, const QrMat* mats, int nm) {
   }
 }
 
+// ---- TK_GEQRT ----------------------------------------------------------------
+// Two-level GEQRT (householder.cuh geqrt2_multi): QR, explicit Y and the full
+// T with one team.  iv: m, n, lda, ldt, ldy; pv: A, tau, Tp, T, Y, Ybuf, S.
+__device__ void team_geqrt_member(Ctx& cx, TeamJob* job, int t, int team) {
+  const QrMat M{job->pv[0], job->pv[1], job->pv[2], job->iv[0], job->iv[1], job->iv[2]};
+  geqrt2_multi(cx, M, job->pv[3], job->iv[3], job->pv[4], job->iv[4], job->pv[5], job->pv[6], t, team,
+               [&] { team_barrier(cx, job, team); });
+}
+
+__device__ void geqrt2_team(Ctx& cx, const QrMat& M, double* T, int ldt, double* Y, int ldy, double* Ybuf,
+                            double* S) {
+  const int nch = (M.n + QR2_NB - 1) / QR2_NB;
+  const bool global = !in_smem(cx, M.A) && !in_smem(cx, M.tau) && !in_smem(cx, M.Tp) && !in_smem(cx, T) &&
+                      !in_smem(cx, Y) && !in_smem(cx, Ybuf) && !in_smem(cx, S);
+  TeamJob* job = (nch >= 2 && global) ? team_reserve(cx) : nullptr;
+  int team = 1;
+  if (job) {
+    if (threadIdx.x == 0) {
+      job->kind = TK_GEQRT;
+      job->iv[0] = M.m; job->iv[1] = M.n; job->iv[2] = M.lda; job->iv[3] = ldt; job->iv[4] = ldy;
+      job->pv[0] = M.A; job->pv[1] = M.tau; job->pv[2] = M.Tp; job->pv[3] = T; job->pv[4] = Y;
+      job->pv[5] = Ybuf; job->pv[6] = S;
+    }
+    team = team_launch(cx, job, min(TEAM_MAX, nch));
+  }
+  if (team > 1) {
+    geqrt2_multi(cx, M, T, ldt, Y, ldy, Ybuf, S, 0, team, [&] { team_barrier(cx, job, team); });
+    team_finish(cx, job, team);
+  } else {
+    geqrt2_multi(cx, M, T, ldt, Y, ldy, Ybuf, S, 0, 1, [] { __syncthreads(); });
+  }
+}
+
 // ---- TK_QRCP -----------------------------------------------------------------
 // iv: m, n, lda, max_steps; pv: A, col2, col2o, piv (int*), taus; dv: stop2, fro2
 __device__ void team_qrcp_member(Ctx& cx, TeamJob* job, int t, int team) {
@@ -636,6 +670,7 @@ __device__ void team_help(Ctx& cx, TeamCtx* tc, int slot, int member) {
     case TK_TBUILD: team_tbuild_member(cx, job, member, team); break;
     case TK_TPQRT: team_tpqrt_member(cx, job, member, team); break;
     case TK_GEMM: team_gemm_member(cx, job, member, team); break;
+    case TK_GEQRT: team_geqrt_member(cx, job, member, team); break;
     default: break;
   }
   __syncthreads();

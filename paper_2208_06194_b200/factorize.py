@@ -214,51 +214,70 @@ class DeviceFactorization:
             return FactorizationResult("tiled-hh", r, q_tiles=self._tiles_host())
         return FactorizationResult("blocked-hh", r, q_columns=self._columns_host())
 
-    def _ytilde(self, i: int, k: int, yr: np.ndarray):
-        """Reflector entry (i, k): LowRankBlock(U_ik, Y_i^T) aliasing the cell's
-        slabs, or the dense Y block (factorize.py:214-224, 404-407)."""
+    # -- reflector download: one D2H of the reflector store and one packed D2H
+    # of the low-rank Ytilde factors; the returned numpy arrays are views into
+    # those (pinned, caching-allocator) host buffers -- no per-tile copies
+    def _host_stores(self):
         g, rf = self.g, self.rf
         b = g.b
-        c = i * g.q + k
-        if yr[c] >= 0:
-            r = int(yr[c])
-            ou, ov = g.off_u_host[c], g.off_v_host[c]
-            u = g.pool[ou:ou + b * r].cpu().numpy().reshape(r, b).T
-            v = g.pool[ov:ov + b * r].cpu().numpy().reshape(r, b).T
-            return LowRankBlock(np.ascontiguousarray(u), np.ascontiguousarray(v))
-        return rf.mat(rf.y_off_host[c], b, b)
+        pool_h = torch.empty(rf.pool.numel(), dtype=torch.float64, pin_memory=True)
+        pool_h.copy_(rf.pool)
+        yr = rf.yrank.cpu().numpy()
+        sel = (yr >= 0) & g.kind_host.ravel()
+        ranks = np.where(sel, yr, 0).astype(np.int32)
+        sz = (2 * b * ranks).astype(np.int64)
+        off = np.zeros_like(sz)
+        off[1:] = np.cumsum(sz)[:-1]
+        tot = int(sz.sum())
+        off_pack = np.where(sel, off, -1)
+        fac_h = torch.empty(max(tot, 1), dtype=torch.float64, pin_memory=True)
+        if tot:
+            dev = g.pool.device
+            stage = torch.empty(tot, dtype=torch.float64, device=dev)
+            rank_t = torch.from_numpy(ranks).to(dev)
+            od = torch.from_numpy(off_pack).to(dev)
+            gs = g.cstruct()
+            gs.rank = rank_t.data_ptr()
+            _lib.check(_lib.load().blrqr_grid_pack(C.byref(gs), stage.data_ptr(), od.data_ptr(), 0,
+                                                   _lib.stream_ptr()), "grid_pack")
+            fac_h.copy_(stage)
+        self._host_bufs = (pool_h, fac_h)  # the views below keep them alive
+        P, F = pool_h.numpy(), fac_h.numpy()
+
+        def mat(o, rows, cols):
+            return P[o:o + rows * cols].reshape(cols, rows).T
+
+        def ytilde(c):
+            if sel[c]:
+                r, o = int(ranks[c]), int(off[c])
+                return LowRankBlock(F[o:o + b * r].reshape(r, b).T, F[o + b * r:o + 2 * b * r].reshape(r, b).T)
+            return mat(int(rf.y_off_host[c]), b, b)
+
+        return mat, ytilde
 
     def _columns_host(self) -> list:
         g, rf = self.g, self.rf
         b = g.b
-        yr = rf.yrank.cpu().numpy()
+        mat, ytilde = self._host_stores()
         cols = []
         for k in range(g.q):
             c = k * g.q + k
-            entries = [(k, rf.mat(rf.y_off_host[c], b, b))]
-            entries += [(i, self._ytilde(i, k, yr)) for i in range(k + 1, g.p)]
-            cols.append(ReflectorColumn(k, entries, rf.mat(rf.t_off_host[c], b, b)))
+            entries = [(k, mat(int(rf.y_off_host[c]), b, b))]
+            entries += [(i, ytilde(i * g.q + k)) for i in range(k + 1, g.p)]
+            cols.append(ReflectorColumn(k, entries, mat(int(rf.t_off_host[c]), b, b)))
         return cols
 
     def _tiles_host(self) -> TileReflectorStore:
         g, rf = self.g, self.rf
         b, p, q = g.b, g.p, g.q
+        mat, ytilde = self._host_stores()
         store = TileReflectorStore()
-        yr = rf.yrank.cpu().numpy()
         for k in range(q):
             c = k * q + k
-            store.diag[k] = WYReflector(rf.mat(rf.y_off_host[c], b, b), rf.mat(rf.t_off_host[c], b, b))
+            store.diag[k] = WYReflector(mat(int(rf.y_off_host[c]), b, b), mat(int(rf.t_off_host[c]), b, b))
             for i in range(k + 1, p):
                 c = i * q + k
-                t = rf.mat(rf.t_off_host[c], b, b)
-                if yr[c] >= 0:
-                    r = int(yr[c])
-                    ou, ov = g.off_u_host[c], g.off_v_host[c]
-                    u = g.pool[ou:ou + b * r].cpu().numpy().reshape(r, b).T
-                    v = g.pool[ov:ov + b * r].cpu().numpy().reshape(r, b).T
-                    store.updates[(i, k)] = (LowRankBlock(np.ascontiguousarray(u), np.ascontiguousarray(v)), t)
-                else:
-                    store.updates[(i, k)] = (rf.mat(rf.y_off_host[c], b, b), t)
+                store.updates[(i, k)] = (ytilde(c), mat(int(rf.t_off_host[c]), b, b))
         return store
 
 

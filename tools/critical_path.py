@@ -77,3 +77,9 @@ if len(sys.argv) > 2:  # full path, one task per line: kind k i j seconds
         for t in path:
             extra = f" r={int(ph[t, 15] * 1.965e9)}" if tasks[t, 0] == 2 else ""
             fh.write(f"{kinds[tasks[t, 0]]} {int(tasks[t, 1])} {int(tasks[t, 2])} {int(tasks[t, 3])} {dur[t]:.5f}{extra}\n")
+# phase breakdown of the longest tasks (seconds of the leader CTA's SM clock)
+top = np.argsort(-dur)[:12]
+print(json.dumps({"top_task_phases_ms": [
+    [kinds[tasks[t, 0]], int(tasks[t, 1]), int(tasks[t, 2]), int(tasks[t, 3]), round(float(dur[t]) * 1e3, 2),
+     {nm: round(float(ph[t, i]) * 1e3, 2) for i, nm in enumerate(_lib.PHASES[:15]) if ph[t, i] > 0 and i not in (13, 14)}]
+    for t in top]}, indent=0))
