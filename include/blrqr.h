@@ -224,6 +224,10 @@ int blrqr_debug_gemm(int ta, int tb, int M, int N, int K, const double* A, int l
  * 0 default dispatch (DMMA FP64 tensor-core tiles where they apply), 1 DFMA
  * tiles only, 2 DMMA wherever a DMMA tile shape exists (A/B runs). */
 int blrqr_debug_gemm_impl(int impl);
+/* Debug tripwire: keep the last guard_doubles of every per-CTA workspace
+ * stride out of the bump arena (callers size ws_per_cta accordingly and fill
+ * the guard with a canary to detect out-of-arena writes).  0 = off. */
+int blrqr_debug_arena_guard(int64_t guard_doubles);
 /* The reference's tiled task DAG (scheduler.py:173-201: nodes in sweep order
  * tiled_sequential_tasks :127-138, edges last writer -> any later touch and
  * readers since the last write -> the next writer over the read/write sets of

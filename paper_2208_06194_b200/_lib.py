@@ -81,6 +81,7 @@ _SIGS = {
     "blrqr_debug_jacobi": ([_I, _I, _P, _P, _P, _P, _I, _P, _L, _I, _P, _P, _P], _I),
     "blrqr_debug_gemm": ([_I, _I, _I, _I, _I, _P, _I, _P, _I, _P, _I, _I, _I, _P], _I),
     "blrqr_debug_gemm_impl": ([_I], _I),
+    "blrqr_debug_arena_guard": ([_L], _I),
     "blrqr_panel_team": ([_I, _I, _I, _P, _P, _P, _P, _P, _P, _L, _I, _P, _P, _P], _I),
     "blrqr_tiled_dag": ([_I, _I, _P, _P, _P, _P, _P], _I),
     "blrqr_tiled_ref_dag": ([_I, _I, _P, _P, _P, _L], _L),
@@ -157,6 +158,8 @@ class Runtime:
         self.nctas = int(self.lib.blrqr_default_ctas())
         self._ws = None
         self._ws_per_cta = 0
+        self.arena_guard = 0
+        self._guard = (0, 0)
         self._pinned = None
         self._pinned_ev = None
         self.dag_cache = {}
@@ -178,16 +181,36 @@ class Runtime:
         ev.record()
         self._pinned_ev = ev
 
+    CANARY = -1.2345678901234567e300
+
     def workspace(self, b: int, cap: int, panel_rows: int = 0, nctas: int | None = None):
-        """(ptr, doubles_per_cta, nctas) — grows the shared arena on demand."""
+        """(ptr, doubles_per_cta, nctas) — grows the shared arena on demand.
+        With an arena guard set (set_arena_guard), every CTA stride ends in a
+        canary-filled zone the device arena never allocates."""
         nctas = nctas or self.nctas
-        per = int(self.lib.blrqr_workspace_doubles(b, cap, panel_rows))
+        per = int(self.lib.blrqr_workspace_doubles(b, cap, panel_rows)) + self.arena_guard
         need = per * nctas
         if self._ws is None or self._ws.numel() < need:
             self._ws = None
             torch.cuda.synchronize()
             self._ws = torch.empty(need, dtype=torch.float64, device=self.dev)
+        if self.arena_guard:
+            self._ws[:need].view(nctas, per)[:, per - self.arena_guard:] = self.CANARY
+            self._guard = (per, nctas)
         return self._ws.data_ptr(), per, nctas
+
+    def set_arena_guard(self, doubles: int) -> None:
+        """Debug tripwire for out-of-arena writes (blrqr_debug_arena_guard)."""
+        torch.cuda.synchronize()
+        self.arena_guard = int(doubles)
+        check(self.lib.blrqr_debug_arena_guard(self.arena_guard), "arena_guard")
+
+    def guards_intact(self) -> bool:
+        """True when every CTA's guard zone of the last workspace still holds the canary."""
+        per, nct = self._guard
+        torch.cuda.synchronize()
+        z = self._ws[:per * nct].view(nct, per)[:, per - self.arena_guard:]
+        return bool((z == self.CANARY).all())
 
     def reset_counters(self):
         self.status.zero_()

@@ -1258,6 +1258,13 @@ extern "C" int blrqr_debug_jacobi(int rows, int ncols, double* X, double* J, dou
   return 0;
 }
 
+extern "C" int blrqr_debug_arena_guard(int64_t guard_doubles) {
+  if (guard_doubles < 0) return -1;
+  long long g = guard_doubles;
+  CK(cudaMemcpyToSymbol(g_arena_guard, &g, sizeof(long long)));
+  return 0;
+}
+
 extern "C" int blrqr_debug_gemm_impl(int impl) {
   CK(cudaMemcpyToSymbol(g_gemm_impl, &impl, sizeof(int)));
   return 0;

@@ -20,10 +20,16 @@ __device__ __forceinline__ Cell grid_cell(const blrqr_grid& g, int i, int j) {
   return x;
 }
 
+// Debug tripwire (blrqr_debug_arena_guard): the last g_arena_guard doubles of
+// every CTA's workspace stride are kept out of the bump arena, so a test can
+// fill them with a canary and detect out-of-arena writes (compute-sanitizer is
+// not available on the GPU pool).
+__device__ long long g_arena_guard = 0;
+
 __device__ __forceinline__ Ctx make_ctx(double* ws, long long ws_per_cta, int* status, unsigned long long* flops) {
   Ctx c;
   c.base = ws + (long long)blockIdx.x * ws_per_cta;
-  c.cap = ws_per_cta;
+  c.cap = ws_per_cta - g_arena_guard;
   c.top = 0;
   c.sbase = dyn_smem;
   c.scap = SMEM_ARENA;

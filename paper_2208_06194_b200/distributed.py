@@ -59,19 +59,32 @@ def level_plan(tasks: np.ndarray, level_start: np.ndarray, world: int, rank: int
     return plan
 
 
-def run_tiled_distributed(store, plan, world: int, rank: int, broadcast) -> None:
+def run_tiled_distributed(store, plan, world: int, rank: int, broadcast, allreduce=None) -> None:
     """Drive the level-synchronous distributed tiled factorization.
 
     store.run(level, tasks)       -- execute this rank's tasks of one level
+    store.level_ranks(refl)       -- optional: int32 tensor, the Ytilde rank of
+                                     each of the level's reflectors this rank
+                                     produced (0 elsewhere); summed over ranks
+                                     (allreduce) and handed back through
+                                     store.set_level_ranks, so every payload
+                                     below is sized by its rank (b * r), not by
+                                     the slab capacity -- one small collective
+                                     and one host read per level
     store.reflector_buffers(t)    -- tensors holding reflector t's payload
                                      (filled on the owner, overwritten elsewhere)
     store.received(t, buffers)    -- unpack on non-owners (no-op when in place)
     broadcast(tensor, src)        -- in-place collective broadcast
+    allreduce(tensor)             -- in-place sum over ranks
     """
     for lv, (own, refl) in enumerate(plan):
         if len(own):
             store.run(lv, own)
         if world > 1:
+            if refl and hasattr(store, "level_ranks"):
+                hdr = store.level_ranks(refl)
+                allreduce(hdr)
+                store.set_level_ranks(refl, hdr)
             for t in refl:
                 src = task_owner(t, world)
                 bufs = store.reflector_buffers(t)
@@ -84,7 +97,13 @@ def run_tiled_distributed(store, plan, world: int, rank: int, broadcast) -> None
 
 class GpuStore:
     """A rank's device grid + reflector store (full-size layout; only the
-    owned columns and the received reflectors are ever touched)."""
+    owned columns and the received reflectors are ever touched).
+
+    Built once per grid shape (schedule, ownership plan and device task list:
+    host work that stays out of any timed region); ``reset`` re-arms it for a
+    new input.  Reflector payloads are sized by rank: the Ytilde ranks of a
+    level are exchanged first (one all-reduce of an int vector), then only
+    b * r columns of U_ik and of Y_i^T travel, not the 2 b cap slabs."""
 
     def __init__(self, grid, cfg, world: int, rank: int):
         from . import _lib
@@ -107,6 +126,31 @@ class GpuStore:
         self.tasks = torch.from_numpy(np.ascontiguousarray(allt, dtype=np.int32)).to(self.rt.dev)
         b, q = grid.b, grid.q
         self.b, self.q = b, q
+        self.world, self.rank = world, rank
+        self._ranks = {}
+
+    def reset(self, grid) -> None:
+        """Re-arm for a new input of the same structure (the schedule, plan and
+        reflector store are reused; the store's contents are rewritten by the run)."""
+        self.g = grid
+        self.rf.grid = grid
+        self.rf.yrank.fill_(-1)
+        self._ranks = {}
+
+    def level_ranks(self, refl):
+        dev = self.rf.yrank.device
+        rk = torch.zeros(len(refl), dtype=torch.int32, device=dev)
+        sel = [(n, t[2] * self.q + t[1]) for n, t in enumerate(refl)
+               if t[0] == UPDATE and task_owner(t, self.world) == self.rank]
+        if sel:
+            pos = torch.tensor([x[0] for x in sel], dtype=torch.int64, device=dev)
+            cel = torch.tensor([x[1] for x in sel], dtype=torch.int64, device=dev)
+            rk[pos] = self.rf.yrank[cel].clamp(min=0)
+        return rk
+
+    def set_level_ranks(self, refl, hdr):
+        for t, r in zip(refl, hdr.cpu().tolist()):
+            self._ranks[t] = int(r)
 
     def run(self, lv, own):
         rt, g = self.rt, self.g
@@ -132,7 +176,12 @@ class GpuStore:
         bufs = []
         if g.kind_host[i, k]:
             ou = int(g.off_u_host[c])
-            bufs.append(g.pool[ou:ou + 2 * b * g.cap])  # U slab then V slab (holds Y^T)
+            r = self._ranks.get(t)
+            if r is None:  # no rank exchange (single process / emulation): whole slabs
+                bufs.append(g.pool[ou:ou + 2 * b * g.cap])  # U slab then V slab (holds Y^T)
+            elif r > 0:  # U_ik (b x r) and Y_i^T (b x r) at the head of the U / V slabs
+                bufs.append(g.pool[ou:ou + b * r])
+                bufs.append(g.pool[ou + b * g.cap:ou + b * g.cap + b * r])
         else:
             y = int(rf.y_off_host[c])
             bufs.append(rf.pool[y:y + b * b])
@@ -144,17 +193,22 @@ class GpuStore:
         pass
 
 
-def factorize_distributed(grid, cfg, world: int, rank: int, broadcast=None):
+def factorize_distributed(grid, cfg, world: int, rank: int, broadcast=None, allreduce=None, store=None):
     """Distributed tiled-hh on this rank's GPU.  ``grid`` holds the full input
     (only owned columns are read).  Returns the GpuStore; owned columns of
-    store.g hold R-tilde, store.rf the reflectors of every column."""
+    store.g hold R-tilde, store.rf the reflectors of every column.  Pass a
+    previously built ``store`` to reuse its plan (it is reset to ``grid``)."""
+    import torch.distributed as dist
     if broadcast is None:
-        import torch.distributed as dist
-
         def broadcast(t, src):
             dist.broadcast(t, src)
-    st = GpuStore(grid, cfg, world, rank)
-    run_tiled_distributed(st, st.plan, world, rank, broadcast)
+    if allreduce is None:
+        def allreduce(t):
+            dist.all_reduce(t)
+    st = store if store is not None else GpuStore(grid, cfg, world, rank)
+    if store is not None:
+        st.reset(grid)
+    run_tiled_distributed(st, st.plan, world, rank, broadcast, allreduce)
     return st
 
 

@@ -179,8 +179,9 @@ def test_cta_teams_bitwise_equal_to_single_cta(pk):
 @pytest.mark.parametrize("world", [1, 2, 3])
 def test_distributed_gpu_store_emulated_ranks(pk, world):
     """The GPU store of the block-cyclic driver, with `world` ranks emulated
-    on one GPU level by level (no rank ever waits on another; broadcasts are
-    device copies from the owner's buffers): the assembled R-tilde and every
+    on one GPU level by level (no rank ever waits on another; the per-level
+    rank exchange is summed on the host and broadcasts are device copies of
+    the owner's rank-sized payloads): the assembled R-tilde and every
     reflector must equal the single-GPU run bit for bit."""
     import torch
     from paper_2208_06194_b200 import distributed as D
@@ -198,6 +199,11 @@ def test_distributed_gpu_store_emulated_ranks(pk, world):
             own = st.plan[lv][0]
             if len(own):
                 st.run(lv, own)
+        refl = stores[0].plan[lv][1]
+        if world > 1 and refl:  # the rank exchange (all-reduce of the level's Ytilde ranks)
+            hdr = sum(st.level_ranks(refl) for st in stores)
+            for st in stores:
+                st.set_level_ranks(refl, hdr)
         for t in stores[0].plan[lv][1]:
             src = D.task_owner(t, world)
             sb = stores[src].reflector_buffers(t)
