@@ -193,17 +193,28 @@ def run_ours(args):
 
     distributed = ws_ > 1 and method == "tiled-hh"
 
-    dist_store = []  # the rank's GpuStore: schedule / plan / task list built once, before the timed region
+    dist_store = []  # the rank's store: DAG / plan / IPC peers built once, before the timed region
 
-    class _DistStep:  # distributed run: 1-D block-cyclic columns + NCCL reflector broadcasts
+    class _DistStep:  # distributed run: 1-D block-cyclic columns
+        """--dist peer (default): per-rank dynamic DAGs, reflectors pushed into
+        the peers' stores over NVLink (distributed.PeerDagRank); --dist levels:
+        level-synchronous tasks + NCCL reflector broadcasts (GpuStore)."""
+
         def __init__(self):
-            from paper_2208_06194_b200.distributed import GpuStore, factorize_distributed
-            if not dist_store:
-                dist_store.append(GpuStore(g0.clone(), tol, ws_, rank))
-                torch.cuda.synchronize()
-            self.st = factorize_distributed(g0.clone(), tol, ws_, rank, store=dist_store[0])
+            from paper_2208_06194_b200 import distributed as D
+            if args.dist == "peer":
+                if not dist_store:
+                    dist_store.append(D.PeerDagRank(g0.clone(), tol, ws_, rank))
+                    torch.cuda.synchronize()
+                self.st = dist_store[0].run(g0.clone())
+                self.nlevels = 0
+            else:
+                if not dist_store:
+                    dist_store.append(D.GpuStore(g0.clone(), tol, ws_, rank))
+                    torch.cuda.synchronize()
+                self.st = D.factorize_distributed(g0.clone(), tol, ws_, rank, store=dist_store[0])
+                self.nlevels = len(self.st.plan)
             self.g = self.st.g
-            self.nlevels = len(self.st.plan)
 
         def finish(self):
             return rt.harvest()[1]
@@ -260,7 +271,9 @@ def run_ours(args):
         ms = float(t.item())
     gflops = F_step / (ms * 1e-3) / 1e9
     k_ms = (sum(kern_ms) / len(kern_ms)) if kern_ms else ms
-    if distributed:
+    if distributed and args.dist == "peer":
+        launches, kernel_name = 2, "k_tiled_dag (per-rank dynamic DAG, reflector pushes over NVLink peer memory)"
+    elif distributed:
         launches, kernel_name = nlev, "k_tiled (per-level task batches, block-cyclic)"
     elif method == "tiled-hh" and getattr(f, "scheduler", "") == "dag":
         launches, kernel_name = 2, "k_tiled_dag (persistent dynamic-DAG task kernel, one CTA per SM)"
@@ -585,6 +598,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C3")
     ap.add_argument("--method", default=None)
+    ap.add_argument("--dist", default="peer", choices=["peer", "levels"],
+                    help="N > 1 tiled driver: per-rank DAGs with NVLink reflector pushes, or level-synchronous NCCL")
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--cpu-rows", type=int, default=24)
     ap.add_argument("--no-cpu", action="store_true")

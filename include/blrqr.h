@@ -248,6 +248,72 @@ int blrqr_tiled_run_dag(const blrqr_grid* g, const blrqr_refl* rf, int ntasks, c
                         const int* prio_dev, int* work_dev, double eps, double* ws, int64_t ws_per_cta, int nctas,
                         double timeout_s, int* status, unsigned long long* flops, void* stream);
 
+/* ---- multi-GPU tiled Householder: per-rank dynamic DAGs with
+ * reflector pushes over NVLink peer memory ------------------------------------
+ * Column j of the grid lives on rank j mod world; rank r runs the tasks
+ * that write its columns (factorize.py:379-444 task set, the reference's
+ * execute_taskgraph semantics, scheduler.py:335-416) in its own persistent
+ * kernel.  After DiagQR(k) / UpdateQR(k, i) the producing rank runs one push
+ * task (kind 8: k, i (-1 for DiagQR), j = destination rank) per peer: it
+ * stores the reflector (Y_kk, T_kk / Ytilde_ik at its rank, T_ik, yrank) into
+ * the peer's stores at the same offsets and releases the peer's dependent
+ * tasks with system-scope atomics on the peer's in-degrees and ready rings.
+ * This replaces the reference's shared-memory task graph with no host in the
+ * loop and no collective call.  Every rank allocates the same grid / store
+ * layout.  With one process per GPU the peer pointers come from CUDA IPC
+ * (blrqr_ipc_*); for emulation one launch hosts every rank on one GPU. */
+#define BLRQR_MAX_WORLD 8
+int64_t blrqr_tiled_dist_dag_size(int p, int q, int world, int rank, int64_t* nedges, int64_t* nredges);
+/* rank's DAG: tasks (owned tasks in canonical order, each reflector producer
+ * followed by its push tasks), in-degrees (remote predecessors included),
+ * local successor CSR, priorities, and the push tasks' remote successors
+ * (the peer's local task ids) as a second CSR.  Returns 0, -1 bad shape,
+ * -3 internal (a cross-rank edge that is not a reflector read). */
+int blrqr_tiled_dist_dag(int p, int q, int world, int rank, blrqr_task* tasks_host, int* indeg_host,
+                         int64_t* succ_off_host, int* succ_host, int* prio_host, int64_t* rsucc_off_host,
+                         int* rsucc_host);
+/* one rank's DAG as device arrays (rsucc_off / rsucc may be NULL when world = 1) */
+typedef struct {
+  blrqr_grid g;
+  blrqr_refl rf;
+  int ntasks;
+  const blrqr_task* tasks;
+  const int* indeg0;
+  const int64_t* succ_off;
+  const int* succ;
+  const int* prio;
+  const int64_t* rsucc_off;
+  const int* rsucc;
+  int* work; /* blrqr_dag_work_ints(ntasks) ints */
+} blrqr_dag_rank;
+/* another rank's memory as addressed from this device */
+typedef struct {
+  double* gpool; /* its blrqr_grid.pool */
+  double* rpool; /* its blrqr_refl.pool */
+  int* yrank;    /* its blrqr_refl.yrank */
+  int* work;     /* its blrqr_dag_rank.work */
+  const int* prio;
+  int ntasks;
+} blrqr_peer;
+/* Re-arm the scheduler state of nranks hosted ranks (in-degrees, ready rings,
+ * counters; initially ready tasks queued).  Every rank of a multi-GPU run
+ * must finish its reset (stream sync + a barrier) before any rank launches. */
+int blrqr_tiled_dag_reset(int nranks, const blrqr_dag_rank* ranks, void* stream);
+/* One persistent launch hosting ranks rank_ids[0..nranks) of `world` (nctas
+ * CTAs split evenly); peers[world] addresses every rank's memory (unused
+ * when world = 1).  Stream-ordered; returns 0 or an error code. */
+int blrqr_tiled_run_dag_multi(int world, int nranks, const int* rank_ids, const blrqr_dag_rank* ranks,
+                              const blrqr_peer* peers, double eps, double* ws, int64_t ws_per_cta, int nctas,
+                              double timeout_s, int* status, unsigned long long* flops, void* stream);
+/* CUDA IPC for the peer pointers: export the allocation holding ptr (64-byte
+ * handle + ptr's offset inside it), open a peer's (returns the mapped base,
+ * add the offset), close it. */
+int blrqr_ipc_handle(const void* ptr, void* handle64, int64_t* offset);
+int blrqr_ipc_open(const void* handle64, void** base);
+int blrqr_ipc_close(void* base);
+/* Enable peer access from the current device to every other visible device (idempotent). */
+int blrqr_enable_peer_access(void);
+
 /* Blocked Householder (factorize.py:187-292), one step k: panel GEQRT of
  * block column k (triangularize_block_column, :187-229; one task), then for
  * every j > k the ascending-i accumulation chain z_j = T_k^T sum_i Y_ik^T A_ij

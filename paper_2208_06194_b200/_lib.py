@@ -44,6 +44,22 @@ class Task(C.Structure):
     _fields_ = [("kind", C.c_int), ("k", C.c_int), ("i", C.c_int), ("j", C.c_int)]
 
 
+class DagRank(C.Structure):
+    """blrqr_dag_rank: one rank's DAG as device arrays."""
+    _fields_ = [("g", Grid), ("rf", Refl), ("ntasks", C.c_int), ("tasks", C.c_void_p), ("indeg0", C.c_void_p),
+                ("succ_off", C.c_void_p), ("succ", C.c_void_p), ("prio", C.c_void_p), ("rsucc_off", C.c_void_p),
+                ("rsucc", C.c_void_p), ("work", C.c_void_p)]
+
+
+class Peer(C.Structure):
+    """blrqr_peer: another rank's memory as addressed from this device."""
+    _fields_ = [("gpool", C.c_void_p), ("rpool", C.c_void_p), ("yrank", C.c_void_p), ("work", C.c_void_p),
+                ("prio", C.c_void_p), ("ntasks", C.c_int)]
+
+
+MAX_WORLD = 8
+
+
 _P = C.c_void_p
 _I = C.c_int
 _L = C.c_int64
@@ -88,6 +104,14 @@ _SIGS = {
     "blrqr_dag_policy": ([], _L),
     "blrqr_tiled_run_dag": ([C.POINTER(Grid), C.POINTER(Refl), _I, _P, _P, _P, _P, _P, _P, _D, _P, _L, _I, _D, _P,
                              _P, _P], _I),
+    "blrqr_tiled_dist_dag_size": ([_I, _I, _I, _I, _P, _P], _L),
+    "blrqr_tiled_dist_dag": ([_I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P], _I),
+    "blrqr_tiled_dag_reset": ([_I, _P, _P], _I),
+    "blrqr_tiled_run_dag_multi": ([_I, _I, _P, _P, _P, _D, _P, _L, _I, _D, _P, _P, _P], _I),
+    "blrqr_ipc_handle": ([_P, _P, _P], _I),
+    "blrqr_ipc_open": ([_P, _P], _I),
+    "blrqr_ipc_close": ([_P], _I),
+    "blrqr_enable_peer_access": ([], _I),
     "blrqr_blocked_step": ([C.POINTER(Grid), C.POINTER(Refl), _I, _D, _P, _P, _P, _L, _P, _L, _I, _P, _P, _P], _I),
     "blrqr_blocked_step_dist": ([C.POINTER(Grid), C.POINTER(Refl), _I, _D, _P, _P, _P, _L, _P, _L, _I, _I, _I, _I,
                                  _P, _P, _P], _I),

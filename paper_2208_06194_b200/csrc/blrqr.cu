@@ -419,6 +419,20 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM) k_mgs_stage(int stage, blrqr_
 #endif
 constexpr int DAG_RINGS = BLR_DAG_RINGS;
 
+// Another rank's scheduler state and stores as addressed from this GPU
+// (NVLink peer pointers from CUDA IPC; the same GPU for emulated ranks).
+// Every rank holds the same grid / reflector layout, so a reflector's offset
+// from the pool base is the same on every rank.
+struct PeerDev {
+  double* gpool;
+  double* rpool;
+  int* yrank;
+  int* indeg;
+  int* q[DAG_RINGS];
+  int* ctr;
+  const int* prio;
+};
+
 struct DagDev {
   int n;
   const blrqr_task* tasks;
@@ -432,6 +446,19 @@ struct DagDev {
   TeamCtx* team;     // optional: CTA teams for large Jacobi cores (team.cuh)
   int reserve;       // the last `reserve` CTAs only help priority team jobs
   unsigned long long* ptrace;  // optional: per task PH_COUNT phase cycle counters
+  // multi-GPU (peer push): a push task (kind 8, reflector of (k, i) -- i < 0:
+  // DiagQR(k) -- to rank j) copies the reflector into rank j's memory and
+  // releases rank j's dependents rsucc[rsucc_off[t] .. rsucc_off[t+1])
+  const long long* rsucc_off;
+  const int* rsucc;
+  const PeerDev* peers;  // [world], nullptr on one GPU
+};
+
+// one rank hosted by a launch: its scheduler state and its grid / store
+struct DagRank {
+  DagDev d;
+  blrqr_grid g;
+  blrqr_refl rf;
 };
 
 __device__ __forceinline__ long long global_ns() {
@@ -448,12 +475,75 @@ __device__ __forceinline__ void dag_push(const DagDev& d, int t) {
   atomicExch(d.q[c] + slot, t);
 }
 
-__global__ void __launch_bounds__(NT, CTAS_PER_SM) k_tiled_dag(DagDev d, blrqr_grid g, blrqr_refl rf, double eps, double* ws,
-                                                     long long wsp, int* status, unsigned long long* flops,
-                                                     long long timeout_cycles) {
+// release on another rank: system-scope atomics (NVLink peer memory)
+__device__ __forceinline__ void dag_push_peer(const PeerDev& P, int t) {
+  const int c = min(DAG_RINGS - 1, P.prio[t] >> 2);
+  const int slot = atomicAdd_system(P.ctr + 2 * c + 1, 1);
+  atomicExch_system(P.q[c] + slot, t);
+}
+
+__device__ __forceinline__ void copy_to_peer(const double* src, double* dst, long long n) {
+  if (n <= 0) return;
+  const long long n2 = n >> 1;  // offsets are multiples of b: 16-byte aligned
+  const double2* s2 = reinterpret_cast<const double2*>(src);
+  double2* d2 = reinterpret_cast<double2*>(dst);
+  for (long long e = threadIdx.x; e < n2; e += NT) d2[e] = s2[e];
+  if ((n & 1) && threadIdx.x == 0) dst[n - 1] = src[n - 1];
+}
+
+// Push task: the reflector produced by DiagQR(k) (i < 0) or UpdateQR(k, i) --
+// exactly the data ApplyBlock / ApplyTrap read (refl_blk, T, yrank) -- is
+// stored into rank `to`'s stores at the same offsets, then rank `to`'s
+// dependents are released.  Low-rank Ytilde travels at its rank (b x r of
+// U_ik and of Y^T), not at the slab capacity.
+__device__ void tiled_push(const DagDev& d, const blrqr_grid& g, const blrqr_refl& rf, int t, int k, int i,
+                           int to) {
+  const PeerDev& P = d.peers[to];
+  const int b = g.b;
+  const long long bb = (long long)b * b;
+  if (i < 0) {
+    const long long c = (long long)k * g.q + k;
+    copy_to_peer(rf.pool + rf.y_off[c], P.rpool + rf.y_off[c], bb);
+    copy_to_peer(rf.pool + rf.t_off[c], P.rpool + rf.t_off[c], bb);
+  } else {
+    const long long c = (long long)i * g.q + k;
+    const int yr = rf.yrank[c];
+    if (yr >= 0) {
+      copy_to_peer(g.pool + g.off_u[c], P.gpool + g.off_u[c], (long long)b * yr);
+      copy_to_peer(g.pool + g.off_v[c], P.gpool + g.off_v[c], (long long)b * yr);
+    } else {
+      copy_to_peer(rf.pool + rf.y_off[c], P.rpool + rf.y_off[c], bb);
+    }
+    copy_to_peer(rf.pool + rf.t_off[c], P.rpool + rf.t_off[c], bb);
+    if (threadIdx.x == 0) P.yrank[c] = yr;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();  // payload visible on the peer before any release
+    for (long long e = d.rsucc_off[t]; e < d.rsucc_off[t + 1]; ++e) {
+      const int s2 = d.rsucc[e];
+      if (atomicSub_system(P.indeg + s2, 1) == 1) dag_push_peer(P, s2);
+    }
+  }
+  __syncthreads();
+}
+
+// One launch hosts `vranks` ranks (1 on a multi-GPU rank or a single GPU;
+// every rank of the world when ranks are emulated on one GPU): CTA block
+// vr * per .. (vr + 1) * per - 1 runs rank vr's DAG.  The CTA teams are shared
+// (a team job carries all its pointers, and helpers use their own arenas).
+__global__ void __launch_bounds__(NT, CTAS_PER_SM) k_tiled_dag(const DagRank* ranks, int vranks, double eps,
+                                                     double* ws, long long wsp, int* status,
+                                                     unsigned long long* flops, long long timeout_cycles) {
+  const int per = (int)gridDim.x / vranks;
+  const int vr = min((int)blockIdx.x / per, vranks - 1);
+  const int lcta = (int)blockIdx.x - vr * per;
+  const DagDev d = ranks[vr].d;
+  const blrqr_grid g = ranks[vr].g;
+  const blrqr_refl rf = ranks[vr].rf;
   Ctx cx = make_ctx(ws, wsp, status, flops);
   cx.team = d.team;
-  const bool reserved = d.team && (int)blockIdx.x >= (int)gridDim.x - d.reserve;
+  const bool reserved = d.team && lcta >= per - d.reserve;
   __shared__ int s_task, s_member;
   while (true) {
     if (threadIdx.x == 0) {
@@ -518,6 +608,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM) k_tiled_dag(DagDev d, blrqr_g
       case 4: tiled_trap_a1(cx, g, rf, eps, tk.k, tk.i, tk.j); break;
       case 5: tiled_trap_b(cx, g, rf, eps, tk.k, tk.i, tk.j); break;
       case 6: tiled_trap_a2(cx, g, rf, eps, tk.k, tk.i, tk.j); break;
+      case 8: tiled_push(d, g, rf, t, tk.k, tk.i, tk.j); break;
       default: tiled_trap(cx, g, rf, eps, tk.k, tk.i, tk.j); break;
     }
     tt.stop(cx, PH_TASK);
@@ -1023,19 +1114,13 @@ int64_t blrqr_tiled_ref_dag(int p, int q, blrqr_task* tasks_host, int64_t* succ_
   return (int64_t)succ.size();
 }
 
-int blrqr_tiled_dag(int p, int q, blrqr_task* tasks_host, int* indeg_host, int64_t* succ_off_host,
-                    int* succ_host, int* prio_host) {
-  if (q < 1 || p < q) return -1;
-  std::vector<blrqr_task> tasks;
-  std::vector<int> indeg, succ;
-  std::vector<int64_t> off;
-  tiled_dag_host(p, q, tasks, indeg, off, succ);
-  std::copy(tasks.begin(), tasks.end(), tasks_host);
-  std::copy(indeg.begin(), indeg.end(), indeg_host);
-  std::copy(off.begin(), off.end(), succ_off_host);
-  std::copy(succ.begin(), succ.end(), succ_host);
-  // unit-weight slack of every task: the critical chains (DiagQR -> UpdateQR
-  // -> the column-(k+1) traps -> DiagQR(k+1)) have slack 0
+// unit-weight slack of every task: the critical chains (DiagQR -> UpdateQR
+// -> the column-(k+1) traps -> DiagQR(k+1)) have slack 0
+// bit 0: DiagQR / UpdateQR / the R_kj chain of the next panel column;
+// bit 1: may form CTA teams (slack <= g_team_slack); bits 2+: ready ring,
+// by bottom level (longest remaining chain first, DAG_RINGS classes)
+static void dag_prio(const std::vector<blrqr_task>& tasks, const std::vector<int64_t>& off,
+                     const std::vector<int>& succ, std::vector<int>& prio) {
   const int n = (int)tasks.size();
   std::vector<int> top(n, 0), bot(n, 0);
   for (int t = 0; t < n; ++t)  // canonical order is topological
@@ -1044,17 +1129,254 @@ int blrqr_tiled_dag(int p, int q, blrqr_task* tasks_host, int* indeg_host, int64
     for (int64_t e = off[t]; e < off[t + 1]; ++e) bot[t] = std::max(bot[t], bot[succ[e]] + 1);
   int cp = 0;
   for (int t = 0; t < n; ++t) cp = std::max(cp, top[t] + bot[t]);
-  // bit 0: DiagQR / UpdateQR / the R_kj chain of the next panel column;
-  // bit 1: may form CTA teams (slack <= g_team_slack); bits 2+: ready ring,
-  // by bottom level (longest remaining chain first, DAG_RINGS classes)
+  prio.assign(n, 0);
   for (int t = 0; t < n; ++t) {
     const int slack = cp - top[t] - bot[t];
     const bool hi = tasks[t].kind == 0 || tasks[t].kind == 2 || (tasks[t].kind >= 4 && tasks[t].j == tasks[t].k + 1);
     int ring;
     if (g_dag_rings == 2) ring = hi ? 0 : 1;
     else ring = std::min(DAG_RINGS - 1, (cp - bot[t]) * DAG_RINGS / (cp + 1));
-    prio_host[t] = (hi ? 1 : 0) | (slack <= g_team_slack ? 2 : 0) | (ring << 2);
+    prio[t] = (hi ? 1 : 0) | (slack <= g_team_slack ? 2 : 0) | (ring << 2);
   }
+}
+
+int blrqr_tiled_dag(int p, int q, blrqr_task* tasks_host, int* indeg_host, int64_t* succ_off_host,
+                    int* succ_host, int* prio_host) {
+  if (q < 1 || p < q) return -1;
+  std::vector<blrqr_task> tasks;
+  std::vector<int> indeg, succ, prio;
+  std::vector<int64_t> off;
+  tiled_dag_host(p, q, tasks, indeg, off, succ);
+  std::copy(tasks.begin(), tasks.end(), tasks_host);
+  std::copy(indeg.begin(), indeg.end(), indeg_host);
+  std::copy(off.begin(), off.end(), succ_off_host);
+  std::copy(succ.begin(), succ.end(), succ_host);
+  dag_prio(tasks, off, succ, prio);
+  std::copy(prio.begin(), prio.end(), prio_host);
+  return 0;
+}
+
+// ---- multi-GPU tiled DAG (peer push) ----------------------------------------
+// Rank r's DAG: the tasks it owns (columns j = r mod G: DiagQR(k) / UpdateQR(k,
+// i) by column k, ApplyBlock / ApplyTrap parts by column j), in canonical
+// order, each reflector producer followed by one push task per peer.  Edges
+// between two owned tasks are kept; an edge u -> v into another rank's task
+// is routed u -> push(u, owner(v)) -> v, the last hop a remote release; the
+// global DAG's only cross-rank edges are reflector reads (D(k), U(i, k) in
+// tiled_access), checked here.  Priorities are the global DAG's; a push task
+// inherits its producer's (critical-chain) ring.
+struct DistDag {
+  std::vector<blrqr_task> tasks;
+  std::vector<int> indeg, succ, prio, rsucc;
+  std::vector<int64_t> off, roff;
+};
+
+static int dist_dag_host(int p, int q, int world, int rank, DistDag& out) {
+  std::vector<blrqr_task> gt;
+  std::vector<int> gind, gsucc, gprio;
+  std::vector<int64_t> goff;
+  tiled_dag_host(p, q, gt, gind, goff, gsucc);
+  dag_prio(gt, goff, gsucc, gprio);
+  const int n = (int)gt.size();
+  auto owner = [&](int t) { return (gt[t].kind == 0 || gt[t].kind == 2 ? gt[t].k : gt[t].j) % world; };
+  auto producer = [&](int t) { return gt[t].kind == 0 || gt[t].kind == 2; };
+  // local ids on every rank; push ids by (producer, peer)
+  std::vector<int> lid(n, -1), cnt(world, 0);
+  std::vector<int> push_base(n, -1);  // push(t, P) = push_base[t] + (P < owner ? P : P - 1)
+  for (int t = 0; t < n; ++t) {
+    const int o = owner(t);
+    lid[t] = cnt[o]++;
+    if (producer(t) && world > 1) {
+      push_base[t] = cnt[o];
+      cnt[o] += world - 1;
+    }
+  }
+  auto push_id = [&](int t, int P) { return push_base[t] + (P < owner(t) ? P : P - 1); };
+  const int nl = cnt[rank];
+  out.tasks.assign(nl, blrqr_task{0, 0, 0, 0});
+  out.prio.assign(nl, 0);
+  out.indeg.assign(nl, 0);
+  std::vector<std::vector<int>> ls(nl), rs(nl);
+  for (int t = 0; t < n; ++t) {
+    const int o = owner(t);
+    for (int64_t e = goff[t]; e < goff[t + 1]; ++e) {
+      const int v = gsucc[e], ov = owner(v);
+      if (o == ov) {
+        if (o == rank) ls[lid[t]].push_back(lid[v]);
+        continue;
+      }
+      if (!producer(t)) return -3;  // a cross-rank edge that is not a reflector read
+      if (o == rank) rs[push_id(t, ov)].push_back(lid[v]);
+      if (ov == rank) out.indeg[lid[v]] += 1;
+    }
+    if (o != rank) continue;
+    out.tasks[lid[t]] = gt[t];
+    out.prio[lid[t]] = gprio[t];
+    if (push_base[t] >= 0)
+      for (int P = 0; P < world; ++P) {
+        if (P == rank) continue;
+        const int u = push_id(t, P);
+        out.tasks[u] = blrqr_task{8, gt[t].k, gt[t].kind == 0 ? -1 : gt[t].i, P};
+        out.prio[u] = gprio[t] & ~2;  // a push never recruits a team
+        ls[lid[t]].push_back(u);
+      }
+  }
+  out.off.assign(nl + 1, 0);
+  out.roff.assign(nl + 1, 0);
+  out.succ.clear();
+  out.rsucc.clear();
+  for (int t = 0; t < nl; ++t) {
+    for (int v : ls[t]) {
+      out.succ.push_back(v);
+      out.indeg[v] += 1;
+    }
+    std::sort(rs[t].begin(), rs[t].end());
+    rs[t].erase(std::unique(rs[t].begin(), rs[t].end()), rs[t].end());
+    for (int v : rs[t]) out.rsucc.push_back(v);
+    out.off[t + 1] = (int64_t)out.succ.size();
+    out.roff[t + 1] = (int64_t)out.rsucc.size();
+  }
+  return 0;
+}
+
+int64_t blrqr_tiled_dist_dag_size(int p, int q, int world, int rank, int64_t* nedges, int64_t* nredges) {
+  if (q < 1 || p < q || world < 1 || world > BLRQR_MAX_WORLD || rank < 0 || rank >= world) return -1;
+  DistDag d;
+  if (int e = dist_dag_host(p, q, world, rank, d)) return e;
+  if (nedges) *nedges = (int64_t)d.succ.size();
+  if (nredges) *nredges = (int64_t)d.rsucc.size();
+  return (int64_t)d.tasks.size();
+}
+
+int blrqr_tiled_dist_dag(int p, int q, int world, int rank, blrqr_task* tasks_host, int* indeg_host,
+                         int64_t* succ_off_host, int* succ_host, int* prio_host, int64_t* rsucc_off_host,
+                         int* rsucc_host) {
+  if (q < 1 || p < q || world < 1 || world > BLRQR_MAX_WORLD || rank < 0 || rank >= world) return -1;
+  DistDag d;
+  if (int e = dist_dag_host(p, q, world, rank, d)) return e;
+  std::copy(d.tasks.begin(), d.tasks.end(), tasks_host);
+  std::copy(d.indeg.begin(), d.indeg.end(), indeg_host);
+  std::copy(d.off.begin(), d.off.end(), succ_off_host);
+  std::copy(d.succ.begin(), d.succ.end(), succ_host);
+  std::copy(d.prio.begin(), d.prio.end(), prio_host);
+  std::copy(d.roff.begin(), d.roff.end(), rsucc_off_host);
+  std::copy(d.rsucc.begin(), d.rsucc.end(), rsucc_host);
+  return 0;
+}
+
+static DagDev dag_dev(const blrqr_dag_rank& r) {
+  DagDev d;
+  std::memset(&d, 0, sizeof(d));
+  d.n = r.ntasks;
+  d.tasks = r.tasks;
+  d.succ_off = (const long long*)r.succ_off;
+  d.succ = r.succ;
+  d.prio = r.prio;
+  d.indeg = r.work;
+  for (int c = 0; c < DAG_RINGS; ++c) d.q[c] = r.work + (int64_t)(c + 1) * r.ntasks;
+  d.ctr = r.work + (int64_t)(DAG_RINGS + 1) * r.ntasks;
+  d.rsucc_off = (const long long*)r.rsucc_off;
+  d.rsucc = r.rsucc;
+  return d;
+}
+
+int blrqr_tiled_dag_reset(int nranks, const blrqr_dag_rank* ranks, void* stream) {
+  if (nranks < 1 || !ranks) return -1;
+  cudaStream_t st = as_stream(stream);
+  for (int v = 0; v < nranks; ++v) {
+    const blrqr_dag_rank& r = ranks[v];
+    if (r.ntasks <= 0 || !r.work || !r.indeg0) return -1;
+    DagDev d = dag_dev(r);
+    CK(cudaMemcpyAsync(d.indeg, r.indeg0, sizeof(int) * r.ntasks, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemsetAsync(d.q[0], 0xFF, sizeof(int) * DAG_RINGS * (size_t)r.ntasks, st));
+    CK(cudaMemsetAsync(d.ctr, 0, sizeof(int) * (2 * DAG_RINGS + 1), st));
+    k_dag_init<<<1, 256, 0, st>>>(d);
+    CK(cudaGetLastError());
+  }
+  return 0;
+}
+
+// launch arguments live in a per-(device, stream) device buffer (stream-ordered copies)
+static void* launch_args_buf(cudaStream_t st, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, std::pair<void*, size_t>> bufs;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto& b = bufs[{dev, st}];
+  if (b.second < bytes) {
+    if (b.first) {
+      cudaStreamSynchronize(st);
+      cudaFree(b.first);
+    }
+    b.first = nullptr;
+    if (cudaMalloc(&b.first, bytes) != cudaSuccess) {
+      b.second = 0;
+      return nullptr;
+    }
+    b.second = bytes;
+  }
+  return b.first;
+}
+
+int blrqr_tiled_run_dag_multi(int world, int nranks, const int* rank_ids, const blrqr_dag_rank* ranks,
+                              const blrqr_peer* peers, double eps, double* ws, int64_t ws_per_cta, int nctas,
+                              double timeout_s, int* status, unsigned long long* flops, void* stream) {
+  if (world < 1 || world > BLRQR_MAX_WORLD || nranks < 1 || nranks > world || !ranks || !rank_ids) return -1;
+  if (world > 1 && !peers) return -1;
+  if (nctas < nranks) return -1;
+  if (!(eps > 0.0 && eps < 1.0)) return -2;
+  INIT_KERNELS();
+  cudaStream_t st = as_stream(stream);
+  TeamCtx* team = nullptr;
+  if (int e = team_for_launch(st, &team, nullptr)) return e;
+  const int per = nctas / nranks;
+  std::vector<DagRank> hr(nranks);
+  std::vector<PeerDev> hp(world);
+  for (int P = 0; P < world && world > 1; ++P) {
+    const blrqr_peer& x = peers[P];
+    PeerDev& y = hp[P];
+    y.gpool = x.gpool;
+    y.rpool = x.rpool;
+    y.yrank = x.yrank;
+    y.indeg = x.work;
+    for (int c = 0; c < DAG_RINGS; ++c) y.q[c] = x.work + (int64_t)(c + 1) * x.ntasks;
+    y.ctr = x.work + (int64_t)(DAG_RINGS + 1) * x.ntasks;
+    y.prio = x.prio;
+  }
+  const size_t rb = sizeof(DagRank) * nranks, pb = sizeof(PeerDev) * world;
+  char* buf = static_cast<char*>(launch_args_buf(st, rb + pb + 256));
+  if (!buf) return 1000 + (int)cudaErrorMemoryAllocation;
+  PeerDev* dpeers = world > 1 ? reinterpret_cast<PeerDev*>(buf + ((rb + 255) & ~(size_t)255)) : nullptr;
+  for (int v = 0; v < nranks; ++v) {
+    const blrqr_dag_rank& r = ranks[v];
+    if (r.ntasks <= 0 || rank_ids[v] < 0 || rank_ids[v] >= world) return -1;
+    DagRank& x = hr[v];
+    x.d = dag_dev(r);
+    x.d.trace = g_dag_trace;
+    x.d.ptrace = g_phase_trace;
+    x.d.team = team;
+    x.d.reserve = team ? std::min(g_team_reserve / nranks, per / 4) : 0;
+    x.d.peers = dpeers;
+    x.g = r.g;
+    x.rf = r.rf;
+  }
+  // pageable source: the copy is staged before the call returns
+  CK(cudaMemcpyAsync(buf, hr.data(), rb, cudaMemcpyHostToDevice, st));
+  if (dpeers) CK(cudaMemcpyAsync(dpeers, hp.data(), pb, cudaMemcpyHostToDevice, st));
+  int dev = 0, clk_khz = 1965000;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev);
+  const long long timeout_cycles = (long long)(timeout_s * clk_khz * 1e3);
+  // The persistent scheduler spins on work released by other CTAs, so all
+  // nctas CTAs must be co-resident: a cooperative launch guarantees it (or
+  // fails with cudaErrorCooperativeLaunchTooLarge instead of deadlocking).
+  const DagRank* dr = reinterpret_cast<const DagRank*>(buf);
+  int nr = nranks;
+  double* ws_arg = ws;
+  long long wsp_arg = ws_per_cta;
+  void* args[] = {&dr, &nr, &eps, &ws_arg, &wsp_arg, &status, &flops, const_cast<long long*>(&timeout_cycles)};
+  CK(cudaLaunchCooperativeKernel((const void*)k_tiled_dag, dim3(per * nranks), dim3(NT), args, SMEM_BYTES, st));
   return 0;
 }
 
@@ -1064,38 +1386,71 @@ int blrqr_tiled_run_dag(const blrqr_grid* g, const blrqr_refl* rf, int ntasks, c
                         double timeout_s, int* status, unsigned long long* flops, void* stream) {
   if (!g || !rf || ntasks <= 0) return -1;
   if (!(eps > 0.0 && eps < 1.0)) return -2;
-  INIT_KERNELS();
-  cudaStream_t st = as_stream(stream);
-  DagDev d;
-  d.n = ntasks;
-  d.tasks = tasks_dev;
-  d.succ_off = (const long long*)succ_off_dev;
-  d.succ = succ_dev;
-  d.prio = prio_dev;
-  d.indeg = work_dev;
-  for (int c = 0; c < DAG_RINGS; ++c) d.q[c] = work_dev + (int64_t)(c + 1) * ntasks;
-  d.ctr = work_dev + (int64_t)(DAG_RINGS + 1) * ntasks;
-  d.trace = g_dag_trace;
-  d.ptrace = g_phase_trace;
-  int dev = 0, clk_khz = 1965000;
-  cudaGetDevice(&dev);
-  if (int e = team_for_launch(st, &d.team, nullptr)) return e;
-  d.reserve = d.team ? std::min(g_team_reserve, nctas / 4) : 0;
-  CK(cudaMemcpyAsync(d.indeg, indeg0_dev, sizeof(int) * ntasks, cudaMemcpyDeviceToDevice, st));
-  CK(cudaMemsetAsync(d.q[0], 0xFF, sizeof(int) * DAG_RINGS * (size_t)ntasks, st));
-  CK(cudaMemsetAsync(d.ctr, 0, sizeof(int) * (2 * DAG_RINGS + 1), st));
-  k_dag_init<<<1, 256, 0, st>>>(d);
-  CK(cudaGetLastError());
-  cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev);
-  const long long timeout_cycles = (long long)(timeout_s * clk_khz * 1e3);
-  // The persistent scheduler spins on work released by other CTAs, so all
-  // nctas CTAs must be co-resident: a cooperative launch guarantees it (or
-  // fails with cudaErrorCooperativeLaunchTooLarge instead of deadlocking).
-  double* ws_arg = ws;
-  int64_t wsp_arg = ws_per_cta;
-  void* args[] = {&d, const_cast<blrqr_grid*>(g), const_cast<blrqr_refl*>(rf), &eps, &ws_arg, &wsp_arg, &status,
-                  &flops, const_cast<long long*>(&timeout_cycles)};
-  CK(cudaLaunchCooperativeKernel((const void*)k_tiled_dag, dim3(nctas), dim3(NT), args, SMEM_BYTES, st));
+  blrqr_dag_rank r;
+  std::memset(&r, 0, sizeof(r));
+  r.g = *g;
+  r.rf = *rf;
+  r.ntasks = ntasks;
+  r.tasks = tasks_dev;
+  r.indeg0 = indeg0_dev;
+  r.succ_off = succ_off_dev;
+  r.succ = succ_dev;
+  r.prio = prio_dev;
+  r.work = work_dev;
+  if (int e = blrqr_tiled_dag_reset(1, &r, stream)) return e;
+  const int rank0 = 0;
+  return blrqr_tiled_run_dag_multi(1, 1, &rank0, &r, nullptr, eps, ws, ws_per_cta, nctas, timeout_s, status, flops,
+                                   stream);
+}
+
+typedef int (*cu_range_fn)(unsigned long long*, size_t*, unsigned long long);  // cuMemGetAddressRange_v2
+
+int blrqr_ipc_handle(const void* ptr, void* handle64, int64_t* offset) {
+  if (!ptr || !handle64 || !offset) return -1;
+  static cu_range_fn range = nullptr;
+  if (!range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) return -4;
+    range = reinterpret_cast<cu_range_fn>(fn);
+  }
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (range(&base, &size, (unsigned long long)(uintptr_t)ptr) != 0) return -4;
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  std::memcpy(handle64, &h, sizeof(h));
+  *offset = (int64_t)((uintptr_t)ptr - (uintptr_t)base);
+  return 0;
+}
+
+int blrqr_ipc_open(const void* handle64, void** base) {
+  if (!handle64 || !base) return -1;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof(h));
+  CK(cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess));
+  return 0;
+}
+
+int blrqr_ipc_close(void* base) {
+  CK(cudaIpcCloseMemHandle(base));
+  return 0;
+}
+
+int blrqr_enable_peer_access(void) {
+  int dev = 0, n = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaGetDeviceCount(&n));
+  for (int o = 0; o < n; ++o) {
+    if (o == dev) continue;
+    int can = 0;
+    cudaDeviceCanAccessPeer(&can, dev, o);
+    if (!can) continue;
+    const cudaError_t e = cudaDeviceEnablePeerAccess(o, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+    else if (e != cudaSuccess) return 1000 + (int)e;
+  }
   return 0;
 }
 

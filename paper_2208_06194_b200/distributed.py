@@ -374,3 +374,199 @@ def factorize_columns_distributed(method: str, grid, cfg, world: int, rank: int,
         raise ValueError(f"column-cyclic driver covers blocked-hh and mgs, not {method!r}")
     run_column_distributed(st, grid.q, world, rank, broadcast)
     return st
+
+
+# ---------------------------------------------------------------------------
+# tiled Householder on per-rank dynamic DAGs with NVLink peer pushes
+# ---------------------------------------------------------------------------
+# The level-synchronous driver above puts a host-issued collective between
+# every pair of DAG levels.  The peer-DAG driver below runs the reference's
+# task-graph engine (execute_taskgraph, scheduler.py:335-416) per rank with no
+# host in the loop: each rank's persistent k_tiled_dag runs the tasks of its
+# columns; a reflector producer (DiagQR(k), UpdateQR(k, i)) is followed by one
+# push task per peer that stores the reflector straight into the peer's
+# stores over NVLink and releases the peer's dependent ApplyBlock / ApplyTrap
+# tasks with system-scope atomics (blrqr_tiled_run_dag_multi).  Ownership is
+# the block-cyclic one above; every rank's DAG is derived from the same global
+# DAG (blrqr_tiled_dist_dag), so the operation sequence on each cell, and
+# hence R-tilde and every reflector, is bitwise the single-GPU result.
+
+PUSH = 8
+
+
+def dist_dag_arrays(p: int, q: int, world: int, rank: int):
+    """Rank's DAG (numpy): tasks[n, 4], indeg, succ_off, succ, prio, rsucc_off, rsucc."""
+    from . import _lib
+    lib = _lib.load()
+    ne, nr = C.c_int64(0), C.c_int64(0)
+    n = int(lib.blrqr_tiled_dist_dag_size(p, q, world, rank, C.byref(ne), C.byref(nr)))
+    if n < 0:
+        raise ValueError(f"bad distributed DAG shape p={p} q={q} world={world} rank={rank} ({n})")
+    a = {"tasks": np.zeros((n, 4), dtype=np.int32), "indeg": np.zeros(n, dtype=np.int32),
+         "off": np.zeros(n + 1, dtype=np.int64), "succ": np.zeros(max(ne.value, 1), dtype=np.int32),
+         "prio": np.zeros(n, dtype=np.int32), "roff": np.zeros(n + 1, dtype=np.int64),
+         "rsucc": np.zeros(max(nr.value, 1), dtype=np.int32)}
+    rc = lib.blrqr_tiled_dist_dag(p, q, world, rank, *(a[k].ctypes.data for k in
+                                                        ("tasks", "indeg", "off", "succ", "prio", "roff", "rsucc")))
+    if rc != 0:
+        raise RuntimeError(f"distributed DAG build failed ({rc})")
+    return a
+
+
+class PeerDagStore:
+    """One rank's device state for the peer-DAG driver: its copy of the grid
+    (the full layout, so reflector offsets agree on every rank; only owned
+    columns are written by its tasks, remote columns receive the pushed
+    reflectors), its reflector store, and its DAG arrays.  Built once per
+    shape (host DAG derivation stays out of timed regions); ``reset`` re-arms
+    it for a new input."""
+
+    def __init__(self, grid, cfg, world: int, rank: int):
+        from . import _lib
+        from .device import DeviceRefl
+
+        if world < 1 or world > _lib.MAX_WORLD or not 0 <= rank < world:
+            raise ValueError(f"world must be 1..{_lib.MAX_WORLD} and 0 <= rank < world")
+        self.lib = _lib
+        self.rt = _lib.runtime()
+        self.cfg = cfg
+        self.world, self.rank = world, rank
+        self.g = grid
+        self.rf = DeviceRefl(grid)
+        self.rf.enable_split_traps()
+        a = dist_dag_arrays(grid.p, grid.q, world, rank)
+        self.host = a
+        dev = self.rt.dev
+        self.n = len(a["tasks"])
+        self.dev = {k: torch.from_numpy(v).to(dev) for k, v in a.items()}
+        self.work = torch.empty(int(self.rt.lib.blrqr_dag_work_ints(self.n)), dtype=torch.int32, device=dev)
+
+    def reset(self, grid) -> None:
+        self.g = grid
+        self.rf.grid = grid
+        self.rf.yrank.fill_(-1)
+
+    def dag_rank(self):
+        d = self.dev
+        r = self.lib.DagRank()
+        r.g, r.rf = self.g.cstruct(), self.rf.cstruct()
+        r.ntasks = self.n
+        r.tasks, r.indeg0 = d["tasks"].data_ptr(), d["indeg"].data_ptr()
+        r.succ_off, r.succ, r.prio = d["off"].data_ptr(), d["succ"].data_ptr(), d["prio"].data_ptr()
+        r.rsucc_off, r.rsucc = d["roff"].data_ptr(), d["rsucc"].data_ptr()
+        r.work = self.work.data_ptr()
+        return r
+
+    def peer_tensors(self):
+        """The tensors other ranks write into or read: grid pool, reflector
+        pool, yrank, scheduler work area, priorities."""
+        return [self.g.pool, self.rf.pool, self.rf.yrank, self.work, self.dev["prio"]]
+
+    def local_peer(self):
+        return self._peer([t.data_ptr() for t in self.peer_tensors()], self.n)
+
+    def _peer(self, ptrs, n):
+        p = self.lib.Peer()
+        p.gpool, p.rpool, p.yrank, p.work, p.prio = ptrs
+        p.ntasks = n
+        return p
+
+
+def _launch(stores, peers, rank_ids, world, nctas=None):
+    """Reset the hosted ranks' scheduler state, then one persistent launch."""
+    from . import _lib
+    from .factorize import DAG_TIMEOUT_S
+    rt = stores[0].rt
+    g = stores[0].g
+    nr = len(stores)
+    ranks = (_lib.DagRank * nr)(*[s.dag_rank() for s in stores])
+    _lib.check(rt.lib.blrqr_tiled_dag_reset(nr, C.addressof(ranks), _lib.stream_ptr()), "tiled_dag_reset")
+    return ranks
+
+
+def _run(stores, ranks, peers, rank_ids, world, nctas=None):
+    from . import _lib
+    from .factorize import DAG_TIMEOUT_S
+    rt = stores[0].rt
+    g = stores[0].g
+    ws, per, nct = rt.workspace(g.b, g.cap, 0, nctas)
+    nr = len(stores)
+    ids = (C.c_int * nr)(*rank_ids)
+    pa = (_lib.Peer * world)(*peers) if world > 1 else None
+    _lib.check(rt.lib.blrqr_tiled_run_dag_multi(
+        world, nr, C.addressof(ids), C.addressof(ranks), C.addressof(pa) if pa is not None else None,
+        stores[0].cfg.epsilon, ws, per, nct, DAG_TIMEOUT_S, rt.status.data_ptr(), rt.flops.data_ptr(),
+        _lib.stream_ptr()), "tiled_run_dag_multi")
+
+
+def factorize_peer_dag_emulated(grid, cfg, world: int, stores=None):
+    """All `world` ranks of the peer-DAG protocol in ONE persistent launch on
+    this GPU (CTA block r runs rank r's DAG; pushes go to the other ranks'
+    copies on the same device).  Each rank gets its own clone of ``grid``.
+    This exercises the exact device protocol -- push tasks, remote releases,
+    per-rank DAGs -- without ranks in separate kernels waiting on one another.
+    Returns the stores (rank r's owned columns hold R-tilde)."""
+    if stores is None:
+        stores = [PeerDagStore(grid.clone(), cfg, world, r) for r in range(world)]
+    else:
+        for s in stores:
+            s.reset(grid.clone())
+    peers = [s.local_peer() for s in stores]
+    ranks = _launch(stores, peers, list(range(world)), world)
+    _run(stores, ranks, peers, list(range(world)), world)
+    return stores
+
+
+class PeerDagRank:
+    """One process per GPU: this rank's PeerDagStore plus the other ranks'
+    memory opened through CUDA IPC (exchanged once with all_gather_object)."""
+
+    def __init__(self, grid, cfg, world: int, rank: int, group=None):
+        import torch.distributed as dist
+        from . import _lib
+
+        self.store = PeerDagStore(grid, cfg, world, rank)
+        self.world, self.rank = world, rank
+        self.group = group
+        lib = self.store.rt.lib
+        _lib.check(lib.blrqr_enable_peer_access(), "enable_peer_access")
+        mine = []
+        for t in self.store.peer_tensors():
+            h = (C.c_char * 64)()
+            off = C.c_int64(0)
+            _lib.check(lib.blrqr_ipc_handle(t.data_ptr(), C.addressof(h), C.byref(off)), "ipc_handle")
+            mine.append((bytes(h), int(off.value)))
+        allh = [None] * world
+        dist.all_gather_object(allh, (mine, self.store.n), group=group)
+        self._opened = []
+        self.peers = []
+        for r in range(world):
+            if r == rank:
+                self.peers.append(self.store.local_peer())
+                continue
+            ptrs = []
+            for hb, off in allh[r][0]:
+                base = C.c_void_p()
+                hbuf = (C.c_char * 64).from_buffer_copy(hb)
+                _lib.check(lib.blrqr_ipc_open(C.addressof(hbuf), C.byref(base)), "ipc_open")
+                self._opened.append(base.value)
+                ptrs.append(base.value + off)
+            self.peers.append(self.store._peer(ptrs, allh[r][1]))
+
+    def run(self, grid=None, nctas=None):
+        """Reset (every rank, then a barrier: no push may land in a rank that
+        has not re-armed), then this rank's persistent launch (no host sync)."""
+        import torch.distributed as dist
+        if grid is not None:
+            self.store.reset(grid)
+        ranks = _launch([self.store], self.peers, [self.rank], self.world)
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)
+        _run([self.store], ranks, self.peers, [self.rank], self.world, nctas)
+        return self.store
+
+    def close(self):
+        lib = self.store.rt.lib
+        for b in self._opened:
+            lib.blrqr_ipc_close(b)
+        self._opened = []

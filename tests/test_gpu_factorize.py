@@ -231,6 +231,51 @@ def test_distributed_gpu_store_emulated_ranks(pk, world):
             assert torch.equal(st.rf.pool[t0:t0 + b * b], ref.rf.pool[t0:t0 + b * b])
 
 
+@pytest.mark.parametrize("tag,world", [("exp512", 1), ("exp512", 2), ("exp512", 3), ("C1", 4), ("C1", 8)])
+def test_peer_dag_emulated_bitwise(pk, tag, world):
+    """Peer-DAG multi-GPU protocol (per-rank dynamic DAGs, reflector pushes
+    into the peers' stores, remote releases by system-scope atomics) with
+    every rank hosted by ONE cooperative launch on this GPU: the owners'
+    R-tilde columns and reflectors, and the pushed copies on every other
+    rank, equal the single-GPU dynamic run bit for bit."""
+    import torch
+    from paper_2208_06194_b200 import distributed as D
+    from paper_2208_06194_b200.device import DeviceGrid
+    from paper_2208_06194_b200.factorize import factorize_device
+    z, meta, dense = _input(tag)
+    n, b, eps = meta["n"], meta["b"], meta["eps"]
+    g = schedule.dense_to_blr(dense, b, oblr.weak_map(n // b, n // b), eps)
+    dg = DeviceGrid.from_host(_to_pkg(pk, g))
+    cfg = pk.ToleranceConfig(eps)
+    ref = factorize_device("tiled-hh", dg, cfg, clone=True, scheduler="dag")
+    stores = D.factorize_peer_dag_emulated(dg, cfg, world)
+    torch.cuda.synchronize()
+    pk._lib.runtime().harvest()
+    q, p = ref.g.q, ref.g.p
+    for j in range(q):
+        st = stores[D.column_owner(j, world)]
+        for i in range(p):
+            c = i * q + j
+            o = int(ref.g.off_u_host[c])
+            if ref.g.kind_host[i, j]:
+                r_ = int(ref.g.rank[c])
+                assert int(st.g.rank[c]) == r_, (i, j)
+                assert torch.equal(st.g.pool[o:o + b * r_], ref.g.pool[o:o + b * r_]), (i, j)
+                o2 = int(ref.g.off_v_host[c])
+                assert torch.equal(st.g.pool[o2:o2 + b * r_], ref.g.pool[o2:o2 + b * r_]), (i, j)
+            else:
+                assert torch.equal(st.g.pool[o:o + b * b], ref.g.pool[o:o + b * b]), (i, j)
+    for st in stores:  # every rank holds every column's reflectors (owned or pushed)
+        assert torch.equal(st.rf.yrank, ref.rf.yrank)
+        for c in np.nonzero(ref.rf.t_off_host >= 0)[0]:
+            t0 = int(ref.rf.t_off_host[c])
+            assert torch.equal(st.rf.pool[t0:t0 + b * b], ref.rf.pool[t0:t0 + b * b])
+        for c in np.nonzero(ref.rf.y_off_host >= 0)[0]:
+            if int(ref.rf.yrank[c]) < 0:
+                y0 = int(ref.rf.y_off_host[c])
+                assert torch.equal(st.rf.pool[y0:y0 + b * b], ref.rf.pool[y0:y0 + b * b])
+
+
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("method", ["blocked-hh", "mgs"])
 def test_distributed_column_stores_emulated_ranks(pk, method, world):
