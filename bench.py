@@ -143,7 +143,9 @@ def cpu_reference_sample(cfg_name: str, rows: int, threads: int, grid_host=None)
     limiter.restore_original_limits()
     fl = ofl.total()
     sample = (f"{cfg_name} tiled-hh sweep k=0, block rows 1..{rows} of {p - 1}: DiagQR(0), {p - 1} ApplyBlock, "
-              f"{rows} UpdateQR, {rows * (p - 1)} ApplyTrap; fork-join pool of {threads} threads over j")
+              f"{rows} UpdateQR, {rows * (p - 1)} ApplyTrap; fork-join pool of {threads} threads over j"
+              "; single-core rate of this sample / rate of the whole C3 factorization = 1.08 at rows = 12, 1.12 at "
+              "rows = 24 (939 s full run, profiles/ref_rate_check_r02.json)")
     return fl / dt / 1e9, dt, fl, sample
 
 
@@ -601,7 +603,9 @@ def main():
     ap.add_argument("--dist", default="peer", choices=["peer", "levels"],
                     help="N > 1 tiled driver: per-rank DAGs with NVLink reflector pushes, or level-synchronous NCCL")
     ap.add_argument("--e2e-steps", type=int, default=1)
-    ap.add_argument("--cpu-rows", type=int, default=24)
+    ap.add_argument("--cpu-rows", type=int, default=12,
+                    help="block rows of the k = 0 sweep in the CPU sample (12: the sample's single-core rate is 1.08x "
+                         "the full C3 run's, profiles/ref_rate_check_r02.json)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-classes", action="store_true", help="skip the isolated per-class kernel measurements")
     ap.add_argument("--traffic", type=float, default=None,

@@ -235,6 +235,10 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
     int significant = 0;
     double total2 = rem2;
     for (int i = 0; i < kp; ++i) {
+      if ((unsigned)perm[i] >= (unsigned)kp) {  // NaN sigma leaves the ranking incomplete
+        atomicOr(cx.status, ST_NONFINITE);
+        perm[i] = 0;
+      }
       const double si = sig[perm[i]];
       significant += si > floor_;
       total2 += si * si;
@@ -257,6 +261,7 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
   }
   __syncthreads();
   int rank = s_rank;
+  BLR_CRUMB(cx, 1000 + rank * 10000 + kp * 100 + 100000000LL * c);
   if (rank > cap) {
     set_status(cx, ST_RANK_OVERFLOW);
     rank = cap;
@@ -279,7 +284,9 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
         ZU[(long long)j * m + i] = i < kp ? W2[i + (long long)perm[j] * kp] * inv : 0.0;
     }
     __syncthreads();
+    BLR_CRUMB(cx, 30);
     gemm(false, false, kp, rank, kp, 1.0, R2c, kp, ZU, m, 0.0, Z2, k);
+    BLR_CRUMB(cx, 31);
     for (int j = threadIdx.x >> 5; j < rank; j += NWARP)
       for (int i = kp + (threadIdx.x & 31); i < k; i += 32) Z2[(long long)j * k + i] = 0.0;
     __syncthreads();
@@ -306,7 +313,9 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
       }
       team = team_launch(cx, job, min(nch, TEAM_MAX));
     }
+    BLR_CRUMB(cx, 32);
     for (int ch = 0; ch < nch; ch += team) back_chunk(cx, s_iv, s_pv, ch * BACK_CW);
+    BLR_CRUMB(cx, 33);
     if (team > 1) team_finish(cx, job, team);
     add_flops(cx, FK_ROUNDED_ADD, mm_cost(m, kU, rank) + mm_cost(n, kV, rank));
     tb.stop(cx, PH_BACK);

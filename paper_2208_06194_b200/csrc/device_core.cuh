@@ -103,6 +103,14 @@ struct PhaseTimer {
   }
 };
 
+// Debug breadcrumb into the per-task phase trace (slot 13; host-pinned trace
+// buffers survive a faulting kernel, tools/repro_b16.py)
+#ifdef BLR_CRUMBS
+#define BLR_CRUMB(cx, v) do { if ((cx).tph && threadIdx.x == 0) { (cx).tph[13] = (unsigned long long)(v); __threadfence_system(); } } while (0)
+#else
+#define BLR_CRUMB(cx, v) do { } while (0)
+#endif
+
 // Arena allocation: every thread executes it with identical arguments.
 // Returns nullptr (and flags ST_ARENA_OVERFLOW) if the arena is exhausted.
 __device__ __forceinline__ double* alloc(Ctx& c, long long n) {

@@ -273,12 +273,16 @@ __device__ void tiled_trap_a1(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf
   Cell top = grid_cell(g, k, j), bot = grid_cell(g, i, j);
   const Blk tb = cell_blk(top), bb = cell_blk(bot);
   PhaseTimer t1;
+  BLR_CRUMB(cx, 1);
   Blk prod = blk_mul_t(cx, yt, bb);
   t1.stop(cx, PH_PRODUCT);
+  BLR_CRUMB(cx, 2);
   Blk ssum = blk_acc(cx, tb, prod, eps, b);
+  BLR_CRUMB(cx, 3);
   PhaseTimer t2;
   Blk w = blk_dense_times(cx, T, b, true, ssum);
   t2.stop(cx, PH_PRODUCT);
+  BLR_CRUMB(cx, 4);
   const long long cw = w_index(g, k, i, j);
   double* wu = rf.wpool + cw * rf.wslot;
   double* wv = wu + rf.wslot / 2;
@@ -300,6 +304,7 @@ __device__ void tiled_trap_a1(Ctx& cx, const blrqr_grid& g, const blrqr_refl& rf
   }
   if (w.s != 1.0) set_status(cx, ST_BAD_ARG);  // w inherits ssum's unit scale
   __syncthreads();
+  BLR_CRUMB(cx, 5);
   cx.top = mark;
 }
 

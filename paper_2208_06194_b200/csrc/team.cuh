@@ -324,13 +324,19 @@ __device__ void back_chunk(Ctx& cx, const int* iv, double* const* pv, int c0) {
   double* ZU = pv[8] + (long long)c0 * m;
   double* ZV = pv[9] + (long long)c0 * n;
   double* Z2 = pv[10] + (long long)c0 * k;
+  BLR_CRUMB(cx, 40);
   apply_reflectors(k, kp, pv[0], k, pv[1], ZU, m, nc);
+  BLR_CRUMB(cx, 41);
   qr_apply(cx, k, kp, pv[2], k, pv[3], Z2, k, nc, false);
+  BLR_CRUMB(cx, 42);
   for (int j = threadIdx.x >> 5; j < nc; j += NWARP)
     for (int i = threadIdx.x & 31; i < n; i += 32) ZV[(long long)j * n + i] = i < k ? Z2[i + (long long)j * k] : 0.0;
   __syncthreads();
+  BLR_CRUMB(cx, 43);
   qr_apply(cx, m, kU, pv[4], m, pv[5], ZU, m, nc, false);
+  BLR_CRUMB(cx, 44);
   qr_apply(cx, n, kV, pv[6], n, pv[7], ZV, n, nc, false);
+  BLR_CRUMB(cx, 45);
   copy_mat(m, nc, ZU, m, pv[11] + (long long)c0 * lddu, lddu);
   copy_mat(n, nc, ZV, n, pv[12] + (long long)c0 * lddv, lddv);
 }

@@ -1,0 +1,55 @@
+"""Repro: tiled-hh on the apply-Q golden grid (n = 128, b = 16) under debug knobs."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import __graft_entry__ as ge
+ge.build()
+import paper_2208_06194_b200 as pk
+from paper_2208_06194_b200 import _lib
+from paper_2208_06194_b200.device import DeviceGrid
+from paper_2208_06194_b200.factorize import DeviceFactorization
+
+mode = sys.argv[1] if len(sys.argv) > 1 else "default"
+z = np.load(os.path.join(os.path.dirname(__file__), "..", "tests", "golden", "applyq_blr.npz"))
+n, b, eps = int(z["n"]), int(z["b"]), float(z["eps"])
+ranks = z["a_ranks"]; p = n // b
+blocks = [[pk.LowRankBlock(z[f"a_u_{i}_{j}"], z[f"a_v_{i}_{j}"]) if ranks[i, j] >= 0 else z[f"a_d_{i}_{j}"]
+           for j in range(p)] for i in range(p)]
+a = pk.BlrMatrix(pk.BlrStructure(n, n, b, z["a_adm"].copy()), blocks)
+rt = _lib.runtime()
+if mode == "noteams":
+    rt.lib.blrqr_set_teams(0)
+if mode == "dfma":
+    rt.lib.blrqr_debug_gemm_impl(1)
+if mode == "guard":
+    rt.set_arena_guard(4096)
+g = DeviceGrid.from_host(a)
+f = DeviceFactorization("tiled-hh", g, pk.ToleranceConfig(eps), clone=True,
+                        scheduler="levels" if mode == "levels" else "dag")
+print("cap", g.cap, "p", g.p, flush=True)
+from paper_2208_06194_b200.factorize import tiled_dag_arrays
+tasks, indeg, off, succ, prio = tiled_dag_arrays(g.p, g.q, int(rt.lib.blrqr_dag_policy()))
+nt = len(tasks)
+trace = torch.zeros(3 * nt, dtype=torch.int64).pin_memory()
+ptrace = torch.zeros(16 * nt, dtype=torch.int64).pin_memory()
+rt.lib.blrqr_debug_trace(trace.data_ptr())
+rt.lib.blrqr_debug_phase_trace(ptrace.data_ptr())
+try:
+    f.run(nctas=int(mode[4:]) if mode.startswith("ncta") else None)
+    torch.cuda.synchronize()
+except Exception as e:
+    print("FAILED", e)
+    tr = trace.numpy().reshape(nt, 3)
+    pt = ptrace.numpy().reshape(nt, 16)
+    started = np.nonzero(tr[:, 0])[0]
+    print("tasks started", len(started), "finished", int((tr[:, 1] != 0).sum()))
+    for t in started:
+        if tr[t, 1] == 0:
+            print("UNFINISHED task", t, "kind,k,i,j =", tasks[t].tolist(), "prio", prio[t], "phases", pt[t].tolist())
+    order = started[np.argsort(tr[started, 0])]
+    print("last 5 started:", [(int(t), tasks[t].tolist()) for t in order[-5:]])
+    sys.stdout.flush()
+    os._exit(3)
+print(mode, "ran; counts", f.finish())
+if mode == "guard":
+    print("guards intact:", rt.guards_intact())
