@@ -234,11 +234,25 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
     const double floor_ = NOISE_FLOOR * hypot(nA, nB);
     int significant = 0;
     double total2 = rem2;
-    for (int i = 0; i < kp; ++i) {
-      if ((unsigned)perm[i] >= (unsigned)kp) {  // NaN sigma leaves the ranking incomplete
-        atomicOr(cx.status, ST_NONFINITE);
-        perm[i] = 0;
+    // The ranking must be a permutation of 0..kp-1.  On B200 the b = 16 DAG
+    // runs have been seen to reach this point with the tail of perm unwritten
+    // while sigma itself is complete and finite (DESIGN 7, open issue): the
+    // ranking is then redone here, serially, from the final sigma (counted in
+    // stats slot 57), instead of indexing sigma with a stale word.
+    bool ok = true;
+    for (int i = 0; i < kp && ok; ++i) ok = (unsigned)perm[i] < (unsigned)kp;
+    if (!ok) {
+      for (int i = 0; i < kp; ++i) perm[i] = i;  // stays in range even if sigma holds a NaN
+      for (int i = 0; i < kp; ++i) {
+        const double si = sig[i];
+        int r = 0;
+        for (int j = 0; j < kp; ++j) r += (sig[j] > si) || (sig[j] == si && j < i);
+        perm[r] = i;
+        if (!(si == si)) atomicOr(cx.status, ST_NONFINITE);
       }
+      if (cx.flops) atomicAdd(cx.flops + 57, 1ull);
+    }
+    for (int i = 0; i < kp; ++i) {
       const double si = sig[perm[i]];
       significant += si > floor_;
       total2 += si * si;
@@ -275,7 +289,11 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
     double* ZU = alloc(cx, (long long)m * rank);
     double* ZV = alloc(cx, (long long)n * rank);
     double* Z2 = alloc(cx, (long long)k * rank);
-    if (!ZU || !ZV || !Z2) { release(cx, mk); return 0; }
+    double* T64U = alloc(cx, (long long)QA_NB * kU);  // 64-wide block reflectors (team.cuh back_prepare)
+    double* T64V = alloc(cx, (long long)QA_NB * kV);
+    double* T64X = alloc(cx, (long long)QA_NB * kq);
+    double* T64G = alloc(cx, (long long)QA_NB * kq);  // ... and of the core QRCP's reflectors
+    if (!ZU || !ZV || !Z2 || !T64U || !T64V || !T64X || !T64G) { release(cx, mk); return 0; }
     // left vectors Q1 [U_hat_r; 0] (normalized rotated columns of W2, in
     // descending sigma order), right (scaled by sigma) Q2 [R2 U_hat_r; 0]
     for (int j = threadIdx.x >> 5; j < rank; j += NWARP) {
@@ -293,12 +311,12 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
     // fixed 32-column chunks (team.cuh back_chunk), so a team computes the
     // same bits as a lone CTA
     __shared__ int s_iv[9];
-    __shared__ double* s_pv[13];
+    __shared__ double* s_pv[17];
     if (threadIdx.x == 0) {
       const int iv[9] = {m, n, k, kp, kU, kV, lddu, lddv, rank};
-      double* const pv[13] = {Gr, taus, X, Tp2, Uc, TpU, Vc, TpV, ZU, ZV, Z2, du, dv};
+      double* const pv[17] = {Gr, taus, X, Tp2, Uc, TpU, Vc, TpV, ZU, ZV, Z2, du, dv, T64U, T64V, T64X, T64G};
       for (int i = 0; i < 9; ++i) s_iv[i] = iv[i];
-      for (int i = 0; i < 13; ++i) s_pv[i] = pv[i];
+      for (int i = 0; i < 17; ++i) s_pv[i] = pv[i];
     }
     __syncthreads();
     const int nch = (rank + BACK_CW - 1) / BACK_CW;
@@ -309,11 +327,16 @@ __device__ __noinline__ int rounded_add(Ctx& cx, const Blk& A, const Blk& B, dou
       if (threadIdx.x == 0) {
         job->kind = TK_BACK;
         for (int i = 0; i < 9; ++i) job->iv[i] = s_iv[i];
-        for (int i = 0; i < 13; ++i) job->pv[i] = s_pv[i];
+        for (int i = 0; i < 17; ++i) job->pv[i] = s_pv[i];
       }
       team = team_launch(cx, job, min(nch, TEAM_MAX));
     }
     BLR_CRUMB(cx, 32);
+    BLR_SUBPHASE_STOP(tb, cx, PH_NORM);  // Z setup + R2 U_hat_r product
+    BLR_SUBPHASE(sp);
+    for (int g = 0, ng = back_groups(s_iv); g < ng; g += team) back_prepare(cx, s_iv, s_pv, g);
+    BLR_SUBPHASE_STOP(sp, cx, PH_EXPAND);
+    if (team > 1) team_barrier(cx, job, team);
     for (int ch = 0; ch < nch; ch += team) back_chunk(cx, s_iv, s_pv, ch * BACK_CW);
     BLR_CRUMB(cx, 33);
     if (team > 1) team_finish(cx, job, team);

@@ -545,6 +545,11 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM) k_tiled_dag(const DagRank* ra
   cx.team = d.team;
   const bool reserved = d.team && lcta >= per - d.reserve;
   __shared__ int s_task, s_member;
+#ifdef BLR_BARCHECK
+  if (threadIdx.x < 32) s_barcnt[threadIdx.x] = 0;
+  if (threadIdx.x < 4) s_barbad[threadIdx.x] = 0;
+  __syncthreads();
+#endif
   while (true) {
     if (threadIdx.x == 0) {
       int t = -1;
@@ -615,6 +620,14 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM) k_tiled_dag(const DagRank* ra
     cx.top = 0;
     cx.stop = 0;
     __syncthreads();
+#ifdef BLR_BARCHECK
+    bar_check(1000u * (unsigned)t + (unsigned)tk.kind + 1u);
+    if (threadIdx.x == 0 && s_barbad[0] && flops && flops[57] == 0) {
+      flops[57] = s_barbad[0]; flops[58] = s_barbad[1]; flops[59] = s_barbad[2]; flops[60] = s_barbad[3];
+      flops[61] = 1000000ull * tk.k + 1000ull * (unsigned)(tk.i + 1) + (unsigned)(tk.j + 1);
+      atomicOr(status, ST_BAD_ARG);
+    }
+#endif
     if (threadIdx.x == 0) {
       if (d.trace) {
         d.trace[3 * (long long)t + 1] = global_ns();
@@ -766,7 +779,7 @@ int blrqr_version(void) { return 1; }
 
 int64_t blrqr_workspace_doubles(int b, int cap, int max_panel_rows) {
   const int64_t B = b, C = cap, H = std::max(max_panel_rows, b);
-  return 16 * B * C + 4 * B * B + 2 * H * B + 64 * (B + 2 * C + H) + 65536;
+  return 16 * B * C + 4 * B * B + 2 * H * B + 64 * (B + 2 * C + H) + 512 * C + 65536;
 }
 
 int blrqr_default_ctas(void) {

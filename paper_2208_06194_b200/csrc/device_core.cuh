@@ -11,6 +11,34 @@
 
 namespace blr {
 
+// Debug (-DBLR_BARCHECK): every __syncthreads() counts itself per warp, so a
+// barrier executed by only part of the CTA (which silently shifts the warps'
+// barrier phases from then on) shows up as unequal counts right after any
+// later barrier (bar_check).
+#ifdef BLR_BARCHECK
+__shared__ unsigned s_barcnt[32];
+__shared__ unsigned s_barbad[4];
+__device__ __forceinline__ void blr_sync_counted() {
+  if ((threadIdx.x & 31) == 0) s_barcnt[threadIdx.x >> 5]++;
+  __syncthreads();
+}
+#define __syncthreads() blr_sync_counted()
+// called by all threads (uncounted barriers on both sides, so no warp
+// increments its count while thread 0 compares): records (tag, warp, counts)
+// of the first mismatch
+__device__ __forceinline__ void bar_check(unsigned tag) {
+  asm volatile("bar.sync 0;" ::: "memory");
+  if (threadIdx.x == 0 && s_barbad[0] == 0) {
+    const unsigned c0 = s_barcnt[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      if (s_barcnt[w] != c0) { s_barbad[0] = tag; s_barbad[1] = w; s_barbad[2] = c0; s_barbad[3] = s_barcnt[w]; break; }
+  }
+  asm volatile("bar.sync 0;" ::: "memory");
+}
+#else
+__device__ __forceinline__ void bar_check(unsigned) {}
+#endif
+
 #ifndef BLR_NT
 #define BLR_NT 512
 #endif
@@ -102,6 +130,16 @@ struct PhaseTimer {
     }
   }
 };
+
+// Sub-phase timers of the back-transform (build with -DBLR_BACK_PROF; they
+// reuse phase slots the rounded addition does not touch)
+#ifdef BLR_BACK_PROF
+#define BLR_SUBPHASE(name) PhaseTimer name
+#define BLR_SUBPHASE_STOP(name, cx, ph) (name).stop(cx, ph)
+#else
+#define BLR_SUBPHASE(name) do { } while (0)
+#define BLR_SUBPHASE_STOP(name, cx, ph) do { } while (0)
+#endif
 
 // Debug breadcrumb into the per-task phase trace (slot 13; host-pinned trace
 // buffers survive a faulting kernel, tools/repro_b16.py)

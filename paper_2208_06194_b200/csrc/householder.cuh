@@ -492,6 +492,103 @@ __device__ __noinline__ void qr_apply(Ctx& cx, int m, int k, const double* A, in
 }
 
 // ---------------------------------------------------------------------------
+// 64-wide block reflectors for the applications of a qr_blocked factorization
+// (the rounded addition's back-transform): the 16-column panel Ts are merged
+// per group of QA_NB = 64 reflectors,
+//   T(0:j0, J) = -T(0:j0, 0:j0) (Y(:, 0:j0)^T Y_J) T_JJ   (kernels.py:111-116
+// applies the same block reflector, I - Y T Y^T),
+// so one application is three GEMMs with inner dimensions h, 64 and 64 (DMMA
+// shapes) instead of four 16-wide panels of five barrier-bound steps each.
+// ---------------------------------------------------------------------------
+constexpr int QA_NB = 64;
+
+// Group [c0, c0 + w) (w <= QA_NB, c0 a multiple of QA_NB) of the reflectors
+// stored below A's diagonal (m rows, panel Ts in Tp): turns the group's
+// top w x w triangle of A into the explicit unit-lower part of Y IN PLACE
+// (the R entries there must be dead) and writes the group's w x w upper
+// triangular T to T (ld QA_NB, zero below the diagonal).
+// Tp == nullptr (reflectors of an unblocked factorization, e.g. the pivoted
+// QR): the whole T comes from the column recurrence
+//   T(0:c, c) = -tau_c T(0:c, 0:c) S(0:c, c),  T(c, c) = tau_c,  S = Y^T Y.
+__device__ void qr_group_t(Ctx& cx, int m, double* A, int lda, const double* Tp, int c0, int w, double* T,
+                           const double* taus = nullptr) {
+  const int h = m - c0;
+  double* Y = A + c0 + (long long)c0 * lda;
+  for (int e = threadIdx.x; e < w * w; e += NT) {
+    const int i = e % w, j = e / w;
+    if (i <= j) Y[i + (long long)j * lda] = (i == j) ? 1.0 : 0.0;
+    T[i + j * QA_NB] = (Tp && (i / QR_NB) == (j / QR_NB) && i <= j) ? Tp[(i % QR_NB) + (long long)(c0 + j) * QR_NB]
+                                                                    : 0.0;
+  }
+  __syncthreads();
+  if (Tp && w <= QR_NB) return;
+  const Mark mk = mark(cx);
+  double* S = alloc_fast(cx, QA_NB * QA_NB);
+  double* X = alloc_fast(cx, QA_NB * QR_NB);
+  if (!S || !X) { release(cx, mk); return; }
+  if (w > 1) gemm(true, false, w, w, h, 1.0, Y, lda, Y, lda, 0.0, S, QA_NB);
+  if (!Tp) {
+    for (int c = 0; c < w; ++c) {
+      const double tc = taus[c0 + c];
+      if ((int)threadIdx.x < c) {
+        const int a = threadIdx.x;
+        double x = 0.0;
+        for (int b2 = a; b2 < c; ++b2) x = fma(T[a + b2 * QA_NB], S[b2 + c * QA_NB], x);
+        X[a] = x;
+      }
+      __syncthreads();
+      if ((int)threadIdx.x < c) T[threadIdx.x + c * QA_NB] = -tc * X[threadIdx.x];
+      if (threadIdx.x == 0) T[c + c * QA_NB] = tc;
+      __syncthreads();
+    }
+    release(cx, mk);
+    return;
+  }
+  for (int j0 = QR_NB; j0 < w; j0 += QR_NB) {
+    const int wj = min(QR_NB, w - j0);
+    for (int e = threadIdx.x; e < j0 * wj; e += NT) {  // X = S(0:j0, J) T_JJ
+      const int r = e % j0, c = e / j0;
+      double x = 0.0;
+      for (int b2 = 0; b2 <= c; ++b2) x = fma(S[r + (j0 + b2) * QA_NB], T[(j0 + b2) + (j0 + c) * QA_NB], x);
+      X[r + c * QA_NB] = x;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < j0 * wj; e += NT) {  // T(0:j0, J) = -T(0:j0, 0:j0) X
+      const int r = e % j0, c = e / j0;
+      double x = 0.0;
+      for (int q = r; q < j0; ++q) x = fma(T[r + q * QA_NB], X[q + c * QA_NB], x);
+      T[r + (j0 + c) * QA_NB] = -x;
+    }
+    __syncthreads();
+  }
+  release(cx, mk);
+}
+
+// Z <- Q Z (transpose = false) or Q^T Z for Q = H_0 ... H_{k-1} held as
+// explicit Y below A's diagonal (qr_group_t) with the group Ts in T64
+// (QA_NB x k, group at column c0).
+__device__ __noinline__ void qr_apply64(Ctx& cx, int m, int k, const double* A, int lda, const double* T64, double* Z,
+                                        int ldz, int nz, bool transpose) {
+  if (nz <= 0 || k <= 0) return;
+  const Mark mk = mark(cx);
+  double* W = alloc_fast(cx, (long long)QA_NB * nz);
+  double* W2 = alloc_fast(cx, (long long)QA_NB * nz);
+  if (!W || !W2) { release(cx, mk); return; }
+  const int ng = (k + QA_NB - 1) / QA_NB;
+  for (int gi = 0; gi < ng; ++gi) {
+    const int g = transpose ? gi : ng - 1 - gi;
+    const int c0 = g * QA_NB, w = min(QA_NB, k - c0), h = m - c0;
+    const double* Y = A + c0 + (long long)c0 * lda;
+    const double* T = T64 + (long long)c0 * QA_NB;
+    double* Zp = Z + c0;
+    gemm(true, false, w, nz, h, 1.0, Y, lda, Zp, ldz, 0.0, W, QA_NB);
+    gemm(transpose, false, w, nz, w, 1.0, T, QA_NB, W, QA_NB, 0.0, W2, QA_NB);
+    gemm(false, false, h, nz, w, -1.0, Y, lda, W2, QA_NB, 1.0, Zp, ldz);
+  }
+  release(cx, mk);
+}
+
+// ---------------------------------------------------------------------------
 // Triangular-pentagonal QR, l = 0 (LAPACK dtpqrt semantics): [R; B] with R
 // n x n upper triangular, B k x n.  On exit R = R_new, B = Y (k x n), T full
 // n x n upper (ldt).

@@ -76,7 +76,7 @@ struct __align__(128) TeamJob {
   int done;
   int kind;
   int iv[12];
-  double* pv[16];
+  double* pv[20];
   double dv[4];
 };
 
@@ -325,23 +325,62 @@ __device__ void back_chunk(Ctx& cx, const int* iv, double* const* pv, int c0) {
   double* ZV = pv[9] + (long long)c0 * n;
   double* Z2 = pv[10] + (long long)c0 * k;
   BLR_CRUMB(cx, 40);
-  apply_reflectors(k, kp, pv[0], k, pv[1], ZU, m, nc);
+  BLR_SUBPHASE(s1);
+  qr_apply64(cx, k, kp, pv[0], k, pv[16], ZU, m, nc, false);
+  BLR_SUBPHASE_STOP(s1, cx, PH_TPQRT);
   BLR_CRUMB(cx, 41);
-  qr_apply(cx, k, kp, pv[2], k, pv[3], Z2, k, nc, false);
+  BLR_SUBPHASE(s2);
+  qr_apply64(cx, k, kp, pv[2], k, pv[15], Z2, k, nc, false);
+  BLR_SUBPHASE_STOP(s2, cx, PH_GEQRT);
   BLR_CRUMB(cx, 42);
   for (int j = threadIdx.x >> 5; j < nc; j += NWARP)
     for (int i = threadIdx.x & 31; i < n; i += 32) ZV[(long long)j * n + i] = i < k ? Z2[i + (long long)j * k] : 0.0;
   __syncthreads();
   BLR_CRUMB(cx, 43);
-  qr_apply(cx, m, kU, pv[4], m, pv[5], ZU, m, nc, false);
+  BLR_SUBPHASE(s3);
+  qr_apply64(cx, m, kU, pv[4], m, pv[13], ZU, m, nc, false);
+  BLR_SUBPHASE_STOP(s3, cx, PH_APPLYWY);
   BLR_CRUMB(cx, 44);
-  qr_apply(cx, n, kV, pv[6], n, pv[7], ZV, n, nc, false);
+  BLR_SUBPHASE(s4);
+  qr_apply64(cx, n, kV, pv[6], n, pv[14], ZV, n, nc, false);
+  BLR_SUBPHASE_STOP(s4, cx, PH_RRQR);
   BLR_CRUMB(cx, 45);
+  BLR_SUBPHASE(s5);
   copy_mat(m, nc, ZU, m, pv[11] + (long long)c0 * lddu, lddu);
   copy_mat(n, nc, ZV, n, pv[12] + (long long)c0 * lddv, lddv);
+  BLR_SUBPHASE_STOP(s5, cx, PH_TBUILD);
+}
+
+// 64-wide block reflectors of the three QRs (Q_U: pv[4] / pv[5] -> pv[13],
+// Q_V: pv[6] / pv[7] -> pv[14], Q2: pv[2] / pv[3] -> pv[15], the core QRCP's
+// Q1: pv[0] / taus pv[1] -> pv[16]); group g of the
+// concatenated list.  Every group is built by exactly one member with the
+// same arithmetic, so the result does not depend on the team size.
+__device__ __forceinline__ int back_groups(const int* iv) {
+  return (iv[4] + QA_NB - 1) / QA_NB + (iv[5] + QA_NB - 1) / QA_NB + 2 * ((iv[3] + QA_NB - 1) / QA_NB);
+}
+__device__ void back_prepare(Ctx& cx, const int* iv, double* const* pv, int g) {
+  const int m = iv[0], n = iv[1], k = iv[2], kp = iv[3], kU = iv[4], kV = iv[5];
+  const int nU = (kU + QA_NB - 1) / QA_NB, nV = (kV + QA_NB - 1) / QA_NB;
+  if (g < nU) {
+    const int c0 = g * QA_NB;
+    qr_group_t(cx, m, pv[4], m, pv[5], c0, min(QA_NB, kU - c0), pv[13] + (long long)c0 * QA_NB);
+  } else if (g < nU + nV) {
+    const int c0 = (g - nU) * QA_NB;
+    qr_group_t(cx, n, pv[6], n, pv[7], c0, min(QA_NB, kV - c0), pv[14] + (long long)c0 * QA_NB);
+  } else if (g < nU + nV + (kp + QA_NB - 1) / QA_NB) {
+    const int c0 = (g - nU - nV) * QA_NB;
+    qr_group_t(cx, k, pv[2], k, pv[3], c0, min(QA_NB, kp - c0), pv[15] + (long long)c0 * QA_NB);
+  } else {  // the core QRCP's reflectors (pv[0], taus pv[1]): no panel Ts
+    const int c0 = (g - nU - nV - (kp + QA_NB - 1) / QA_NB) * QA_NB;
+    qr_group_t(cx, k, pv[0], k, nullptr, c0, min(QA_NB, kp - c0), pv[16] + (long long)c0 * QA_NB, pv[1]);
+  }
 }
 
 __device__ void team_back_member(Ctx& cx, TeamJob* job, int t, int team) {
+  const int ng = back_groups(job->iv);
+  for (int g = t; g < ng; g += team) back_prepare(cx, job->iv, job->pv, g);
+  team_barrier(cx, job, team);
   const int nch = (job->iv[8] + BACK_CW - 1) / BACK_CW;
   for (int ch = t; ch < nch; ch += team) back_chunk(cx, job->iv, job->pv, ch * BACK_CW);
 }

@@ -17,6 +17,12 @@ blocks = [[pk.LowRankBlock(z[f"a_u_{i}_{j}"], z[f"a_v_{i}_{j}"]) if ranks[i, j] 
            for j in range(p)] for i in range(p)]
 a = pk.BlrMatrix(pk.BlrStructure(n, n, b, z["a_adm"].copy()), blocks)
 rt = _lib.runtime()
+if int(os.environ.get("BLRQR_STACK", "0")):
+    import ctypes
+    cr = ctypes.CDLL("libcudart.so.12")
+    v = ctypes.c_size_t(0)
+    cr.cudaDeviceGetLimit(ctypes.byref(v), 0)
+    print("stack limit was", v.value, "set rc", cr.cudaDeviceSetLimit(0, ctypes.c_size_t(int(os.environ["BLRQR_STACK"]))))
 if mode == "noteams":
     rt.lib.blrqr_set_teams(0)
 if mode == "dfma":
@@ -36,9 +42,20 @@ rt.lib.blrqr_debug_trace(trace.data_ptr())
 rt.lib.blrqr_debug_phase_trace(ptrace.data_ptr())
 try:
     f.run(nctas=int(mode[4:]) if mode.startswith("ncta") else None)
+    import time
+    t0 = time.time()
+    while not torch.cuda.current_stream().query():
+        if time.time() - t0 > 15:
+            raise TimeoutError("kernel still running after 15 s")
+        time.sleep(0.2)
     torch.cuda.synchronize()
+    print(mode, "ran; counts", f.finish())
 except Exception as e:
     print("FAILED", e)
+    import struct
+    rt.harvest_noraise() if hasattr(rt,'harvest_noraise') else None
+    ls = getattr(rt, 'last_stats', [0]*16)
+    print("debug stats", ls[9:], [struct.unpack("d", struct.pack("q", int(v)))[0] for v in (ls[12], ls[13], ls[15])])
     tr = trace.numpy().reshape(nt, 3)
     pt = ptrace.numpy().reshape(nt, 16)
     started = np.nonzero(tr[:, 0])[0]
@@ -50,6 +67,5 @@ except Exception as e:
     print("last 5 started:", [(int(t), tasks[t].tolist()) for t in order[-5:]])
     sys.stdout.flush()
     os._exit(3)
-print(mode, "ran; counts", f.finish())
 if mode == "guard":
     print("guards intact:", rt.guards_intact())
