@@ -728,9 +728,9 @@ static void init_kernels() {
 #define INIT_KERNELS() init_kernels()
 
 static int g_teams_enabled = 1;
-static int g_team_reserve = 16;  // dynamic scheduler: CTAs that only help critical-chain team jobs
+static int g_team_reserve = 8;   // dynamic scheduler: CTAs that only help critical-chain team jobs (r02 sweep: 8 best)
 static int g_dag_rings = DAG_RINGS;  // 2: the kind-based two-ring policy
-static int g_team_slack = 1 << 20;  // DAG tasks with unit-weight slack <= this may form teams (all by default: measured best)
+static int g_team_slack = 2;  // DAG tasks with unit-weight slack <= this may form teams (r02 sweep: 2 best; 1 << 20 = all)
 
 // Team-job table + ticket ring + two task counters, one per (device, stream)
 // so concurrent launches on different streams never share them (the host
