@@ -228,6 +228,14 @@ int blrqr_debug_gemm_impl(int impl);
  * stride out of the bump arena (callers size ws_per_cta accordingly and fill
  * the guard with a canary to detect out-of-arena writes).  0 = off. */
 int blrqr_debug_arena_guard(int64_t guard_doubles);
+/* Split arena: the first hot_doubles of every CTA's workspace stride are laid
+ * out contiguously over the CTAs at the start of ws (the rest follows, one
+ * cold stride per CTA), and blrqr_tiled_run_dag(_multi) pins that range in
+ * the persisting part of L2 (stream access-policy window) for its launch, so
+ * the scratch of typical rounded additions is not written back to HBM between
+ * reuses.  Same ws size and ws_per_cta as without the split; 0 = off. */
+int blrqr_set_arena_hot(int64_t hot_doubles);
+int64_t blrqr_arena_hot(void);
 /* The reference's tiled task DAG (scheduler.py:173-201: nodes in sweep order
  * tiled_sequential_tasks :127-138, edges last writer -> any later touch and
  * readers since the last write -> the next writer over the read/write sets of

@@ -98,6 +98,8 @@ _SIGS = {
     "blrqr_debug_gemm": ([_I, _I, _I, _I, _I, _P, _I, _P, _I, _P, _I, _I, _I, _P], _I),
     "blrqr_debug_gemm_impl": ([_I], _I),
     "blrqr_debug_arena_guard": ([_L], _I),
+    "blrqr_set_arena_hot": ([_L], _I),
+    "blrqr_arena_hot": ([], _L),
     "blrqr_panel_team": ([_I, _I, _I, _P, _P, _P, _P, _P, _P, _L, _I, _P, _P, _P], _I),
     "blrqr_tiled_dag": ([_I, _I, _P, _P, _P, _P, _P], _I),
     "blrqr_tiled_ref_dag": ([_I, _I, _P, _P, _P, _L], _L),
@@ -150,6 +152,9 @@ def check(rc: int, what: str) -> None:
     raise RuntimeError(f"{what}: CUDA error {rc - 1000 if rc >= 1000 else rc}")
 
 
+ARENA_HOT_DEFAULT = 0  # doubles per CTA pinned in L2 (0: plain per-CTA strides); see DESIGN 5d
+
+
 def require_cuda() -> torch.device:
     if not torch.cuda.is_available():
         raise RuntimeError("paper_2208_06194_b200 needs a CUDA device (sm_100a); no CPU fallback exists")
@@ -184,6 +189,9 @@ class Runtime:
         self._ws_per_cta = 0
         self.arena_guard = 0
         self._guard = (0, 0)
+        # split arena + L2 persistence of the hot scratch (blrqr_set_arena_hot), doubles per CTA
+        self.arena_hot = int(os.environ.get("BLRQR_ARENA_HOT", ARENA_HOT_DEFAULT))
+        check(self.lib.blrqr_set_arena_hot(self.arena_hot), "arena_hot")
         self._pinned = None
         self._pinned_ev = None
         self.dag_cache = {}
@@ -228,6 +236,8 @@ class Runtime:
         torch.cuda.synchronize()
         self.arena_guard = int(doubles)
         check(self.lib.blrqr_debug_arena_guard(self.arena_guard), "arena_guard")
+        # the canary zones assume one plain stride per CTA: no split while guarded
+        check(self.lib.blrqr_set_arena_hot(0 if self.arena_guard else self.arena_hot), "arena_hot")
 
     def guards_intact(self) -> bool:
         """True when every CTA's guard zone of the last workspace still holds the canary."""

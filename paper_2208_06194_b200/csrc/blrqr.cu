@@ -1332,6 +1332,49 @@ static void* launch_args_buf(cudaStream_t st, size_t bytes) {
   return b.first;
 }
 
+// Split arena + L2 persistence (tasks.cuh g_arena_hot).  hot_doubles = 0 turns
+// both off.  The window is applied by the DAG launch to its stream.
+static long long g_arena_hot_host = 0;
+extern "C" int blrqr_set_arena_hot(int64_t hot_doubles) {
+  if (hot_doubles < 0) return -1;
+  long long h = hot_doubles & ~31LL;
+  CK(cudaMemcpyToSymbol(g_arena_hot, &h, sizeof(long long)));
+  g_arena_hot_host = h;
+  return 0;
+}
+extern "C" int64_t blrqr_arena_hot(void) { return g_arena_hot_host; }
+
+// pins [ws, ws + bytes) in the persisting part of L2 for kernels launched on st
+static void l2_window(cudaStream_t st, const void* base, size_t bytes) {
+  static size_t set_aside = 0;
+  int dev = 0, max_persist = 0, max_win = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+  cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+  if (max_persist <= 0 || max_win <= 0) return;
+  cudaStreamAttrValue v;
+  memset(&v, 0, sizeof(v));
+  if (bytes == 0) {
+    v.accessPolicyWindow.num_bytes = 0;
+    cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v);
+    return;
+  }
+  if (set_aside != (size_t)max_persist) {
+    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)max_persist) != cudaSuccess) {
+      cudaGetLastError();
+      return;
+    }
+    set_aside = (size_t)max_persist;
+  }
+  const size_t win = std::min(bytes, (size_t)max_win);
+  v.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+  v.accessPolicyWindow.num_bytes = win;
+  v.accessPolicyWindow.hitRatio = win <= (size_t)max_persist ? 1.0f : (float)((double)max_persist / (double)win);
+  v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  if (cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v) != cudaSuccess) cudaGetLastError();
+}
+
 int blrqr_tiled_run_dag_multi(int world, int nranks, const int* rank_ids, const blrqr_dag_rank* ranks,
                               const blrqr_peer* peers, double eps, double* ws, int64_t ws_per_cta, int nctas,
                               double timeout_s, int* status, unsigned long long* flops, void* stream) {
@@ -1389,7 +1432,10 @@ int blrqr_tiled_run_dag_multi(int world, int nranks, const int* rank_ids, const 
   double* ws_arg = ws;
   long long wsp_arg = ws_per_cta;
   void* args[] = {&dr, &nr, &eps, &ws_arg, &wsp_arg, &status, &flops, const_cast<long long*>(&timeout_cycles)};
+  const long long hot = std::min(g_arena_hot_host, (long long)ws_per_cta / 2) & ~31LL;
+  if (hot > 0) l2_window(st, ws, (size_t)hot * (size_t)(per * nranks) * sizeof(double));
   CK(cudaLaunchCooperativeKernel((const void*)k_tiled_dag, dim3(per * nranks), dim3(NT), args, SMEM_BYTES, st));
+  if (hot > 0) l2_window(st, nullptr, 0);  // later launches on the stream are not windowed
   return 0;
 }
 

@@ -70,7 +70,9 @@ enum FlopKind : int {
 struct TeamCtx;
 
 struct Ctx {
-  double* base;            // this CTA's global (L2/HBM) arena
+  double* base;            // this CTA's global (L2/HBM) arena (its cold part when the arena is split)
+  double* hbase;           // hot part: the first `hot` doubles of the arena, contiguous over CTAs so that
+  long long hot;           //   one L2 access-policy window pins every CTA's hot scratch (0: no split)
   long long cap;           // doubles
   long long top;           // bump pointer (doubles), identical in all threads
   double* sbase;           // this CTA's shared-memory arena (dynamic smem)
@@ -153,11 +155,12 @@ struct PhaseTimer {
 // Returns nullptr (and flags ST_ARENA_OVERFLOW) if the arena is exhausted.
 __device__ __forceinline__ double* alloc(Ctx& c, long long n) {
   n = (n + 31) & ~31LL;    // 256-byte alignment
+  if (c.top < c.hot && c.top + n > c.hot) c.top = c.hot;  // does not fit the hot part: continue in the cold one
   if (c.top + n > c.cap) {
     set_status(c, ST_ARENA_OVERFLOW);
     return nullptr;
   }
-  double* p = c.base + c.top;
+  double* p = c.top < c.hot ? c.hbase + c.top : c.base + (c.top - c.hot);
   c.top += n;
   return p;
 }

@@ -438,6 +438,13 @@ __device__ __noinline__ void jacobi_smem(const Ctx& cx, int rows, int ncols, dou
     a = warp_sum(a);
     if (lane == 0) sigma[c] = sqrt(a);
   }
+  // sigma / perm are generic pointers into the shared arena (ST.E / LD.E, not
+  // STS / LDS); the CTA-scope fences make the stores performed before the
+  // barrier releases the readers (DESIGN 7: ranking tails were seen unwritten
+  // without them)
+#ifndef BLR_NO_TAIL_FENCE
+  __threadfence_block();
+#endif
   __syncthreads();
   for (int i = threadIdx.x; i < ncols; i += NT) {
     const double si = sigma[i];
@@ -448,6 +455,9 @@ __device__ __noinline__ void jacobi_smem(const Ctx& cx, int rows, int ncols, dou
     }
     perm[r] = i;
   }
+#ifndef BLR_NO_TAIL_FENCE
+  __threadfence_block();
+#endif
   __syncthreads();
 }
 

@@ -25,10 +25,19 @@ __device__ __forceinline__ Cell grid_cell(const blrqr_grid& g, int i, int j) {
 // fill them with a canary and detect out-of-arena writes (compute-sanitizer is
 // not available on the GPU pool).
 __device__ long long g_arena_guard = 0;
+// Split arena (blrqr_set_arena_hot): workspace layout [hot parts of all CTAs |
+// cold parts of all CTAs]; a CTA's first g_arena_hot doubles of scratch -- the
+// Uc / Vc panels and cores of a typical rounded addition -- then sit in one
+// contiguous range that the launch pins in L2 (persisting access-policy
+// window), instead of being written back to HBM between reuses.
+__device__ long long g_arena_hot = 0;
 
 __device__ __forceinline__ Ctx make_ctx(double* ws, long long ws_per_cta, int* status, unsigned long long* flops) {
   Ctx c;
-  c.base = ws + (long long)blockIdx.x * ws_per_cta;
+  const long long hot = min(g_arena_hot, ws_per_cta / 2) & ~31LL;
+  c.hot = hot;
+  c.hbase = ws + (long long)blockIdx.x * hot;
+  c.base = ws + (long long)gridDim.x * hot + (long long)blockIdx.x * (ws_per_cta - hot);
   c.cap = ws_per_cta - g_arena_guard;
   c.top = 0;
   c.sbase = dyn_smem;
