@@ -214,7 +214,13 @@ __device__ void qr_factor_panel(Ctx& cx, const QrMat& M, int c0, int w) {
   const int h = M.m - c0;
   const Mark pm = mark(cx);
   double* S = alloc_fast(cx, (long long)QR_NB * QR_NB);
-  double* P = salloc(cx, (long long)h * w);
+  // Shared-memory staging of the panel, for matrices of at least 32 rows.  On
+  // 16-row matrices (b = 16 grids) this path has produced box-dependent wrong
+  // results under the persistent DAG kernel on B200 (DESIGN 7: bisected with
+  // runtime knobs to exactly this staging; cause not understood), while the
+  // in-place path below is correct everywhere; nothing measurable is lost at
+  // that size.
+  double* P = M.m >= 32 ? salloc(cx, (long long)h * w) : nullptr;
   double* Y;
   double* Ap = M.A + c0 + (long long)c0 * M.lda;
   if (P) {  // stage the h x w panel in shared memory and factor it there
