@@ -87,9 +87,9 @@ def tiled_dag_arrays(p: int, q: int, policy: int = 0):
 
 SCHEDULERS = ("auto", "dag", "levels")
 # "auto": the persistent dynamic-DAG kernel from b = 32 on, the level scheduler
-# below.  At b = 16 the DAG kernel has produced box-dependent wrong results on
-# B200 (DESIGN 7, open issue: root cause not found; the level scheduler, same
-# task bodies, never has), and toy block sizes gain nothing from it.
+# below.  At b = 16 the DAG kernel produced box-dependent wrong results on
+# B200 until the 16-row panel staging was taken out (DESIGN 7); the level
+# scheduler never did, and toy block sizes gain nothing from the DAG kernel.
 DAG_MIN_B = 32
 
 
