@@ -10,7 +10,3 @@ for hot in 0 32768 65536 98304; do
   grep -E "dram__bytes|hit_rate|time_duration" gpurun_out/hot_$hot.csv | awk -F'","' '{print $(NF-2), $(NF-1), $NF}' >> gpurun_out/hot.log
 done
 cat gpurun_out/hot.log
-for i in 1 2; do
-  BLRQR_ARENA_HOT=0 BLRQR_LIB=$PWD/tools/_tmp/libnofence.so timeout 300 python tools/repro_perm.py 30 2>&1 | tail -1
-  BLRQR_ARENA_HOT=0 timeout 300 python tools/repro_perm.py 30 2>&1 | tail -1
-done
